@@ -1,0 +1,150 @@
+"""The oracle's backbone: a Qwen3-like GQA transformer (SURVEY c.1, reading A-M1).
+
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
+
+PAPER.md does not give the backbone (it evaluates SDAR, continually pre-trained
+from an AR LLM).  Reading A-M1: pre-RMSNorm blocks,
+q = h Wq^T, k = h Wk^T, v = h Wv^T, rotate-half RoPE on q and k at absolute
+positions, GQA (q-head h uses kv-head floor(h/G)), x += attn(...) Wo^T,
+x += (silu(h Wg^T) * (h Wu^T)) Wd^T, untied LM head, mask id = V-1 excluded
+from the logits.  Norm gains are 1.
+
+Two precisions:
+  mode="ref": binary64 throughout.
+  mode="gpu": binary64 arithmetic, but values are rounded at the GPU's storage
+              points: bf16 for GEMM inputs
+              (normed h, attention output, silu*mul), q and K/V; fp32 for the
+              residual stream and the logits.  Emulation by specification,
+              not shared code.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from synth.configs import ModelConfig
+from synth.gen import (TID_EMBED, TID_LMHEAD, layer_tid, weight_matrix)
+
+from .numerics import attend, bf16_round, f32, rms_norm, rope, silu
+
+
+class OracleWeights:
+    """Weights regenerated from the synth counter hash (exact bf16 values, held as float64).
+
+    Per-layer tensors are generated on first use; `cache=False` regenerates on every use
+    (bounded memory for 8B-shaped models)."""
+
+    def __init__(self, cfg: ModelConfig, seed: int = 0, cache: bool = True):
+        self.cfg, self.seed, self.cache = cfg, seed, cache
+        self._layers: dict[int, dict[str, np.ndarray]] = {}
+        self._lm: np.ndarray | None = None
+
+    def embed_rows(self, tokens) -> np.ndarray:
+        c = self.cfg
+        return np.stack([weight_matrix(TID_EMBED, c.vocab, c.d_model, c.d_model, self.seed, t, t + 1)[0]
+                         for t in np.asarray(tokens).tolist()]).astype(np.float64) \
+            if len(tokens) else np.zeros((0, c.d_model))
+
+    def layer(self, l: int) -> dict[str, np.ndarray]:
+        if l in self._layers:
+            return self._layers[l]
+        c = self.cfg
+        d, hq, hkv, dh, ff = c.d_model, c.n_q_heads, c.n_kv_heads, c.head_dim, c.d_ff
+        w = {
+            "q": weight_matrix(layer_tid(l, "q"), hq * dh, d, d, self.seed),
+            "k": weight_matrix(layer_tid(l, "k"), hkv * dh, d, d, self.seed),
+            "v": weight_matrix(layer_tid(l, "v"), hkv * dh, d, d, self.seed),
+            "o": weight_matrix(layer_tid(l, "o"), d, hq * dh, hq * dh, self.seed),
+            "gate": weight_matrix(layer_tid(l, "gate"), ff, d, d, self.seed),
+            "up": weight_matrix(layer_tid(l, "up"), ff, d, d, self.seed),
+            "down": weight_matrix(layer_tid(l, "down"), d, ff, ff, self.seed),
+        }
+        w = {k: v.astype(np.float64) for k, v in w.items()}
+        if self.cache:
+            self._layers[l] = w
+        return w
+
+    def lm_head(self) -> np.ndarray:
+        if self._lm is not None:
+            return self._lm
+        c = self.cfg
+        lm = weight_matrix(TID_LMHEAD, c.vocab, c.d_model, c.d_model, self.seed).astype(np.float64)
+        if self.cache:
+            self._lm = lm
+        return lm
+
+
+class Backbone:
+    """Layer pieces of the forward pass on a set of rows of ONE request."""
+
+    def __init__(self, cfg: ModelConfig, weights: OracleWeights, mode: str = "ref"):
+        assert mode in ("ref", "gpu")
+        self.cfg, self.w, self.mode = cfg, weights, mode
+
+    # storage-point rounding (identity in ref mode)
+    def _bf(self, x):
+        return bf16_round(x) if self.mode == "gpu" else np.asarray(x, dtype=np.float64)
+
+    def _f32(self, x):
+        return f32(x) if self.mode == "gpu" else np.asarray(x, dtype=np.float64)
+
+    def embed(self, tokens) -> np.ndarray:
+        """x_j = E[tok_j] (Alg.1 input "Masked Block X")."""
+        return self.w.embed_rows(tokens)
+
+    def qkv(self, l: int, x: np.ndarray, positions) -> tuple[np.ndarray, np.ndarray, np.ndarray]:
+        """RMSNorm, projections, RoPE at absolute positions.  Returns q [n,Hq,dh], k, v [n,Hkv,dh]."""
+        c, w = self.cfg, self.w.layer(l)
+        h = self._bf(rms_norm(x, 1.0, c.rms_eps))
+        n = h.shape[0]
+        q = (h @ w["q"].T).reshape(n, c.n_q_heads, c.head_dim)
+        k = (h @ w["k"].T).reshape(n, c.n_kv_heads, c.head_dim)
+        v = (h @ w["v"].T).reshape(n, c.n_kv_heads, c.head_dim)
+        q = self._bf(rope(self._f32(q), positions, c.rope_theta))
+        k = self._bf(rope(self._f32(k), positions, c.rope_theta))
+        v = self._bf(v)
+        return q, k, v
+
+    def attention(self, q: np.ndarray, K: np.ndarray, V: np.ndarray) -> np.ndarray:
+        """Each query row attends to ALL given keys (the caller builds the key set:
+        block-diffusion = context + block extent, bidirectional inside the block).
+        q [n,Hq,dh]; K, V [m,Hkv,dh] -> [n, Hq*dh]."""
+        c = self.cfg
+        out = np.empty((q.shape[0], c.n_q_heads, c.head_dim))
+        for h in range(c.n_q_heads):
+            g = h // c.group
+            out[:, h, :] = attend(q[:, h, :], K[:, g, :], V[:, g, :])
+        return self._bf(out.reshape(q.shape[0], -1))
+
+    def attention_causal(self, q: np.ndarray, K: np.ndarray, V: np.ndarray, first_pos: int) -> np.ndarray:
+        """Prefill: query row i (absolute position first_pos+i) attends to keys [0, first_pos+i]
+        (exact AR-style KV; reading A-K5)."""
+        c = self.cfg
+        out = np.empty((q.shape[0], c.n_q_heads, c.head_dim))
+        for i in range(q.shape[0]):
+            lim = first_pos + i + 1
+            for h in range(c.n_q_heads):
+                g = h // c.group
+                out[i, h, :] = attend(q[i:i + 1, h, :], K[:lim, g, :], V[:lim, g, :])[0]
+        return self._bf(out.reshape(q.shape[0], -1))
+
+    def o_proj(self, l: int, x: np.ndarray, o: np.ndarray) -> np.ndarray:
+        """x + o Wo^T (residual stream fp32 in gpu mode)."""
+        w = self.w.layer(l)
+        return self._f32(x + self._f32(o @ w["o"].T))
+
+    def mlp(self, l: int, x: np.ndarray) -> np.ndarray:
+        """x + (silu(h Wg^T) * h Wu^T) Wd^T with h = RMSNorm(x)."""
+        c, w = self.cfg, self.w.layer(l)
+        h = self._bf(rms_norm(x, 1.0, c.rms_eps))
+        g = self._f32(h @ w["gate"].T)
+        u = self._f32(h @ w["up"].T)
+        a = self._bf(silu(g) * u)
+        return self._f32(x + self._f32(a @ w["down"].T))
+
+    def logits(self, x: np.ndarray) -> np.ndarray:
+        """z = RMSNorm(x) W_lm^T; z[mask id] = -inf (A-CF1)."""
+        c = self.cfg
+        h = self._bf(rms_norm(x, 1.0, c.rms_eps))
+        z = self._f32(h @ self.w.lm_head().T)
+        z[:, c.mask_token_id] = -np.inf
+        return z
