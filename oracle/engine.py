@@ -223,9 +223,12 @@ class OracleEngine:
         if rec.flush:
             rec.S = list(rec.P)
         else:
-            dI = sc["dI"]
-            rec.I0 = np.zeros(B)
-            rec.I1 = np.array([dI.get(j, 0.0) for j in range(B)])
+            if "I0" in sc:                       # importance fed from elsewhere (parity protocol)
+                rec.I0, rec.I1 = np.asarray(sc["I0"]), np.asarray(sc["I1"])
+            else:
+                dI = sc["dI"]
+                rec.I0 = np.zeros(B)
+                rec.I1 = np.array([dI.get(j, 0.0) for j in range(B)])
             d = F.delta(rec.I0, rec.I1)
             rec.sel = F.select(d, rec.M, rec.U, st.committed, st.R, st.token_sum, st.total_steps, B,
                                m.alpha_num, m.alpha_den, m.placeholder_mode, m.strategy, m.fixed_k,

@@ -1,0 +1,137 @@
+// Internal declarations shared by the libfocus CUDA translation units (sm_100a only).
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "focus.h"
+
+typedef __nv_bfloat16 bf16;
+
+namespace focus {
+
+constexpr int kMaxB = 64;          // per-request masks are uint64 (focus.h)
+constexpr int kGuGroup = 128;      // gate/up rows interleaved in groups of 128 (Wgu layout)
+constexpr int kAttnQRows = 64;     // query rows (G x block rows) per attention CTA
+constexpr int kAttnKT = 32;        // keys per attention tile (SIMT path)
+
+// One processed / retained / logit row of the ragged batch.
+struct RowInfo {
+  int slot;   // request slot
+  int j;      // block position (-1 for prefill rows)
+  int pos;    // absolute position (RoPE angle, KV slot)
+  int ri;     // index of the request in the call's req list
+};
+
+struct Counters {
+  int M_P, M_S, M_L, invariant;
+  int pad[4];
+};
+
+struct VocabPartial {   // running (max, sum exp(x - max), argmax) of a vocab chunk
+  float m, s;
+  int idx, pad;
+};
+
+struct TokConf {
+  int tok;
+  float conf;
+};
+
+// Device pointers + geometry of the paged KV pool of one layer.
+struct KVView {
+  bf16* K;
+  bf16* V;
+  const int* page_table;   // [max_requests][max_pages]
+  int max_pages, page_size, n_kv_heads, head_dim;
+};
+
+__device__ __forceinline__ size_t kv_offset(const KVView& kv, int slot, int pos, int kvh) {
+  int page = kv.page_table[(size_t)slot * kv.max_pages + pos / kv.page_size];
+  int off = pos % kv.page_size;
+  return (((size_t)page * kv.n_kv_heads + kvh) * kv.page_size + off) * kv.head_dim;
+}
+
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+constexpr uint64_t kGolden = 0x9E3779B97F4A7C15ull;
+
+__host__ __device__ __forceinline__ uint64_t full_mask(int B) {
+  return B >= 64 ? ~0ull : ((1ull << B) - 1ull);
+}
+
+// ---------------------------------------------------------------- launchers (kernels_*.cu)
+void launch_init_weights(bf16* dst, int rows, int cols, uint64_t tid, uint64_t seed, int exp2,
+                         int gu_group, int gu_off, cudaStream_t st);
+
+void launch_step_setup(const int* req_list, int n_req, focus_req_state* st, int B, RowInfo* rowP,
+                       int* offP, int* tokP, Counters* cnt, cudaStream_t s);
+void launch_embed(const int* tok, const int* M_dev, int M_max, const bf16* E, int d, float* x,
+                  cudaStream_t s);
+void launch_rmsnorm(const float* x, const int* src_map, const int* M_dev, int M_max, int d, float eps,
+                    bf16* out, cudaStream_t s);
+void launch_rope_store(const float* qkv_f32, const RowInfo* rows, const int* M_dev, int M_max,
+                       int n_q_heads, const float* rope_cos, const float* rope_sin,
+                       const focus_req_state* st, KVView kv, bf16* qkv_out, Counters* cnt,
+                       cudaStream_t s);
+void launch_silu_mul(const float* gu, const int* M_dev, int M_max, int d_ff, bf16* act, cudaStream_t s);
+void launch_gather_rows(const float* x, const bf16* qkv, int qkv_dim, int q_dim, const int* src,
+                        const int* M_dev, int M_max, int d, float* x_out, bf16* q_out, cudaStream_t s);
+
+// GEMM: C[M x N] (fp32) = A[M x K] (bf16, row stride lda) . W[N x K]^T (bf16), store or accumulate.
+enum GemmMode { GEMM_STORE = 0, GEMM_ADD = 1 };
+void launch_gemm(const bf16* A, int lda, const bf16* W, int N, int K, float* C, int ldc,
+                 const int* M_dev, int M_max, GemmMode mode, cudaStream_t s);
+
+struct AttnArgs {
+  const bf16* q;  int ldq;      // query rows; head h at column h*head_dim
+  bf16* out;      int ldo;      // [rows][n_q_heads*head_dim] (nullptr in importance-only mode)
+  KVView kv;
+  const int* req_list;          // decode: request slots of the call
+  const int* row_off;           // decode: rows of list index i are [row_off[i], row_off[i+1])
+  const focus_req_state* st;
+  int n_req, B, n_q_heads;
+  int ext_mode;                 // 0: keys [0, s+B)  1: keys [0, s+R_new+1)  2: causal prefill
+  int imp_only;                 // 1: keys = block [s, s+B) only, no output (layer-1 importance)
+  int prefill_slot, prefill_pos0, prefill_rows;
+  float* imp;                   // [n_req][n_chunks][n_kv_heads][B] partial importance or nullptr
+  int n_chunks;                 // query-row chunks per request (decode)
+  int mp_kernel;                // MaxPool1D kernel (odd)
+  float scale;                  // 1/sqrt(head_dim)
+};
+void launch_attention(const AttnArgs& a, cudaStream_t s);
+
+struct SelectArgs {
+  const int* req_list; int n_req;
+  focus_req_state* st;
+  const float* I0p; const float* I1p; int n_parts;   // partial importance [n_req][n_parts][B]
+  int B, alpha_num, alpha_den, placeholder_mode, strategy, fixed_k;
+  uint64_t seed;
+  const int* offP;
+  RowInfo* rowS; int* srcP; int* offS;
+  RowInfo* rowL; int* srcL; int* offL;
+  Counters* cnt;
+};
+void launch_select_plan(const SelectArgs& a, cudaStream_t s);
+
+void launch_vocab_reduce(const float* logits, const int* M_dev, int M_max, int V, int mask_id, int nch,
+                         VocabPartial* part, cudaStream_t s);
+
+struct CommitArgs {
+  const int* req_list; int n_req;
+  focus_req_state* st;
+  const RowInfo* rowL; const int* offL;
+  const VocabPartial* part; int nch;
+  float tau;
+  int B, cache_mode, mask_id, max_gen;
+  int* out_tokens;              // [max_requests][max_gen]
+  TokConf* tokconf;             // [M_logit]
+  focus_commit_result* res;     // [n_req]
+  Counters* cnt;
+};
+void launch_commit(const CommitArgs& a, cudaStream_t s);
+
+}  // namespace focus

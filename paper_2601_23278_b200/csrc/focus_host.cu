@@ -1,0 +1,696 @@
+// libfocus host orchestration: config validation, arena carving, synthetic weights, page
+// allocator, the per-step kernel sequence and the C ABI of include/focus.h.
+//
+// The step (focus_step_block) is a fixed sequence of stream-ordered launches with no host sync and
+// no device->host copy; ragged sizes (M_P, M_S, M_logit) live in device counters and every kernel
+// reads them, so grids are sized by host-known upper bounds (n_req * B).
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "common.cuh"
+
+using namespace focus;
+
+namespace focus {
+void launch_gemm_simt(const bf16* A, int lda, const bf16* W, int N, int K, float* C, int ldc, const int* M_dev,
+                      int M_max, GemmMode mode, cudaStream_t s);
+bool launch_gemm_tc(const bf16* A, int lda, const bf16* W, int N, int K, float* C, int ldc, const int* M_dev,
+                    int M_max, GemmMode mode, cudaStream_t s);
+int gemm_backend();   // 0 = SIMT scaffolding, 1 = tcgen05
+
+void launch_gemm(const bf16* A, int lda, const bf16* W, int N, int K, float* C, int ldc, const int* M_dev,
+                 int M_max, GemmMode mode, cudaStream_t s) {
+  if (gemm_backend() == 1 && launch_gemm_tc(A, lda, W, N, K, C, ldc, M_dev, M_max, mode, s)) return;
+  launch_gemm_simt(A, lda, W, N, K, C, ldc, M_dev, M_max, mode, s);
+}
+}  // namespace focus
+
+namespace {
+
+constexpr int kTapCount = 10;
+enum { TAP_X_IN = 0, TAP_H, TAP_QKV, TAP_ATTN, TAP_X_MID, TAP_H2, TAP_ACT, TAP_X_OUT, TAP_QS, TAP_ROWS };
+
+struct Upload {                 // pinned staging ring for small host->device copies
+  char* host = nullptr;
+  size_t cap = 0, head = 0;
+  static constexpr int kSlots = 16;
+  cudaEvent_t ev[kSlots];
+  size_t slot_end[kSlots];
+  int next = 0;
+};
+
+int weight_exp(int fan_in) {
+  return -(int)std::ceil(std::log2(255.0 * std::sqrt((double)fan_in / 3.0)));
+}
+
+}  // namespace
+
+struct focus_ctx {
+  focus_config cfg;
+  cudaStream_t stream;
+  char* arena = nullptr;
+  size_t arena_bytes = 0;
+  // geometry
+  int B, G, qkv_dim, q_dim, max_rows, max_pages_per_req, n_chunks, nch_vocab, mask_id, max_gen;
+  size_t kv_layer_elems;
+  // weights
+  bf16* E = nullptr;
+  bf16* Wlm = nullptr;
+  std::vector<bf16*> Wqkv, Wo, Wgu, Wd;
+  // KV pool
+  bf16* Kpool = nullptr;
+  bf16* Vpool = nullptr;
+  float* rope_cos = nullptr;
+  float* rope_sin = nullptr;
+  int* page_table = nullptr;
+  focus_req_state* st = nullptr;
+  int* out_tokens = nullptr;
+  // workspace
+  float *x = nullptr, *x2 = nullptr, *f32tmp = nullptr, *logits = nullptr;
+  bf16 *h = nullptr, *qkv = nullptr, *qS = nullptr, *attn = nullptr, *act = nullptr;
+  RowInfo *rowP = nullptr, *rowS = nullptr, *rowL = nullptr;
+  int *offP = nullptr, *offS = nullptr, *offL = nullptr, *srcP = nullptr, *srcL = nullptr, *tokP = nullptr;
+  int* req_dev = nullptr;
+  Counters* cnt = nullptr;
+  float *I0p = nullptr, *I1p = nullptr;
+  VocabPartial* vpart = nullptr;
+  TokConf* tokconf = nullptr;
+  focus_commit_result* res_dev = nullptr;
+  void* taps[kTapCount] = {};
+  size_t tap_bytes[kTapCount] = {};
+  // host state
+  std::vector<int> slot_used;                 // 0 free, 1 allocated
+  std::vector<std::vector<int>> slot_pages;
+  std::vector<int> free_pages;
+  std::vector<int> last_list, pending_list;
+  bool step_pending = false;
+  int last_n_req = 0;
+  int tap_layer = -1;
+  Upload up;
+};
+
+namespace {
+
+focus_status cuda_status(cudaError_t e) {
+  if (e == cudaSuccess) return FOCUS_OK;
+  std::fprintf(stderr, "[focus] CUDA error: %s\n", cudaGetErrorString(e));
+  return FOCUS_ERR_CUDA;
+}
+
+bool valid_config(const focus_config& c) {
+  if (c.n_layers < 2 || c.d_model <= 0 || c.d_model % 64) return false;
+  if (c.n_q_heads <= 0 || c.n_kv_heads <= 0 || c.n_q_heads % c.n_kv_heads) return false;
+  if (!(c.head_dim == 16 || c.head_dim == 32 || c.head_dim == 64 || c.head_dim == 128)) return false;
+  if (c.d_ff <= 0 || c.d_ff % kGuGroup) return false;
+  if (c.vocab < 2) return false;
+  if (c.block_size < 1 || c.block_size > kMaxB) return false;
+  if (c.alpha_den <= 0 || c.alpha_num <= c.alpha_den) return false;       // alpha > 1
+  if (!(c.conf_threshold > 0.f && c.conf_threshold <= 1.f)) return false;
+  if (c.maxpool_kernel < 1 || c.maxpool_kernel % 2 == 0) return false;
+  if (c.cache_mode < 0 || c.cache_mode > 2 || c.placeholder_mode < 0 || c.placeholder_mode > 1) return false;
+  if (c.strategy < 0 || c.strategy > 4) return false;
+  if (c.strategy >= FOCUS_STRATEGY_FIXED_TOP && c.fixed_k < 1) return false;
+  if (c.max_requests < 1 || c.max_requests > 1024 || c.max_seq_len < 1 || c.page_size < 1) return false;
+  if (c.max_prefill_chunk < 1) return false;
+  const int G = c.n_q_heads / c.n_kv_heads;
+  if (G > kAttnQRows) return false;
+  if ((c.n_q_heads * c.head_dim) % 64) return false;
+  return true;
+}
+
+// Carve (or, with base == nullptr, size) the arena.  Returns bytes used.
+size_t carve(focus_ctx* x, char* base) {
+  const focus_config& c = x->cfg;
+  size_t off = 0;
+  auto take = [&](size_t bytes) -> char* {
+    off = (off + 255) & ~size_t(255);
+    char* p = base ? base + off : nullptr;
+    off += bytes;
+    return p;
+  };
+  const size_t d = c.d_model, ff = c.d_ff, V = c.vocab;
+  const size_t qkv = x->qkv_dim, qd = x->q_dim, L = c.n_layers;
+  x->E = (bf16*)take(V * d * 2);
+  x->Wlm = (bf16*)take(V * d * 2);
+  x->Wqkv.assign(L, nullptr); x->Wo.assign(L, nullptr); x->Wgu.assign(L, nullptr); x->Wd.assign(L, nullptr);
+  for (size_t l = 0; l < L; ++l) {
+    x->Wqkv[l] = (bf16*)take(qkv * d * 2);
+    x->Wo[l] = (bf16*)take(d * qd * 2);
+    x->Wgu[l] = (bf16*)take(2 * ff * d * 2);
+    x->Wd[l] = (bf16*)take(d * ff * 2);
+  }
+  x->Kpool = (bf16*)take(L * x->kv_layer_elems * 2);
+  x->Vpool = (bf16*)take(L * x->kv_layer_elems * 2);
+  const size_t half = c.head_dim / 2;
+  x->rope_cos = (float*)take((size_t)c.max_seq_len * half * 4);
+  x->rope_sin = (float*)take((size_t)c.max_seq_len * half * 4);
+  x->page_table = (int*)take((size_t)c.max_requests * x->max_pages_per_req * 4);
+  x->st = (focus_req_state*)take((size_t)c.max_requests * sizeof(focus_req_state));
+  x->out_tokens = (int*)take((size_t)c.max_requests * x->max_gen * 4);
+  const size_t R = x->max_rows;
+  x->x = (float*)take(R * d * 4);
+  x->x2 = (float*)take(R * d * 4);
+  x->f32tmp = (float*)take(R * std::max(qkv, 2 * ff) * 4);
+  x->h = (bf16*)take(R * std::max(d, ff) * 2);
+  x->qkv = (bf16*)take(R * qkv * 2);
+  x->qS = (bf16*)take(R * qd * 2);
+  x->attn = (bf16*)take(R * qd * 2);
+  x->act = (bf16*)take(R * ff * 2);
+  const size_t RL = (size_t)c.max_requests * x->B;   // logit rows <= retained masked rows
+  x->logits = (float*)take(RL * V * 4);
+  x->rowP = (RowInfo*)take(R * sizeof(RowInfo));
+  x->rowS = (RowInfo*)take(R * sizeof(RowInfo));
+  x->rowL = (RowInfo*)take(RL * sizeof(RowInfo));
+  x->offP = (int*)take((c.max_requests + 1) * 4);
+  x->offS = (int*)take((c.max_requests + 1) * 4);
+  x->offL = (int*)take((c.max_requests + 1) * 4);
+  x->srcP = (int*)take(R * 4);
+  x->srcL = (int*)take(RL * 4);
+  x->tokP = (int*)take(R * 4);
+  x->req_dev = (int*)take(c.max_requests * 4);
+  x->cnt = (Counters*)take(sizeof(Counters));
+  const size_t nparts = (size_t)x->n_chunks * c.n_kv_heads;
+  x->I0p = (float*)take(c.max_requests * nparts * x->B * 4);
+  x->I1p = (float*)take(c.max_requests * nparts * x->B * 4);
+  x->vpart = (VocabPartial*)take(RL * x->nch_vocab * sizeof(VocabPartial));
+  x->tokconf = (TokConf*)take(RL * sizeof(TokConf));
+  x->res_dev = (focus_commit_result*)take(c.max_requests * sizeof(focus_commit_result));
+  if (c.debug_taps) {
+    const size_t sz[kTapCount] = {R * d * 4, R * d * 2, R * qkv * 2, R * qd * 2, R * d * 4,
+                                  R * d * 2, R * ff * 2, R * d * 4, R * qd * 2, R * sizeof(RowInfo)};
+    for (int t = 0; t < kTapCount; ++t) {
+      x->taps[t] = take(sz[t]);
+      x->tap_bytes[t] = sz[t];
+    }
+  }
+  return off + 256;
+}
+
+void derive(focus_ctx* x) {
+  const focus_config& c = x->cfg;
+  x->B = c.block_size;
+  x->G = c.n_q_heads / c.n_kv_heads;
+  x->q_dim = c.n_q_heads * c.head_dim;
+  x->qkv_dim = (c.n_q_heads + 2 * c.n_kv_heads) * c.head_dim;
+  x->max_rows = std::max(c.max_requests * c.block_size, c.max_prefill_chunk);
+  x->max_pages_per_req = (c.max_seq_len + c.page_size - 1) / c.page_size;
+  const int64_t pages = c.kv_pages > 0 ? c.kv_pages : (int64_t)c.max_requests * x->max_pages_per_req;
+  x->kv_layer_elems = (size_t)pages * c.n_kv_heads * c.page_size * c.head_dim;
+  const int rpc = kAttnQRows / x->G;
+  x->n_chunks = (x->B + rpc - 1) / rpc;
+  x->nch_vocab = std::max(1, std::min(16, c.vocab / 8192));
+  x->mask_id = c.vocab - 1;
+  x->max_gen = c.max_seq_len;
+}
+
+KVView kv_view(focus_ctx* x, int layer) {
+  KVView v;
+  v.K = x->Kpool + (size_t)layer * x->kv_layer_elems;
+  v.V = x->Vpool + (size_t)layer * x->kv_layer_elems;
+  v.page_table = x->page_table;
+  v.max_pages = x->max_pages_per_req;
+  v.page_size = x->cfg.page_size;
+  v.n_kv_heads = x->cfg.n_kv_heads;
+  v.head_dim = x->cfg.head_dim;
+  return v;
+}
+
+// Stage `bytes` of host data in the pinned ring and copy them to `dst` on the stream.
+focus_status upload(focus_ctx* x, void* dst, const void* src, size_t bytes) {
+  Upload& u = x->up;
+  if (bytes > u.cap / Upload::kSlots) {           // large: synchronous copy
+    return cuda_status(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, x->stream)) == FOCUS_OK
+               ? cuda_status(cudaStreamSynchronize(x->stream)) : FOCUS_ERR_CUDA;
+  }
+  const int s = u.next;
+  u.next = (u.next + 1) % Upload::kSlots;
+  cudaEventSynchronize(u.ev[s]);                   // previous use of this slot finished
+  char* h = u.host + (size_t)s * (u.cap / Upload::kSlots);
+  std::memcpy(h, src, bytes);
+  cudaError_t e = cudaMemcpyAsync(dst, h, bytes, cudaMemcpyHostToDevice, x->stream);
+  cudaEventRecord(u.ev[s], x->stream);
+  return cuda_status(e);
+}
+
+void tap(focus_ctx* x, int layer, int which, const void* src, size_t bytes) {
+  if (!x->cfg.debug_taps || layer != x->tap_layer || !x->taps[which]) return;
+  cudaMemcpyAsync(x->taps[which], src, std::min(bytes, x->tap_bytes[which]), cudaMemcpyDeviceToDevice, x->stream);
+}
+
+// ---------------------------------------------------------------- one transformer layer, pieces
+struct RowSpace {             // the rows a layer piece runs on
+  const int* M_dev;           // device row count (nullptr: M_host exact)
+  int M_max;
+  const RowInfo* rows;
+};
+
+void qkv_piece(focus_ctx* x, int l, int tl, float* xr, const RowSpace& rs) {
+  const focus_config& c = x->cfg;
+  cudaStream_t s = x->stream;
+  tap(x, tl, TAP_X_IN, xr, (size_t)rs.M_max * c.d_model * 4);
+  launch_rmsnorm(xr, nullptr, rs.M_dev, rs.M_max, c.d_model, c.rms_eps, x->h, s);
+  tap(x, tl, TAP_H, x->h, (size_t)rs.M_max * c.d_model * 2);
+  launch_gemm(x->h, c.d_model, x->Wqkv[l], x->qkv_dim, c.d_model, x->f32tmp, x->qkv_dim, rs.M_dev, rs.M_max,
+              GEMM_STORE, s);
+  launch_rope_store(x->f32tmp, rs.rows, rs.M_dev, rs.M_max, c.n_q_heads, x->rope_cos, x->rope_sin, x->st,
+                    kv_view(x, l), x->qkv, x->cnt, s);
+  tap(x, tl, TAP_QKV, x->qkv, (size_t)rs.M_max * x->qkv_dim * 2);
+  tap(x, tl, TAP_ROWS, rs.rows, (size_t)rs.M_max * sizeof(RowInfo));
+}
+
+void out_mlp_piece(focus_ctx* x, int l, int tl, float* xr, const RowSpace& rs) {
+  const focus_config& c = x->cfg;
+  cudaStream_t s = x->stream;
+  tap(x, tl, TAP_ATTN, x->attn, (size_t)rs.M_max * x->q_dim * 2);
+  launch_gemm(x->attn, x->q_dim, x->Wo[l], c.d_model, x->q_dim, xr, c.d_model, rs.M_dev, rs.M_max, GEMM_ADD, s);
+  tap(x, tl, TAP_X_MID, xr, (size_t)rs.M_max * c.d_model * 4);
+  launch_rmsnorm(xr, nullptr, rs.M_dev, rs.M_max, c.d_model, c.rms_eps, x->h, s);
+  tap(x, tl, TAP_H2, x->h, (size_t)rs.M_max * c.d_model * 2);
+  launch_gemm(x->h, c.d_model, x->Wgu[l], 2 * c.d_ff, c.d_model, x->f32tmp, 2 * c.d_ff, rs.M_dev, rs.M_max,
+              GEMM_STORE, s);
+  launch_silu_mul(x->f32tmp, rs.M_dev, rs.M_max, c.d_ff, x->act, s);
+  tap(x, tl, TAP_ACT, x->act, (size_t)rs.M_max * c.d_ff * 2);
+  launch_gemm(x->act, c.d_ff, x->Wd[l], c.d_model, c.d_ff, xr, c.d_model, rs.M_dev, rs.M_max, GEMM_ADD, s);
+  tap(x, tl, TAP_X_OUT, xr, (size_t)rs.M_max * c.d_model * 4);
+}
+
+AttnArgs attn_args(focus_ctx* x, int l, const bf16* q, int ldq, int n_req, const int* row_off, int ext_mode) {
+  AttnArgs a{};
+  a.q = q;
+  a.ldq = ldq;
+  a.out = x->attn;
+  a.ldo = x->q_dim;
+  a.kv = kv_view(x, l);
+  a.req_list = x->req_dev;
+  a.row_off = row_off;
+  a.st = x->st;
+  a.n_req = n_req;
+  a.B = x->B;
+  a.n_q_heads = x->cfg.n_q_heads;
+  a.ext_mode = ext_mode;
+  a.n_chunks = x->n_chunks;
+  a.mp_kernel = x->cfg.maxpool_kernel;
+  a.scale = 1.0f / std::sqrt((float)x->cfg.head_dim);
+  return a;
+}
+
+}  // namespace
+
+// ======================================================================= C ABI
+extern "C" {
+
+const char* focus_status_str(focus_status s) {
+  switch (s) {
+    case FOCUS_OK: return "ok";
+    case FOCUS_ERR_CONFIG: return "invalid configuration";
+    case FOCUS_ERR_INVARIANT: return "device invariant violated";
+    case FOCUS_ERR_IO: return "host buffer error";
+    case FOCUS_ERR_NOMEM: return "out of memory (arena or KV pages)";
+    case FOCUS_ERR_STATE: return "invalid request state";
+    case FOCUS_ERR_CUDA: return "CUDA error";
+  }
+  return "unknown";
+}
+
+size_t focus_required_bytes(const focus_config* cfg) {
+  if (!cfg || !valid_config(*cfg)) return 0;
+  focus_ctx tmp;
+  tmp.cfg = *cfg;
+  derive(&tmp);
+  return carve(&tmp, nullptr);
+}
+
+focus_status focus_init(const focus_config* cfg, void* dev_arena, size_t arena_bytes, void* cuda_stream,
+                        focus_ctx** out) {
+  if (!cfg || !out || !valid_config(*cfg)) return FOCUS_ERR_CONFIG;
+  focus_ctx* x = new (std::nothrow) focus_ctx();
+  if (!x) return FOCUS_ERR_NOMEM;
+  x->cfg = *cfg;
+  derive(x);
+  const size_t need = carve(x, nullptr);
+  if (!dev_arena || arena_bytes < need) { delete x; return FOCUS_ERR_NOMEM; }
+  x->arena = (char*)dev_arena;
+  x->arena_bytes = arena_bytes;
+  carve(x, (char*)(((uintptr_t)dev_arena + 255) & ~uintptr_t(255)) - 0);
+  x->stream = (cudaStream_t)cuda_stream;
+  const focus_config& c = x->cfg;
+  cudaStream_t s = x->stream;
+  // pinned staging ring
+  x->up.cap = Upload::kSlots * 65536;
+  if (cudaMallocHost(&x->up.host, x->up.cap) != cudaSuccess) { delete x; return FOCUS_ERR_CUDA; }
+  for (int i = 0; i < Upload::kSlots; ++i) {
+    cudaEventCreateWithFlags(&x->up.ev[i], cudaEventDisableTiming);
+    cudaEventRecord(x->up.ev[i], s);
+  }
+  // synthetic weights (synth/gen.py recipe; tensor ids: E=1, W_lm=2, layer l: 16(l+1)+kind)
+  const uint64_t seed = c.weight_seed;
+  const int d = c.d_model, ff = c.d_ff, qd = x->q_dim, kd = c.n_kv_heads * c.head_dim;
+  launch_init_weights(x->E, c.vocab, d, 1, seed, weight_exp(d), 0, 0, s);
+  launch_init_weights(x->Wlm, c.vocab, d, 2, seed, weight_exp(d), 0, 0, s);
+  for (int l = 0; l < c.n_layers; ++l) {
+    const uint64_t t0 = 16ull * (l + 1);
+    launch_init_weights(x->Wqkv[l], qd, d, t0 + 0, seed, weight_exp(d), 0, 0, s);
+    launch_init_weights(x->Wqkv[l] + (size_t)qd * d, kd, d, t0 + 1, seed, weight_exp(d), 0, 0, s);
+    launch_init_weights(x->Wqkv[l] + (size_t)(qd + kd) * d, kd, d, t0 + 2, seed, weight_exp(d), 0, 0, s);
+    launch_init_weights(x->Wo[l], d, qd, t0 + 3, seed, weight_exp(qd), 0, 0, s);
+    launch_init_weights(x->Wgu[l], ff, d, t0 + 4, seed, weight_exp(d), kGuGroup, 0, s);
+    launch_init_weights(x->Wgu[l], ff, d, t0 + 5, seed, weight_exp(d), kGuGroup, 1, s);
+    launch_init_weights(x->Wd[l], d, ff, t0 + 6, seed, weight_exp(ff), 0, 0, s);
+  }
+  // RoPE table in binary64 on the host (angle pos * theta^(-2k/dh), rotate-half pairs)
+  {
+    const int half = c.head_dim / 2;
+    std::vector<float> cs((size_t)c.max_seq_len * half), sn(cs.size());
+    for (int p = 0; p < c.max_seq_len; ++p)
+      for (int k = 0; k < half; ++k) {
+        const double ang = (double)p * std::pow((double)c.rope_theta, -2.0 * k / c.head_dim);
+        cs[(size_t)p * half + k] = (float)std::cos(ang);
+        sn[(size_t)p * half + k] = (float)std::sin(ang);
+      }
+    cudaMemcpyAsync(x->rope_cos, cs.data(), cs.size() * 4, cudaMemcpyHostToDevice, s);
+    cudaMemcpyAsync(x->rope_sin, sn.data(), sn.size() * 4, cudaMemcpyHostToDevice, s);
+    cudaStreamSynchronize(s);
+  }
+  cudaMemsetAsync(x->st, 0, (size_t)c.max_requests * sizeof(focus_req_state), s);
+  cudaMemsetAsync(x->cnt, 0, sizeof(Counters), s);
+  cudaMemsetAsync(x->page_table, 0, (size_t)c.max_requests * x->max_pages_per_req * 4, s);
+  cudaMemsetAsync(x->out_tokens, 0, (size_t)c.max_requests * x->max_gen * 4, s);
+  x->slot_used.assign(c.max_requests, 0);
+  x->slot_pages.assign(c.max_requests, {});
+  const int64_t pages = x->kv_layer_elems / ((size_t)c.n_kv_heads * c.page_size * c.head_dim);
+  x->free_pages.reserve(pages);
+  for (int64_t p = pages - 1; p >= 0; --p) x->free_pages.push_back((int)p);
+  focus_status st = cuda_status(cudaStreamSynchronize(s));
+  if (st != FOCUS_OK) {
+    cudaFreeHost(x->up.host);
+    delete x;
+    return st;
+  }
+  *out = x;
+  return FOCUS_OK;
+}
+
+focus_status focus_destroy(focus_ctx* x) {
+  if (!x) return FOCUS_ERR_STATE;
+  cudaStreamSynchronize(x->stream);
+  for (int i = 0; i < Upload::kSlots; ++i) cudaEventDestroy(x->up.ev[i]);
+  cudaFreeHost(x->up.host);
+  delete x;
+  return FOCUS_OK;
+}
+
+focus_status focus_kv_append(focus_ctx* x, int32_t req_id, const int32_t* prompt, int32_t n_tokens, int32_t gen_len) {
+  if (!x) return FOCUS_ERR_STATE;
+  const focus_config& c = x->cfg;
+  if (x->step_pending) return FOCUS_ERR_STATE;
+  if (req_id < 0 || req_id >= c.max_requests || x->slot_used[req_id]) return FOCUS_ERR_STATE;
+  if (!prompt || n_tokens < 1 || gen_len < x->B || gen_len % x->B) return FOCUS_ERR_CONFIG;
+  if (n_tokens + gen_len > c.max_seq_len) return FOCUS_ERR_NOMEM;
+  for (int i = 0; i < n_tokens; ++i)
+    if (prompt[i] < 0 || prompt[i] >= c.vocab - 1) return FOCUS_ERR_CONFIG;
+  const int np = (n_tokens + gen_len + c.page_size - 1) / c.page_size;
+  if ((int)x->free_pages.size() < np) return FOCUS_ERR_NOMEM;
+  std::vector<int> pt(x->max_pages_per_req, 0);
+  for (int i = 0; i < np; ++i) {
+    pt[i] = x->free_pages.back();
+    x->free_pages.pop_back();
+    x->slot_pages[req_id].push_back(pt[i]);
+  }
+  x->slot_used[req_id] = 1;
+  cudaStream_t s = x->stream;
+  focus_status rc = upload(x, x->page_table + (size_t)req_id * x->max_pages_per_req, pt.data(), pt.size() * 4);
+  if (rc != FOCUS_OK) return rc;
+  // state: prefill is in progress (not active for steps yet)
+  focus_req_state st{};
+  st.active = 0;
+  st.s = n_tokens;
+  st.gen_len = gen_len;
+  st.prompt_len = n_tokens;
+  st.R = -1;
+  st.masked = full_mask(x->B);
+  for (int j = 0; j < kMaxB; ++j) { st.tok[j] = x->mask_id; st.dstep[j] = 0x7fffffff; }
+  rc = upload(x, x->st + req_id, &st, sizeof(st));
+  if (rc != FOCUS_OK) return rc;
+  // causal prefill in chunks
+  std::vector<RowInfo> rows;
+  for (int c0 = 0; c0 < n_tokens; c0 += c.max_prefill_chunk) {
+    const int n = std::min(c.max_prefill_chunk, n_tokens - c0);
+    rows.resize(n);
+    for (int i = 0; i < n; ++i) rows[i] = RowInfo{req_id, -1, c0 + i, 0};
+    if ((rc = upload(x, x->tokP, prompt + c0, (size_t)n * 4)) != FOCUS_OK) return rc;
+    if ((rc = upload(x, x->rowP, rows.data(), (size_t)n * sizeof(RowInfo))) != FOCUS_OK) return rc;
+    launch_embed(x->tokP, nullptr, n, x->E, c.d_model, x->x, s);
+    RowSpace rs{nullptr, n, x->rowP};
+    for (int l = 0; l < c.n_layers; ++l) {
+      qkv_piece(x, l, -1000, x->x, rs);
+      AttnArgs a = attn_args(x, l, x->qkv, x->qkv_dim, 0, nullptr, 2);
+      a.prefill_slot = req_id;
+      a.prefill_pos0 = c0;
+      a.prefill_rows = n;
+      launch_attention(a, s);
+      out_mlp_piece(x, l, -1000, x->x, rs);
+    }
+  }
+  // activate: the request takes part in steps from now on
+  st.active = 1;
+  rc = upload(x, x->st + req_id, &st, sizeof(st));
+  if (rc != FOCUS_OK) return rc;
+  return cuda_status(cudaStreamSynchronize(s));
+}
+
+focus_status focus_release(focus_ctx* x, int32_t req_id) {
+  if (!x) return FOCUS_ERR_STATE;
+  if (x->step_pending) return FOCUS_ERR_STATE;
+  if (req_id < 0 || req_id >= x->cfg.max_requests || !x->slot_used[req_id]) return FOCUS_ERR_STATE;
+  focus_status rc = cuda_status(cudaStreamSynchronize(x->stream));
+  if (rc != FOCUS_OK) return rc;
+  for (int p : x->slot_pages[req_id]) x->free_pages.push_back(p);
+  x->slot_pages[req_id].clear();
+  x->slot_used[req_id] = 0;
+  focus_req_state st{};
+  rc = upload(x, x->st + req_id, &st, sizeof(st));
+  if (rc != FOCUS_OK) return rc;
+  x->last_list.clear();
+  return cuda_status(cudaStreamSynchronize(x->stream));
+}
+
+static focus_status check_list(focus_ctx* x, const int32_t* ids, int32_t n) {
+  if (n < 0 || n > x->cfg.max_requests || (n > 0 && !ids)) return FOCUS_ERR_STATE;
+  std::vector<char> seen(x->cfg.max_requests, 0);
+  for (int i = 0; i < n; ++i) {
+    const int r = ids[i];
+    if (r < 0 || r >= x->cfg.max_requests || !x->slot_used[r] || seen[r]) return FOCUS_ERR_STATE;
+    seen[r] = 1;
+  }
+  return FOCUS_OK;
+}
+
+focus_status focus_step_block(focus_ctx* x, const int32_t* ids, int32_t n_req) {
+  if (!x) return FOCUS_ERR_STATE;
+  if (x->step_pending) return FOCUS_ERR_STATE;
+  focus_status rc = check_list(x, ids, n_req);
+  if (rc != FOCUS_OK) return rc;
+  x->pending_list.assign(ids, ids + n_req);
+  x->step_pending = true;
+  if (n_req == 0) return FOCUS_OK;
+  const focus_config& c = x->cfg;
+  cudaStream_t s = x->stream;
+  if (x->last_list != x->pending_list) {
+    if ((rc = upload(x, x->req_dev, ids, (size_t)n_req * 4)) != FOCUS_OK) return rc;
+    x->last_list = x->pending_list;
+  }
+  const int maxP = n_req * x->B;
+  // A0 setup, A1 embedding
+  launch_step_setup(x->req_dev, n_req, x->st, x->B, x->rowP, x->offP, x->tokP, x->cnt, s);
+  const int* MP = &x->cnt->M_P;
+  const int* MS = &x->cnt->M_S;
+  const int* ML = &x->cnt->M_L;
+  launch_embed(x->tokP, MP, maxP, x->E, c.d_model, x->x, s);
+  RowSpace rsP{MP, maxP, x->rowP};
+  RowSpace rsS{MS, maxP, x->rowS};
+  // A2 layer 0 fully on P (+ fused importance I0)
+  qkv_piece(x, 0, 0, x->x, rsP);
+  {
+    AttnArgs a = attn_args(x, 0, x->qkv, x->qkv_dim, n_req, x->offP, 0);
+    a.imp = x->I0p;
+    launch_attention(a, s);
+  }
+  out_mlp_piece(x, 0, 0, x->x, rsP);
+  // A3 layer-1 projections on P, K1/V1 stored before eviction, importance-only I1
+  qkv_piece(x, 1, 1, x->x, rsP);
+  {
+    AttnArgs a = attn_args(x, 1, x->qkv, x->qkv_dim, n_req, x->offP, 0);
+    a.imp = x->I1p;
+    a.imp_only = 1;
+    a.out = nullptr;
+    launch_attention(a, s);
+  }
+  // A4 selection + compaction plan, A5 gather
+  {
+    SelectArgs sa{};
+    sa.req_list = x->req_dev;
+    sa.n_req = n_req;
+    sa.st = x->st;
+    sa.I0p = x->I0p;
+    sa.I1p = x->I1p;
+    sa.n_parts = x->n_chunks * c.n_kv_heads;
+    sa.B = x->B;
+    sa.alpha_num = c.alpha_num;
+    sa.alpha_den = c.alpha_den;
+    sa.placeholder_mode = c.placeholder_mode;
+    sa.strategy = c.strategy;
+    sa.fixed_k = c.fixed_k;
+    sa.seed = c.weight_seed;
+    sa.offP = x->offP;
+    sa.rowS = x->rowS; sa.srcP = x->srcP; sa.offS = x->offS;
+    sa.rowL = x->rowL; sa.srcL = x->srcL; sa.offL = x->offL;
+    sa.cnt = x->cnt;
+    launch_select_plan(sa, s);
+  }
+  launch_gather_rows(x->x, x->qkv, x->qkv_dim, x->q_dim, x->srcP, MS, maxP, c.d_model, x->x2, x->qS, s);
+  tap(x, 1, TAP_QS, x->qS, (size_t)maxP * x->q_dim * 2);
+  // A6 layer-1 suffix on S: keys = context + whole block
+  {
+    AttnArgs a = attn_args(x, 1, x->qS, x->q_dim, n_req, x->offS, 0);
+    launch_attention(a, s);
+  }
+  out_mlp_piece(x, 1, 1, x->x2, rsS);
+  // A7 layers 2.. on S: keys = context + block [0, R']
+  for (int l = 2; l < c.n_layers; ++l) {
+    qkv_piece(x, l, l, x->x2, rsS);
+    AttnArgs a = attn_args(x, l, x->qkv, x->qkv_dim, n_req, x->offS, 1);
+    launch_attention(a, s);
+    out_mlp_piece(x, l, l, x->x2, rsS);
+  }
+  // A8 final norm + LM head on S cap M, vocab reduction
+  launch_rmsnorm(x->x2, x->srcL, ML, maxP, c.d_model, c.rms_eps, x->h, s);
+  launch_gemm(x->h, c.d_model, x->Wlm, c.vocab, c.d_model, x->logits, c.vocab, ML, maxP, GEMM_STORE, s);
+  launch_vocab_reduce(x->logits, ML, maxP, c.vocab, x->mask_id, x->nch_vocab, x->vpart, s);
+  return cuda_status(cudaGetLastError());
+}
+
+focus_status focus_commit(focus_ctx* x, const int32_t* ids, int32_t n_req, focus_commit_result* out) {
+  if (!x) return FOCUS_ERR_STATE;
+  if (!x->step_pending || n_req != (int)x->pending_list.size()) return FOCUS_ERR_STATE;
+  for (int i = 0; i < n_req; ++i)
+    if (!ids || ids[i] != x->pending_list[i]) return FOCUS_ERR_STATE;
+  x->step_pending = false;
+  if (n_req == 0) return FOCUS_OK;
+  CommitArgs a{};
+  a.req_list = x->req_dev;
+  a.n_req = n_req;
+  a.st = x->st;
+  a.rowL = x->rowL;
+  a.offL = x->offL;
+  a.part = x->vpart;
+  a.nch = x->nch_vocab;
+  a.tau = x->cfg.conf_threshold;
+  a.B = x->B;
+  a.cache_mode = x->cfg.cache_mode;
+  a.mask_id = x->mask_id;
+  a.max_gen = x->max_gen;
+  a.out_tokens = x->out_tokens;
+  a.tokconf = x->tokconf;
+  a.res = x->res_dev;
+  a.cnt = x->cnt;
+  launch_commit(a, x->stream);
+  if (out)
+    cudaMemcpyAsync(out, x->res_dev, (size_t)n_req * sizeof(focus_commit_result), cudaMemcpyDeviceToHost, x->stream);
+  return cuda_status(cudaGetLastError());
+}
+
+focus_status focus_sync(focus_ctx* x) {
+  if (!x) return FOCUS_ERR_STATE;
+  focus_status rc = cuda_status(cudaStreamSynchronize(x->stream));
+  if (rc != FOCUS_OK) return rc;
+  int inv = 0;
+  rc = cuda_status(cudaMemcpy(&inv, &x->cnt->invariant, 4, cudaMemcpyDeviceToHost));
+  if (rc != FOCUS_OK) return rc;
+  return inv ? FOCUS_ERR_INVARIANT : FOCUS_OK;
+}
+
+focus_status focus_get_tokens(focus_ctx* x, int32_t req_id, int32_t* out_host, int32_t cap, int32_t* n_out) {
+  if (!x || req_id < 0 || req_id >= x->cfg.max_requests || !x->slot_used[req_id]) return FOCUS_ERR_STATE;
+  if (!out_host || !n_out) return FOCUS_ERR_IO;
+  focus_status rc = cuda_status(cudaStreamSynchronize(x->stream));
+  if (rc != FOCUS_OK) return rc;
+  focus_req_state st;
+  rc = cuda_status(cudaMemcpy(&st, x->st + req_id, sizeof(st), cudaMemcpyDeviceToHost));
+  if (rc != FOCUS_OK) return rc;
+  const int n = std::min(cap, st.b * x->B);
+  rc = cuda_status(cudaMemcpy(out_host, x->out_tokens + (size_t)req_id * x->max_gen, (size_t)n * 4,
+                              cudaMemcpyDeviceToHost));
+  *n_out = n;
+  return rc;
+}
+
+focus_status focus_set_tap(focus_ctx* x, int32_t layer) {
+  if (!x) return FOCUS_ERR_STATE;
+  if (!x->cfg.debug_taps && layer >= 0) return FOCUS_ERR_CONFIG;
+  x->tap_layer = layer;
+  return FOCUS_OK;
+}
+
+focus_status focus_debug_export(focus_ctx* x, int32_t what, int32_t req_id, int32_t layer, void* dst, size_t cap,
+                                size_t* n_written) {
+  if (!x || !dst || !n_written) return FOCUS_ERR_IO;
+  focus_status rc = cuda_status(cudaStreamSynchronize(x->stream));
+  if (rc != FOCUS_OK) return rc;
+  const focus_config& c = x->cfg;
+  Counters cnt;
+  cudaMemcpy(&cnt, x->cnt, sizeof(cnt), cudaMemcpyDeviceToHost);
+  const int n_req = x->last_list.size();
+  const void* src = nullptr;
+  size_t bytes = 0;
+  switch (what) {
+    case FOCUS_DBG_STATE: src = x->st; bytes = (size_t)c.max_requests * sizeof(focus_req_state); break;
+    case FOCUS_DBG_COUNTERS: src = x->cnt; bytes = sizeof(Counters); break;
+    case FOCUS_DBG_ROWS_P: src = x->rowP; bytes = (size_t)cnt.M_P * sizeof(RowInfo); break;
+    case FOCUS_DBG_ROWS_S: src = x->rowS; bytes = (size_t)cnt.M_S * sizeof(RowInfo); break;
+    case FOCUS_DBG_ROWS_L: src = x->rowL; bytes = (size_t)cnt.M_L * sizeof(RowInfo); break;
+    case FOCUS_DBG_I0: src = x->I0p; bytes = (size_t)n_req * x->n_chunks * c.n_kv_heads * x->B * 4; break;
+    case FOCUS_DBG_I1: src = x->I1p; bytes = (size_t)n_req * x->n_chunks * c.n_kv_heads * x->B * 4; break;
+    case FOCUS_DBG_LOGITS: src = x->logits; bytes = (size_t)cnt.M_L * c.vocab * 4; break;
+    case FOCUS_DBG_TOKCONF: src = x->tokconf; bytes = (size_t)cnt.M_L * sizeof(TokConf); break;
+    case FOCUS_DBG_HL: src = x->h; bytes = (size_t)cnt.M_L * c.d_model * 2; break;
+    case FOCUS_DBG_KV_K:
+    case FOCUS_DBG_KV_V: {
+      if (req_id < 0 || req_id >= c.max_requests || !x->slot_used[req_id] || layer < 0 || layer >= c.n_layers)
+        return FOCUS_ERR_STATE;
+      focus_req_state st;
+      cudaMemcpy(&st, x->st + req_id, sizeof(st), cudaMemcpyDeviceToHost);
+      const int n = std::min(st.s + x->B, c.max_seq_len);
+      const size_t row = (size_t)c.n_kv_heads * c.head_dim;
+      if (cap < (size_t)n * row * 2) return FOCUS_ERR_IO;
+      const bf16* pool = (what == FOCUS_DBG_KV_K ? x->Kpool : x->Vpool) + (size_t)layer * x->kv_layer_elems;
+      char* out = (char*)dst;
+      const auto& pages = x->slot_pages[req_id];
+      for (int p = 0; p < n; ++p) {
+        const int page = pages[p / c.page_size], off = p % c.page_size;
+        for (int h = 0; h < c.n_kv_heads; ++h) {
+          const size_t e = (((size_t)page * c.n_kv_heads + h) * c.page_size + off) * c.head_dim;
+          cudaMemcpy(out + ((size_t)p * row + (size_t)h * c.head_dim) * 2, pool + e, (size_t)c.head_dim * 2,
+                     cudaMemcpyDeviceToHost);
+        }
+      }
+      *n_written = (size_t)n * row * 2;
+      return cuda_status(cudaGetLastError());
+    }
+    default: {
+      const int t = what - FOCUS_DBG_TAP_X_IN;
+      if (t < 0 || t >= kTapCount - 1 || !x->taps[t]) return FOCUS_ERR_IO;
+      src = x->taps[t];
+      bytes = x->tap_bytes[t];
+      if (t == TAP_QS) bytes = std::min(bytes, (size_t)cnt.M_S * x->q_dim * 2);
+    }
+  }
+  bytes = std::min(bytes, cap);
+  rc = cuda_status(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost));
+  *n_written = bytes;
+  return rc;
+}
+
+}  // extern "C"

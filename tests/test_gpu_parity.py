@@ -1,0 +1,208 @@
+"""GPU parity of the CUDA path (libfocus.so through the C ABI) against the CPU oracle.
+
+Bars (BASELINE.json north_star / DESIGN.md "numerics contract"):
+  - selection, compaction indices, committed token ids, decisions and state: bit-exact when the
+    oracle is fed the GPU's importance and confidence values;
+  - importance: per-element relative error <= 1e-3 (denominator floored at 1e-6 * |P| * Hq);
+  - attention output: relative L2 <= 1e-2 at bf16;
+  - confidence: |conf_gpu - conf_oracle| <= 1e-5 * conf_oracle, argmax token bit-exact;
+  - end-to-end committed tokens on the small config: >= 99 % agreement (free running).
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from oracle import focus as F
+from oracle.engine import OracleEngine, request_prompts, run_to_completion
+from synth import get_config
+from synth.configs import (CACHE_DC, CACHE_NONE, PLACEHOLDER_ALL_MASKED, STRATEGY_FIXED_BOTTOM,
+                           STRATEGY_FIXED_RANDOM, STRATEGY_FIXED_TOP, STRATEGY_NONE, MethodConfig, ModelConfig)
+
+from gpu_helpers import bits, gpu_importance_sums, oracle_state_from_gpu
+
+pytestmark = pytest.mark.gpu
+
+
+def _ctx(run, **kw):
+    from paper_2601_23278_b200 import FocusContext, make_config
+    return FocusContext(make_config(run, **kw))
+
+
+def _e2e(run):
+    from paper_2601_23278_b200.runner import generate, prefill_all
+    ctx = _ctx(run)
+    prompts = request_prompts(run)
+    rids = prefill_all(ctx, prompts, run.gen_len)
+    generate(ctx, rids, keep_log=False)
+    ctx.focus_sync()
+    eng, _ = run_to_completion(run, "gpu")
+    tot = agree = 0
+    for r in rids:
+        g, o = ctx.focus_get_tokens(r), eng.req[r].output
+        assert len(g) == run.gen_len
+        tot += len(o)
+        agree += sum(int(a == b) for a, b in zip(g, o))
+    return agree, tot, ctx
+
+
+def test_c1_end_to_end():
+    agree, tot, _ = _e2e(get_config("C1"))
+    assert agree >= 0.99 * tot, (agree, tot)
+
+
+@pytest.mark.parametrize("meth", [
+    MethodConfig(block_size=4),
+    MethodConfig(block_size=4, cache_mode=CACHE_DC),
+    MethodConfig(block_size=4, cache_mode=CACHE_NONE, strategy=STRATEGY_NONE),
+    MethodConfig(block_size=8, placeholder_mode=PLACEHOLDER_ALL_MASKED, alpha_num=6, alpha_den=5),
+    MethodConfig(block_size=8, strategy=STRATEGY_FIXED_TOP, fixed_k=2),
+    MethodConfig(block_size=8, strategy=STRATEGY_FIXED_BOTTOM, fixed_k=2),
+    MethodConfig(block_size=8, strategy=STRATEGY_FIXED_RANDOM, fixed_k=3),
+])
+def test_small_end_to_end_variants(meth):
+    run = get_config("C1").with_(method=meth, n_requests=4, gen_len=2 * meth.block_size)
+    agree, tot, ctx = _e2e(run)
+    assert agree >= 0.99 * tot, (agree, tot)
+    ctx.focus_sync()          # no invariant flag
+
+
+GQA_TINY = ModelConfig(n_layers=3, d_model=128, n_q_heads=8, n_kv_heads=2, head_dim=16, d_ff=256, vocab=61,
+                       rope_theta=1e4)
+
+
+@pytest.mark.parametrize("B,nreq,prompt", [(8, 6, 13), (16, 5, 40), (32, 3, 70), (64, 2, 9), (5, 7, 1)])
+def test_resynced_rules_bit_exact(B, nreq, prompt):
+    """Each step: the oracle is re-synced to the GPU state, fed the GPU's importance partial sums and
+    confidences, and must reproduce P/M, S, K, N_sigma, K_hist, R', the compaction row maps, the
+    decisions and the whole post-commit state bit for bit."""
+    run = get_config("C1").with_(model=GQA_TINY, method=MethodConfig(block_size=B), n_requests=nreq,
+                                 prompt_len=prompt, gen_len=2 * B, page_size=16)
+    ctx = _ctx(run)
+    prompts = request_prompts(run)
+    for r in range(nreq):
+        ctx.focus_kv_append(r, prompts[r], run.gen_len)
+    eng = OracleEngine(run, "gpu")
+    eng.script = {}
+    n_parts = ((B + (64 // GQA_TINY.group) - 1) // (64 // GQA_TINY.group)) * GQA_TINY.n_kv_heads
+    live = list(range(nreq))
+    steps = 0
+    while live:
+        pre = ctx.states()
+        ctx.focus_step_block(live)
+        ctx.focus_sync()
+        mid = ctx.states()
+        I0 = gpu_importance_sums(np.frombuffer(ctx.focus_debug_export("I0"), np.float32), len(live), n_parts, B)
+        I1 = gpu_importance_sums(np.frombuffer(ctx.focus_debug_export("I1"), np.float32), len(live), n_parts, B)
+        rowsS, rowsL = ctx.rows("S"), ctx.rows("L")
+        res = ctx.commit_results(live)
+        post = ctx.states()
+        tc = np.frombuffer(ctx.focus_debug_export("TOKCONF"), dtype=np.dtype([("tok", "<i4"), ("conf", "<f4")]))
+        logits = ctx.export_f32("LOGITS", (len(tc), run.model.vocab))
+        expS, expL = [], []
+        lrow = 0
+        for i, r in enumerate(live):
+            eng.req[r] = oracle_state_from_gpu(pre[r], r, B, prompt)
+            g = mid[r]
+            rec_pos = [j for j in range(B) if j not in eng.req[r].committed]
+            Mpos = [j for j in rec_pos if eng.req[r].dstep[j] is None]
+            # logit rows of this request (S cap M, ascending j) -> GPU conf / tok (fed to the oracle)
+            nl = bin(g.S & g.M).count("1")
+            conf = {int(rowsL[lrow + k][1]): float(tc["conf"][lrow + k]) for k in range(nl)}
+            tok = {int(rowsL[lrow + k][1]): int(tc["tok"][lrow + k]) for k in range(nl)}
+            # oracle's own confidence from the GPU's logits: argmax exact, conf within 1e-5
+            for k in range(nl):
+                z = logits[lrow + k].astype(np.float64).copy()
+                z[run.model.mask_token_id] = -np.inf
+                t_o, c_o = F.confidence(z)
+                assert t_o == tc["tok"][lrow + k]
+                assert abs(c_o - tc["conf"][lrow + k]) <= 1e-5 * c_o
+            lrow += nl
+            eng.script[(r, pre[r].t + 1)] = {"I0": I0[i].astype(np.float64), "I1": I1[i].astype(np.float64),
+                                             "conf": conf, "tok": tok}
+            rec = eng.step_one(r)
+            assert bits(g.P, B) == rec.P and bits(g.M, B) == Mpos == rec.M
+            assert bits(g.S, B) == rec.S, (steps, r)
+            assert g.R_new == rec.R_new
+            if not rec.flush:
+                assert (g.K, g.n_sigma, g.k_hist) == (rec.sel.K, rec.sel.n_sigma, rec.sel.k_hist)
+            com = eng.commit_one(r)
+            o = eng.req[r]
+            p = post[r]
+            assert res[i]["pos"] == com.decoded and res[i]["tok"] == com.tokens
+            assert bits(p.committed, B) == sorted(o.committed) or (com.block_done and p.committed == 0)
+            assert (p.R, p.token_sum, p.total_steps, p.s, p.b, bool(p.finished)) == \
+                (o.R, o.token_sum, o.total_steps, o.s, o.b, o.finished)
+            if not o.finished:
+                assert list(p.tok[:B]) == o.tok
+            expS += [(r, j) for j in rec.S]
+            expL += [(r, j) for j in rec.logit_rows]
+        assert [(int(a), int(b)) for a, b in rowsS[:, :2]] == expS          # compaction row maps
+        assert [(int(a), int(b)) for a, b in rowsL[:, :2]] == expL
+        live = [x["req_id"] for x in res if not x["finished"]]
+        steps += 1
+    ctx.focus_sync()
+    for r in range(nreq):
+        assert ctx.focus_get_tokens(r) == eng.req[r].output
+
+
+def test_determinism_and_batch_invariance():
+    from paper_2601_23278_b200.runner import generate, prefill_all
+    run = get_config("C1").with_(model=GQA_TINY, method=MethodConfig(block_size=8), n_requests=5, gen_len=16)
+    prompts = request_prompts(run)
+    outs = []
+    for _ in range(2):
+        ctx = _ctx(run)
+        rids = prefill_all(ctx, prompts, run.gen_len)
+        generate(ctx, rids, keep_log=False)
+        outs.append([ctx.focus_get_tokens(r) for r in rids])
+    assert outs[0] == outs[1]
+    ctx = _ctx(run)
+    ctx.focus_kv_append(3, prompts[3], run.gen_len)
+    generate(ctx, [3], keep_log=False)
+    assert ctx.focus_get_tokens(3) == outs[0][3]
+
+
+def test_prefill_kv_matches_dense_causal_recompute():
+    run = get_config("C1").with_(model=GQA_TINY, method=MethodConfig(block_size=8), n_requests=2, prompt_len=45,
+                                 gen_len=16, page_size=16)
+    ctx = _ctx(run, max_prefill_chunk=32)            # two prefill chunks
+    prompts = request_prompts(run)
+    ctx.focus_kv_append(1, prompts[1], run.gen_len)
+    eng = OracleEngine(run, "gpu")
+    eng.kv_append(1, prompts[1], run.gen_len)
+    m = run.model
+    for l in range(m.n_layers):
+        for what, ref in (("KV_K", eng.K[1][l]), ("KV_V", eng.V[1][l])):
+            g = ctx.export_bf16(what, (45 + 8, m.n_kv_heads, m.head_dim), req_id=1, layer=l)[:45]
+            want = ref[:45]
+            err = np.linalg.norm(g - want) / np.linalg.norm(want)
+            assert err < 1e-2, (l, what, err)
+            assert np.mean(g == want) > 0.9, (l, what)
+
+
+def test_committed_kv_slots_never_rewritten():
+    from paper_2601_23278_b200.runner import prefill_all
+    run = get_config("C1").with_(model=GQA_TINY, method=MethodConfig(block_size=8), n_requests=2, gen_len=16)
+    ctx = _ctx(run)
+    prompts = request_prompts(run)
+    prefill_all(ctx, prompts, run.gen_len)
+    m = run.model
+    n = run.prompt_len + run.gen_len
+    frozen = {}
+    live = [0, 1]
+    while live:
+        ctx.focus_step_block(live)
+        res = ctx.commit_results(live)
+        for r in live:
+            st = ctx.states()[r]
+            for l in range(m.n_layers):
+                K = ctx.export_bf16("KV_K", (min(st.s + 8, n), m.n_kv_heads, m.head_dim), req_id=r, layer=l)
+                for (rr, ll, p), v in frozen.items():
+                    if rr == r and ll == l:
+                        assert np.array_equal(K[p], v), (r, l, p)
+                for j in bits(st.committed, 8):
+                    frozen.setdefault((r, l, st.s + j), K[st.s + j].copy())
+                for p in range(run.prompt_len):
+                    frozen.setdefault((r, l, p), K[p].copy())
+        live = [x["req_id"] for x in res if not x["finished"]]
