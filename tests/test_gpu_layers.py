@@ -1,0 +1,130 @@
+"""Stage-wise parity of every kernel of the step at SDAR-8B / 1.7B layer shapes (fewer layers),
+through the tap buffers of the C ABI: the oracle is fed each stage's GPU input and compared with the
+stage's GPU output.  Shapes span several GEMM tiles with ragged M,
+several KV pages, GQA packing and block sizes 4/16."""
+import numpy as np
+import pytest
+
+from oracle import focus as F
+from oracle.model import OracleWeights
+from oracle.numerics import attend, bf16_round, f32, rms_norm, rope, silu
+from oracle.engine import request_prompts
+from synth import get_config
+from synth.configs import MethodConfig, ModelConfig
+from synth.gen import TID_LMHEAD, weight_matrix
+
+from gpu_helpers import bits, gpu_importance_sums, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+M8B4 = ModelConfig(n_layers=4, d_model=4096, n_q_heads=32, n_kv_heads=8, head_dim=128, d_ff=12288, vocab=151936,
+                   rope_theta=1e6)
+M1P7B3 = ModelConfig(n_layers=3, d_model=2048, n_q_heads=16, n_kv_heads=8, head_dim=128, d_ff=6144, vocab=151936,
+                     rope_theta=1e6)
+
+
+def _bf16_close(got, want, tag, frac=0.95, tol=4e-3):
+    assert rel_l2(got, want) < tol, (tag, rel_l2(got, want))
+    assert np.mean(got == want) > frac, (tag, np.mean(got == want))
+
+
+@pytest.mark.parametrize("model,B,nreq,prompt,taps", [(M8B4, 16, 3, 100, (0, 1, 3)), (M1P7B3, 4, 5, 70, (0, 1, 2))])
+def test_layer_stages(model, B, nreq, prompt, taps):
+    from paper_2601_23278_b200 import FocusContext, make_config
+    run = get_config("C3").with_(model=model, method=MethodConfig(block_size=B), n_requests=nreq, prompt_len=prompt,
+                                 gen_len=4 * B, page_size=64)
+    ctx = FocusContext(make_config(run, debug_taps=True))
+    prompts = request_prompts(run)
+    for r in range(nreq):
+        ctx.focus_kv_append(r, prompts[r], run.gen_len)
+    W = OracleWeights(model, run.weight_seed)
+    d, qd, hq, hkv, dh, G = model.d_model, model.n_q_heads * model.head_dim, model.n_q_heads, model.n_kv_heads, \
+        model.head_dim, model.group
+    live = list(range(nreq))
+    ctx.focus_step_block(live)                     # one untapped step so U / committed sets are non-trivial
+    ctx.commit_results(live)
+    n_parts = ((B + 64 // G - 1) // (64 // G)) * hkv
+    for l in taps:
+        ctx.focus_set_tap(l)
+        pre = ctx.states()
+        ctx.focus_step_block(live)
+        ctx.focus_sync()
+        st = ctx.states()
+        cnt = ctx.counters()
+        MP, MS, ML = int(cnt[0]), int(cnt[1]), int(cnt[2])
+        rowsP, rowsS, rowsL = ctx.rows("P"), ctx.rows("S"), ctx.rows("L")
+        Mq = MP if l <= 1 else MS
+        rows_q = rowsP if l <= 1 else rowsS
+        Ma = MP if l == 0 else MS
+        rows_a = rowsP if l == 0 else rowsS
+        w = W.layer(l)
+        x_in = ctx.export_f32("TAP_X_IN", (Mq, d)).astype(np.float64)
+        h = ctx.export_bf16("TAP_H", (Mq, d))
+        _bf16_close(h, bf16_round(rms_norm(x_in, 1.0, model.rms_eps)), ("rmsnorm", l), frac=0.99)
+        qkv = ctx.export_bf16("TAP_QKV", (Mq, (hq + 2 * hkv) * dh))
+        pos = rows_q[:, 2]
+        y = f32(h @ np.concatenate([w["q"], w["k"], w["v"]]).T)
+        q_o = bf16_round(rope(f32(y[:, :qd].reshape(Mq, hq, dh)), pos, model.rope_theta)).reshape(Mq, -1)
+        k_o = bf16_round(rope(f32(y[:, qd:qd + hkv * dh].reshape(Mq, hkv, dh)), pos, model.rope_theta)).reshape(Mq, -1)
+        v_o = bf16_round(y[:, qd + hkv * dh:])
+        _bf16_close(qkv, np.concatenate([q_o, k_o, v_o], 1), ("qkv+rope", l))
+        # importance (layers 0, 1) from the GPU's q, k over P
+        if l <= 1:
+            Iraw = np.frombuffer(ctx.focus_debug_export("I0" if l == 0 else "I1"), np.float32)
+            Ig = gpu_importance_sums(Iraw, nreq, n_parts, B)
+            for i, r in enumerate(live):
+                s = st[r]
+                if s.flush:
+                    continue
+                P = bits(s.P, B)
+                qb = np.zeros((B, hq, dh)); kb = np.zeros((B, hkv, dh))
+                for n in range(Mq):
+                    if rows_q[n][0] == r:
+                        qb[rows_q[n][1]] = qkv[n, :qd].reshape(hq, dh)
+                        kb[rows_q[n][1]] = qkv[n, qd:qd + hkv * dh].reshape(hkv, dh)
+                Io = F.importance(qb, kb, P, G, 3)
+                floor = 1e-6 * len(P) * hq
+                err = np.abs(Ig[i][P] - Io[P]) / np.maximum(np.abs(Io[P]), floor)
+                assert err.max() <= 1e-3, (l, r, err.max())
+        # attention (queries: layer-1 uses the compacted q rows)
+        q_att = ctx.export_bf16("TAP_QS", (MS, qd)) if l == 1 else qkv[:, :qd]
+        att = ctx.export_bf16("TAP_ATTN", (Ma, qd))
+        ref = np.zeros_like(att)
+        for n in range(Ma):
+            r, j = int(rows_a[n][0]), int(rows_a[n][1])
+            s = st[r]
+            ext = B if l <= 1 else s.R_new + 1
+            nk = s.s + ext
+            K = ctx.export_bf16("KV_K", (s.s + B, hkv, dh), req_id=r, layer=l)[:nk]
+            V = ctx.export_bf16("KV_V", (s.s + B, hkv, dh), req_id=r, layer=l)[:nk]
+            qr = q_att[n].reshape(hq, dh)
+            ref[n] = np.concatenate([attend(qr[hh:hh + 1], K[:, hh // G], V[:, hh // G])[0] for hh in range(hq)])
+        assert rel_l2(att, ref) <= 1e-2, ("attention", l, rel_l2(att, ref))
+        # O projection + residual (layer 1: residual rows are the gathered P rows)
+        if l == 1:
+            idx = {(int(a), int(b)): n for n, (a, b, _, _) in enumerate(rowsP[:MP])}
+            x_res = np.stack([x_in[idx[(int(a), int(b))]] for a, b, _, _ in rowsS[:MS]])
+        else:
+            x_res = x_in
+        x_mid = ctx.export_f32("TAP_X_MID", (Ma, d)).astype(np.float64)
+        inc = att @ w["o"].T
+        assert rel_l2(x_mid - x_res, inc) < 1e-5, ("o-proj", l, rel_l2(x_mid - x_res, inc))
+        h2 = ctx.export_bf16("TAP_H2", (Ma, d))
+        _bf16_close(h2, bf16_round(rms_norm(x_mid, 1.0, model.rms_eps)), ("rmsnorm2", l), frac=0.99)
+        act = ctx.export_bf16("TAP_ACT", (Ma, model.d_ff))
+        _bf16_close(act, bf16_round(silu(f32(h2 @ w["gate"].T)) * f32(h2 @ w["up"].T)), ("swiglu", l))
+        x_out = ctx.export_f32("TAP_X_OUT", (Ma, d)).astype(np.float64)
+        inc = act @ w["down"].T
+        assert rel_l2(x_out - x_mid, inc) < 1e-5, ("down", l, rel_l2(x_out - x_mid, inc))
+        # LM head on S cap M rows (sampled vocab columns) after the last layer
+        if l == model.n_layers - 1 and ML:
+            hl = ctx.export_bf16("HL", (ML, d))
+            srcL = [int(np.flatnonzero((rowsS[:MS, 0] == a) & (rowsS[:MS, 1] == b))[0]) for a, b, _, _ in rowsL[:ML]]
+            _bf16_close(hl, bf16_round(rms_norm(x_out[srcL], 1.0, model.rms_eps)), "final-norm", frac=0.99)
+            logits = ctx.export_f32("LOGITS", (ML, model.vocab))
+            for lo in (0, model.vocab - 2048):
+                wl = weight_matrix(TID_LMHEAD, model.vocab, d, d, run.weight_seed, lo, lo + 2048).astype(np.float64)
+                assert rel_l2(logits[:, lo:lo + 2048], hl @ wl.T) < 1e-5, ("lm-head", lo)
+        ctx.commit_results(live)
+    ctx.focus_set_tap(-1)
+    ctx.focus_sync()
