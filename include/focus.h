@@ -155,8 +155,27 @@ enum {
   FOCUS_DBG_TAP_ACT = 26,   /* bf16[rows][d_ff] silu(gate)*up                                */
   FOCUS_DBG_TAP_X_OUT = 27, /* float[rows][d]   layer output                                 */
   FOCUS_DBG_TAP_QS = 28,    /* bf16[M_S][Hq dh] compacted layer-1 queries (tap layer 1)      */
-  FOCUS_DBG_HL = 29         /* bf16[M_logit][d] final-norm rows fed to the LM head           */
+  FOCUS_DBG_HL = 29,        /* bf16[M_logit][d] final-norm rows fed to the LM head           */
+  FOCUS_DBG_LAUNCHES = 30,  /* uint64: kernels launched by this context so far                */
+  FOCUS_DBG_PROFILE = 31    /* focus_prof_entry[FOCUS_PROF_KINDS] accumulated since the last
+                               focus_set_profile(ctx, 1)                                       */
 };
+
+/* Per-kernel-kind device time measured with CUDA events on the context stream around every launch
+ * while profiling is on (for the roofline report; adds event records between launches). */
+enum {
+  FOCUS_PROF_SETUP = 0, FOCUS_PROF_EMBED, FOCUS_PROF_RMSNORM, FOCUS_PROF_GEMM_QKV, FOCUS_PROF_ROPE_STORE,
+  FOCUS_PROF_ATTN, FOCUS_PROF_IMPORTANCE, FOCUS_PROF_GEMM_O, FOCUS_PROF_GEMM_GU, FOCUS_PROF_SILU,
+  FOCUS_PROF_GEMM_DOWN, FOCUS_PROF_SELECT, FOCUS_PROF_GATHER, FOCUS_PROF_GEMM_LM, FOCUS_PROF_VOCAB,
+  FOCUS_PROF_COMMIT, FOCUS_PROF_KINDS
+};
+typedef struct {
+  int32_t kind, launches;
+  float total_ms, max_ms;
+} focus_prof_entry;
+
+/* Enable (1) / disable (0) per-launch event timing; enabling resets the accumulators. */
+focus_status focus_set_profile(focus_ctx* ctx, int32_t on);
 
 /* Copy a debug view to host memory (synchronous).  *n_written = bytes copied. */
 focus_status focus_debug_export(focus_ctx* ctx, int32_t what, int32_t req_id, int32_t layer,

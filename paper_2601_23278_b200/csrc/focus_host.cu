@@ -90,6 +90,13 @@ struct focus_ctx {
   int last_n_req = 0;
   int tap_layer = -1;
   Upload up;
+  // launch accounting / profiling
+  uint64_t launches = 0;
+  bool prof_on = false;
+  std::vector<cudaEvent_t> prof_events;
+  size_t prof_used = 0;
+  std::vector<int> prof_kind;                    // per record
+  focus_prof_entry prof_acc[FOCUS_PROF_KINDS];
 };
 
 namespace {
@@ -218,6 +225,49 @@ KVView kv_view(focus_ctx* x, int layer) {
   return v;
 }
 
+int prof_begin(focus_ctx* x) {
+  if (!x->prof_on) return -1;
+  if (x->prof_used + 2 > x->prof_events.size()) {
+    for (int i = 0; i < 512; ++i) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      x->prof_events.push_back(e);
+    }
+  }
+  const int e0 = (int)x->prof_used;
+  x->prof_used += 2;
+  cudaEventRecord(x->prof_events[e0], x->stream);
+  return e0;
+}
+
+void prof_end(focus_ctx* x, int kind, int e0) {
+  ++x->launches;
+  if (e0 < 0) return;
+  cudaEventRecord(x->prof_events[e0 + 1], x->stream);
+  x->prof_kind.push_back(kind);
+}
+
+// Fold recorded event pairs into the per-kind accumulators (caller synchronised the stream).
+void prof_collect(focus_ctx* x) {
+  for (size_t r = 0; r < x->prof_kind.size(); ++r) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, x->prof_events[2 * r], x->prof_events[2 * r + 1]);
+    focus_prof_entry& e = x->prof_acc[x->prof_kind[r]];
+    e.launches += 1;
+    e.total_ms += ms;
+    e.max_ms = std::max(e.max_ms, ms);
+  }
+  x->prof_kind.clear();
+  x->prof_used = 0;
+}
+
+#define LAUNCH(kind, call)                  \
+  do {                                      \
+    const int e0_ = prof_begin(x);          \
+    call;                                   \
+    prof_end(x, FOCUS_PROF_##kind, e0_);    \
+  } while (0)
+
 // Stage `bytes` of host data in the pinned ring and copy them to `dst` on the stream.
 focus_status upload(focus_ctx* x, void* dst, const void* src, size_t bytes) {
   Upload& u = x->up;
@@ -251,12 +301,12 @@ void qkv_piece(focus_ctx* x, int l, int tl, float* xr, const RowSpace& rs) {
   const focus_config& c = x->cfg;
   cudaStream_t s = x->stream;
   tap(x, tl, TAP_X_IN, xr, (size_t)rs.M_max * c.d_model * 4);
-  launch_rmsnorm(xr, nullptr, rs.M_dev, rs.M_max, c.d_model, c.rms_eps, x->h, s);
+  LAUNCH(RMSNORM, launch_rmsnorm(xr, nullptr, rs.M_dev, rs.M_max, c.d_model, c.rms_eps, x->h, s));
   tap(x, tl, TAP_H, x->h, (size_t)rs.M_max * c.d_model * 2);
-  launch_gemm(x->h, c.d_model, x->Wqkv[l], x->qkv_dim, c.d_model, x->f32tmp, x->qkv_dim, rs.M_dev, rs.M_max,
-              GEMM_STORE, s);
-  launch_rope_store(x->f32tmp, rs.rows, rs.M_dev, rs.M_max, c.n_q_heads, x->rope_cos, x->rope_sin, x->st,
-                    kv_view(x, l), x->qkv, x->cnt, s);
+  LAUNCH(GEMM_QKV, launch_gemm(x->h, c.d_model, x->Wqkv[l], x->qkv_dim, c.d_model, x->f32tmp, x->qkv_dim, rs.M_dev,
+                               rs.M_max, GEMM_STORE, s));
+  LAUNCH(ROPE_STORE, launch_rope_store(x->f32tmp, rs.rows, rs.M_dev, rs.M_max, c.n_q_heads, x->rope_cos,
+                                       x->rope_sin, x->st, kv_view(x, l), x->qkv, x->cnt, s));
   tap(x, tl, TAP_QKV, x->qkv, (size_t)rs.M_max * x->qkv_dim * 2);
   tap(x, tl, TAP_ROWS, rs.rows, (size_t)rs.M_max * sizeof(RowInfo));
 }
@@ -265,15 +315,17 @@ void out_mlp_piece(focus_ctx* x, int l, int tl, float* xr, const RowSpace& rs) {
   const focus_config& c = x->cfg;
   cudaStream_t s = x->stream;
   tap(x, tl, TAP_ATTN, x->attn, (size_t)rs.M_max * x->q_dim * 2);
-  launch_gemm(x->attn, x->q_dim, x->Wo[l], c.d_model, x->q_dim, xr, c.d_model, rs.M_dev, rs.M_max, GEMM_ADD, s);
+  LAUNCH(GEMM_O, launch_gemm(x->attn, x->q_dim, x->Wo[l], c.d_model, x->q_dim, xr, c.d_model, rs.M_dev, rs.M_max,
+                             GEMM_ADD, s));
   tap(x, tl, TAP_X_MID, xr, (size_t)rs.M_max * c.d_model * 4);
-  launch_rmsnorm(xr, nullptr, rs.M_dev, rs.M_max, c.d_model, c.rms_eps, x->h, s);
+  LAUNCH(RMSNORM, launch_rmsnorm(xr, nullptr, rs.M_dev, rs.M_max, c.d_model, c.rms_eps, x->h, s));
   tap(x, tl, TAP_H2, x->h, (size_t)rs.M_max * c.d_model * 2);
-  launch_gemm(x->h, c.d_model, x->Wgu[l], 2 * c.d_ff, c.d_model, x->f32tmp, 2 * c.d_ff, rs.M_dev, rs.M_max,
-              GEMM_STORE, s);
-  launch_silu_mul(x->f32tmp, rs.M_dev, rs.M_max, c.d_ff, x->act, s);
+  LAUNCH(GEMM_GU, launch_gemm(x->h, c.d_model, x->Wgu[l], 2 * c.d_ff, c.d_model, x->f32tmp, 2 * c.d_ff, rs.M_dev,
+                              rs.M_max, GEMM_STORE, s));
+  LAUNCH(SILU, launch_silu_mul(x->f32tmp, rs.M_dev, rs.M_max, c.d_ff, x->act, s));
   tap(x, tl, TAP_ACT, x->act, (size_t)rs.M_max * c.d_ff * 2);
-  launch_gemm(x->act, c.d_ff, x->Wd[l], c.d_model, c.d_ff, xr, c.d_model, rs.M_dev, rs.M_max, GEMM_ADD, s);
+  LAUNCH(GEMM_DOWN, launch_gemm(x->act, c.d_ff, x->Wd[l], c.d_model, c.d_ff, xr, c.d_model, rs.M_dev, rs.M_max,
+                                GEMM_ADD, s));
   tap(x, tl, TAP_X_OUT, xr, (size_t)rs.M_max * c.d_model * 4);
 }
 
@@ -378,6 +430,7 @@ focus_status focus_init(const focus_config* cfg, void* dev_arena, size_t arena_b
   cudaMemsetAsync(x->cnt, 0, sizeof(Counters), s);
   cudaMemsetAsync(x->page_table, 0, (size_t)c.max_requests * x->max_pages_per_req * 4, s);
   cudaMemsetAsync(x->out_tokens, 0, (size_t)c.max_requests * x->max_gen * 4, s);
+  for (int k = 0; k < FOCUS_PROF_KINDS; ++k) x->prof_acc[k] = focus_prof_entry{k, 0, 0.f, 0.f};
   x->slot_used.assign(c.max_requests, 0);
   x->slot_pages.assign(c.max_requests, {});
   const int64_t pages = x->kv_layer_elems / ((size_t)c.n_kv_heads * c.page_size * c.head_dim);
@@ -397,6 +450,7 @@ focus_status focus_destroy(focus_ctx* x) {
   if (!x) return FOCUS_ERR_STATE;
   cudaStreamSynchronize(x->stream);
   for (int i = 0; i < Upload::kSlots; ++i) cudaEventDestroy(x->up.ev[i]);
+  for (cudaEvent_t e : x->prof_events) cudaEventDestroy(e);
   cudaFreeHost(x->up.host);
   delete x;
   return FOCUS_OK;
@@ -442,7 +496,7 @@ focus_status focus_kv_append(focus_ctx* x, int32_t req_id, const int32_t* prompt
     for (int i = 0; i < n; ++i) rows[i] = RowInfo{req_id, -1, c0 + i, 0};
     if ((rc = upload(x, x->tokP, prompt + c0, (size_t)n * 4)) != FOCUS_OK) return rc;
     if ((rc = upload(x, x->rowP, rows.data(), (size_t)n * sizeof(RowInfo))) != FOCUS_OK) return rc;
-    launch_embed(x->tokP, nullptr, n, x->E, c.d_model, x->x, s);
+    LAUNCH(EMBED, launch_embed(x->tokP, nullptr, n, x->E, c.d_model, x->x, s));
     RowSpace rs{nullptr, n, x->rowP};
     for (int l = 0; l < c.n_layers; ++l) {
       qkv_piece(x, l, -1000, x->x, rs);
@@ -450,7 +504,7 @@ focus_status focus_kv_append(focus_ctx* x, int32_t req_id, const int32_t* prompt
       a.prefill_slot = req_id;
       a.prefill_pos0 = c0;
       a.prefill_rows = n;
-      launch_attention(a, s);
+      LAUNCH(ATTN, launch_attention(a, s));
       out_mlp_piece(x, l, -1000, x->x, rs);
     }
   }
@@ -498,17 +552,16 @@ focus_status focus_step_block(focus_ctx* x, const int32_t* ids, int32_t n_req) {
   if (n_req == 0) return FOCUS_OK;
   const focus_config& c = x->cfg;
   cudaStream_t s = x->stream;
-  if (x->last_list != x->pending_list) {
-    if ((rc = upload(x, x->req_dev, ids, (size_t)n_req * 4)) != FOCUS_OK) return rc;
-    x->last_list = x->pending_list;
-  }
+  // the request list is uploaded every step (pinned staging, async): the step's host input
+  if ((rc = upload(x, x->req_dev, ids, (size_t)n_req * 4)) != FOCUS_OK) return rc;
+  x->last_list = x->pending_list;
   const int maxP = n_req * x->B;
   // A0 setup, A1 embedding
-  launch_step_setup(x->req_dev, n_req, x->st, x->B, x->rowP, x->offP, x->tokP, x->cnt, s);
+  LAUNCH(SETUP, launch_step_setup(x->req_dev, n_req, x->st, x->B, x->rowP, x->offP, x->tokP, x->cnt, s));
   const int* MP = &x->cnt->M_P;
   const int* MS = &x->cnt->M_S;
   const int* ML = &x->cnt->M_L;
-  launch_embed(x->tokP, MP, maxP, x->E, c.d_model, x->x, s);
+  LAUNCH(EMBED, launch_embed(x->tokP, MP, maxP, x->E, c.d_model, x->x, s));
   RowSpace rsP{MP, maxP, x->rowP};
   RowSpace rsS{MS, maxP, x->rowS};
   // A2 layer 0 fully on P (+ fused importance I0)
@@ -516,7 +569,7 @@ focus_status focus_step_block(focus_ctx* x, const int32_t* ids, int32_t n_req) {
   {
     AttnArgs a = attn_args(x, 0, x->qkv, x->qkv_dim, n_req, x->offP, 0);
     a.imp = x->I0p;
-    launch_attention(a, s);
+    LAUNCH(ATTN, launch_attention(a, s));
   }
   out_mlp_piece(x, 0, 0, x->x, rsP);
   // A3 layer-1 projections on P, K1/V1 stored before eviction, importance-only I1
@@ -526,7 +579,7 @@ focus_status focus_step_block(focus_ctx* x, const int32_t* ids, int32_t n_req) {
     a.imp = x->I1p;
     a.imp_only = 1;
     a.out = nullptr;
-    launch_attention(a, s);
+    LAUNCH(IMPORTANCE, launch_attention(a, s));
   }
   // A4 selection + compaction plan, A5 gather
   {
@@ -548,27 +601,27 @@ focus_status focus_step_block(focus_ctx* x, const int32_t* ids, int32_t n_req) {
     sa.rowS = x->rowS; sa.srcP = x->srcP; sa.offS = x->offS;
     sa.rowL = x->rowL; sa.srcL = x->srcL; sa.offL = x->offL;
     sa.cnt = x->cnt;
-    launch_select_plan(sa, s);
+    LAUNCH(SELECT, launch_select_plan(sa, s));
   }
-  launch_gather_rows(x->x, x->qkv, x->qkv_dim, x->q_dim, x->srcP, MS, maxP, c.d_model, x->x2, x->qS, s);
+  LAUNCH(GATHER, launch_gather_rows(x->x, x->qkv, x->qkv_dim, x->q_dim, x->srcP, MS, maxP, c.d_model, x->x2, x->qS, s));
   tap(x, 1, TAP_QS, x->qS, (size_t)maxP * x->q_dim * 2);
   // A6 layer-1 suffix on S: keys = context + whole block
   {
     AttnArgs a = attn_args(x, 1, x->qS, x->q_dim, n_req, x->offS, 0);
-    launch_attention(a, s);
+    LAUNCH(ATTN, launch_attention(a, s));
   }
   out_mlp_piece(x, 1, 1, x->x2, rsS);
   // A7 layers 2.. on S: keys = context + block [0, R']
   for (int l = 2; l < c.n_layers; ++l) {
     qkv_piece(x, l, l, x->x2, rsS);
     AttnArgs a = attn_args(x, l, x->qkv, x->qkv_dim, n_req, x->offS, 1);
-    launch_attention(a, s);
+    LAUNCH(ATTN, launch_attention(a, s));
     out_mlp_piece(x, l, l, x->x2, rsS);
   }
   // A8 final norm + LM head on S cap M, vocab reduction
-  launch_rmsnorm(x->x2, x->srcL, ML, maxP, c.d_model, c.rms_eps, x->h, s);
-  launch_gemm(x->h, c.d_model, x->Wlm, c.vocab, c.d_model, x->logits, c.vocab, ML, maxP, GEMM_STORE, s);
-  launch_vocab_reduce(x->logits, ML, maxP, c.vocab, x->mask_id, x->nch_vocab, x->vpart, s);
+  LAUNCH(RMSNORM, launch_rmsnorm(x->x2, x->srcL, ML, maxP, c.d_model, c.rms_eps, x->h, s));
+  LAUNCH(GEMM_LM, launch_gemm(x->h, c.d_model, x->Wlm, c.vocab, c.d_model, x->logits, c.vocab, ML, maxP, GEMM_STORE, s));
+  LAUNCH(VOCAB, launch_vocab_reduce(x->logits, ML, maxP, c.vocab, x->mask_id, x->nch_vocab, x->vpart, s));
   return cuda_status(cudaGetLastError());
 }
 
@@ -596,7 +649,7 @@ focus_status focus_commit(focus_ctx* x, const int32_t* ids, int32_t n_req, focus
   a.tokconf = x->tokconf;
   a.res = x->res_dev;
   a.cnt = x->cnt;
-  launch_commit(a, x->stream);
+  LAUNCH(COMMIT, launch_commit(a, x->stream));
   if (out)
     cudaMemcpyAsync(out, x->res_dev, (size_t)n_req * sizeof(focus_commit_result), cudaMemcpyDeviceToHost, x->stream);
   return cuda_status(cudaGetLastError());
@@ -625,6 +678,18 @@ focus_status focus_get_tokens(focus_ctx* x, int32_t req_id, int32_t* out_host, i
                               cudaMemcpyDeviceToHost));
   *n_out = n;
   return rc;
+}
+
+focus_status focus_set_profile(focus_ctx* x, int32_t on) {
+  if (!x) return FOCUS_ERR_STATE;
+  focus_status rc = cuda_status(cudaStreamSynchronize(x->stream));
+  if (rc != FOCUS_OK) return rc;
+  prof_collect(x);
+  if (on) {
+    for (int k = 0; k < FOCUS_PROF_KINDS; ++k) x->prof_acc[k] = focus_prof_entry{k, 0, 0.f, 0.f};
+  }
+  x->prof_on = on != 0;
+  return FOCUS_OK;
 }
 
 focus_status focus_set_tap(focus_ctx* x, int32_t layer) {
@@ -656,6 +721,19 @@ focus_status focus_debug_export(focus_ctx* x, int32_t what, int32_t req_id, int3
     case FOCUS_DBG_LOGITS: src = x->logits; bytes = (size_t)cnt.M_L * c.vocab * 4; break;
     case FOCUS_DBG_TOKCONF: src = x->tokconf; bytes = (size_t)cnt.M_L * sizeof(TokConf); break;
     case FOCUS_DBG_HL: src = x->h; bytes = (size_t)cnt.M_L * c.d_model * 2; break;
+    case FOCUS_DBG_LAUNCHES:
+      if (cap < 8) return FOCUS_ERR_IO;
+      std::memcpy(dst, &x->launches, 8);
+      *n_written = 8;
+      return FOCUS_OK;
+    case FOCUS_DBG_PROFILE: {
+      prof_collect(x);
+      const size_t nb = sizeof(x->prof_acc);
+      if (cap < nb) return FOCUS_ERR_IO;
+      std::memcpy(dst, x->prof_acc, nb);
+      *n_written = nb;
+      return FOCUS_OK;
+    }
     case FOCUS_DBG_KV_K:
     case FOCUS_DBG_KV_V: {
       if (req_id < 0 || req_id >= c.max_requests || !x->slot_used[req_id] || layer < 0 || layer >= c.n_layers)

@@ -21,11 +21,13 @@ FOCUS_ERR_NOMEM, FOCUS_ERR_STATE, FOCUS_ERR_CUDA = 5, 6, 7
 
 DBG = dict(STATE=1, COUNTERS=2, ROWS_P=3, ROWS_S=4, ROWS_L=5, I0=6, I1=7, LOGITS=8, TOKCONF=9, KV_K=10, KV_V=11,
            TAP_X_IN=20, TAP_H=21, TAP_QKV=22, TAP_ATTN=23, TAP_X_MID=24, TAP_H2=25, TAP_ACT=26, TAP_X_OUT=27,
-           TAP_QS=28, HL=29)
+           TAP_QS=28, HL=29, LAUNCHES=30, PROFILE=31)
+PROF_KINDS = ["setup", "embed", "rmsnorm", "gemm_qkv", "rope_store", "attention", "importance", "gemm_o",
+              "gemm_gu", "silu_mul", "gemm_down", "select", "gather", "gemm_lm", "vocab_reduce", "commit"]
 
 EXPORTED = ["focus_required_bytes", "focus_init", "focus_destroy", "focus_kv_append", "focus_step_block",
             "focus_commit", "focus_sync", "focus_get_tokens", "focus_release", "focus_set_tap",
-            "focus_debug_export", "focus_status_str"]
+            "focus_debug_export", "focus_status_str", "focus_set_profile"]
 
 
 class focus_config(C.Structure):
@@ -82,6 +84,7 @@ def _lib() -> C.CDLL:
         L.focus_get_tokens.argtypes = [C.c_void_p, C.c_int32, C.POINTER(C.c_int32), C.c_int32, C.POINTER(C.c_int32)]
         L.focus_release.argtypes = [C.c_void_p, C.c_int32]
         L.focus_set_tap.argtypes = [C.c_void_p, C.c_int32]
+        L.focus_set_profile.argtypes = [C.c_void_p, C.c_int32]
         L.focus_debug_export.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_size_t,
                                          C.POINTER(C.c_size_t)]
         L.focus_status_str.restype = C.c_char_p
@@ -172,6 +175,18 @@ class FocusContext:
 
     def focus_set_tap(self, layer: int):
         _check(_lib().focus_set_tap(self.h, layer), "focus_set_tap")
+
+    def focus_set_profile(self, on: bool):
+        _check(_lib().focus_set_profile(self.h, 1 if on else 0), "focus_set_profile")
+
+    def launches(self) -> int:
+        return int(np.frombuffer(self.focus_debug_export("LAUNCHES", cap=8), dtype=np.uint64)[0])
+
+    def profile(self) -> dict:
+        raw = self.focus_debug_export("PROFILE", cap=16 * len(PROF_KINDS))
+        a = np.frombuffer(raw, dtype=np.dtype([("kind", "<i4"), ("n", "<i4"), ("ms", "<f4"), ("max", "<f4")]))
+        return {PROF_KINDS[int(e["kind"])]: dict(launches=int(e["n"]), total_ms=float(e["ms"]), max_ms=float(e["max"]))
+                for e in a}
 
     def focus_debug_export(self, what, req_id: int = 0, layer: int = 0, cap: int = 1 << 31) -> bytes:
         code = DBG[what] if isinstance(what, str) else int(what)

@@ -60,15 +60,43 @@ def weight_scale_exp(fan_in: int) -> int:
     return -int(math.ceil(math.log2(255.0 * math.sqrt(fan_in / 3.0))))
 
 
-def weight_values(tid: int, start: int, count: int, fan_in: int, seed: int = 0) -> np.ndarray:
+_FAST = None
+
+
+def _fast():
+    """ctypes handle of synth/libsynthgen.so (same recipe in C + OpenMP), or None."""
+    global _FAST
+    if _FAST is None:
+        import ctypes
+        import os
+        path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsynthgen.so")
+        try:
+            if not os.path.exists(path):
+                from .build_gen import build
+                build()
+            lib = ctypes.CDLL(path)
+            lib.synth_weight_values.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
+                                                ctypes.c_uint64, ctypes.c_int]
+            _FAST = lib
+        except Exception:
+            _FAST = False
+    return _FAST or None
+
+
+def weight_values(tid: int, start: int, count: int, fan_in: int, seed: int = 0, fast: bool = True) -> np.ndarray:
     """Flat weight elements [start, start+count) of tensor `tid` as float32."""
+    lib = _fast() if fast else None
+    if lib is not None:
+        out = np.empty(count, dtype=np.float32)
+        lib.synth_weight_values(out.ctypes.data, tid, start, count, seed, weight_scale_exp(fan_in))
+        return out
     u = _stream(tid, start, count, seed)
     k = (u >> np.uint64(56)).astype(np.int32)
     return np.ldexp((2 * k - 255).astype(np.float32), weight_scale_exp(fan_in)).astype(np.float32)
 
 
 def weight_matrix(tid: int, rows: int, cols: int, fan_in: int, seed: int = 0,
-                  row_lo: int = 0, row_hi: int | None = None, chunk: int = 1 << 24) -> np.ndarray:
+                  row_lo: int = 0, row_hi: int | None = None, chunk: int = 1 << 28) -> np.ndarray:
     """Rows [row_lo, row_hi) of the logical [rows][cols] matrix, float32."""
     row_hi = rows if row_hi is None else row_hi
     n = (row_hi - row_lo) * cols
