@@ -83,8 +83,17 @@ void launch_gather_rows(const float* x, const bf16* qkv, int qkv_dim, int q_dim,
 
 // GEMM: C[M x N] (fp32) = A[M x K] (bf16, row stride lda) . W[N x K]^T (bf16), store or accumulate.
 enum GemmMode { GEMM_STORE = 0, GEMM_ADD = 1 };
-void launch_gemm(const bf16* A, int lda, const bf16* W, int N, int K, float* C, int ldc,
-                 const int* M_dev, int M_max, GemmMode mode, cudaStream_t s);
+struct GemmWs {                 // split-K partials + per-tile semaphores (carved from the arena)
+  float* ptr;
+  size_t bytes;
+  int* sem;
+  size_t sem_count;
+};
+// a_rows: allocated rows of A (TMA bounds); M_dev/M_max: live / maximum rows of this call.
+void launch_gemm(const bf16* A, int lda, int a_rows, const bf16* W, int N, int K, float* C, int ldc,
+                 const int* M_dev, int M_max, GemmMode mode, const GemmWs& ws, cudaStream_t s);
+int gemm_backend();
+void gemm_set_backend(int b);
 
 struct AttnArgs {
   const bf16* q;  int ldq;      // query rows; head h at column h*head_dim

@@ -17,13 +17,12 @@ using namespace focus;
 namespace focus {
 void launch_gemm_simt(const bf16* A, int lda, const bf16* W, int N, int K, float* C, int ldc, const int* M_dev,
                       int M_max, GemmMode mode, cudaStream_t s);
-bool launch_gemm_tc(const bf16* A, int lda, const bf16* W, int N, int K, float* C, int ldc, const int* M_dev,
-                    int M_max, GemmMode mode, cudaStream_t s);
-int gemm_backend();   // 0 = SIMT scaffolding, 1 = tcgen05
+bool launch_gemm_tc(const bf16* A, int lda, int a_rows, const bf16* W, int N, int K, float* C, int ldc,
+                    const int* M_dev, int M_max, GemmMode mode, const GemmWs& ws, cudaStream_t s);
 
-void launch_gemm(const bf16* A, int lda, const bf16* W, int N, int K, float* C, int ldc, const int* M_dev,
-                 int M_max, GemmMode mode, cudaStream_t s) {
-  if (gemm_backend() == 1 && launch_gemm_tc(A, lda, W, N, K, C, ldc, M_dev, M_max, mode, s)) return;
+void launch_gemm(const bf16* A, int lda, int a_rows, const bf16* W, int N, int K, float* C, int ldc, const int* M_dev,
+                 int M_max, GemmMode mode, const GemmWs& ws, cudaStream_t s) {
+  if (gemm_backend() == 1 && launch_gemm_tc(A, lda, a_rows, W, N, K, C, ldc, M_dev, M_max, mode, ws, s)) return;
   launch_gemm_simt(A, lda, W, N, K, C, ldc, M_dev, M_max, mode, s);
 }
 }  // namespace focus
@@ -79,6 +78,7 @@ struct focus_ctx {
   VocabPartial* vpart = nullptr;
   TokConf* tokconf = nullptr;
   focus_commit_result* res_dev = nullptr;
+  GemmWs gws{};
   void* taps[kTapCount] = {};
   size_t tap_bytes[kTapCount] = {};
   // host state
@@ -185,6 +185,10 @@ size_t carve(focus_ctx* x, char* base) {
   x->vpart = (VocabPartial*)take(RL * x->nch_vocab * sizeof(VocabPartial));
   x->tokconf = (TokConf*)take(RL * sizeof(TokConf));
   x->res_dev = (focus_commit_result*)take(c.max_requests * sizeof(focus_commit_result));
+  x->gws.bytes = (size_t)64 << 20;
+  x->gws.ptr = (float*)take(x->gws.bytes);
+  x->gws.sem_count = 4096;
+  x->gws.sem = (int*)take(x->gws.sem_count * 4);
   if (c.debug_taps) {
     const size_t sz[kTapCount] = {R * d * 4, R * d * 2, R * qkv * 2, R * qd * 2, R * d * 4,
                                   R * d * 2, R * ff * 2, R * d * 4, R * qd * 2, R * sizeof(RowInfo)};
@@ -303,8 +307,8 @@ void qkv_piece(focus_ctx* x, int l, int tl, float* xr, const RowSpace& rs) {
   tap(x, tl, TAP_X_IN, xr, (size_t)rs.M_max * c.d_model * 4);
   LAUNCH(RMSNORM, launch_rmsnorm(xr, nullptr, rs.M_dev, rs.M_max, c.d_model, c.rms_eps, x->h, s));
   tap(x, tl, TAP_H, x->h, (size_t)rs.M_max * c.d_model * 2);
-  LAUNCH(GEMM_QKV, launch_gemm(x->h, c.d_model, x->Wqkv[l], x->qkv_dim, c.d_model, x->f32tmp, x->qkv_dim, rs.M_dev,
-                               rs.M_max, GEMM_STORE, s));
+  LAUNCH(GEMM_QKV, launch_gemm(x->h, c.d_model, x->max_rows, x->Wqkv[l], x->qkv_dim, c.d_model, x->f32tmp,
+                               x->qkv_dim, rs.M_dev, rs.M_max, GEMM_STORE, x->gws, s));
   LAUNCH(ROPE_STORE, launch_rope_store(x->f32tmp, rs.rows, rs.M_dev, rs.M_max, c.n_q_heads, x->rope_cos,
                                        x->rope_sin, x->st, kv_view(x, l), x->qkv, x->cnt, s));
   tap(x, tl, TAP_QKV, x->qkv, (size_t)rs.M_max * x->qkv_dim * 2);
@@ -315,17 +319,17 @@ void out_mlp_piece(focus_ctx* x, int l, int tl, float* xr, const RowSpace& rs) {
   const focus_config& c = x->cfg;
   cudaStream_t s = x->stream;
   tap(x, tl, TAP_ATTN, x->attn, (size_t)rs.M_max * x->q_dim * 2);
-  LAUNCH(GEMM_O, launch_gemm(x->attn, x->q_dim, x->Wo[l], c.d_model, x->q_dim, xr, c.d_model, rs.M_dev, rs.M_max,
-                             GEMM_ADD, s));
+  LAUNCH(GEMM_O, launch_gemm(x->attn, x->q_dim, x->max_rows, x->Wo[l], c.d_model, x->q_dim, xr, c.d_model,
+                             rs.M_dev, rs.M_max, GEMM_ADD, x->gws, s));
   tap(x, tl, TAP_X_MID, xr, (size_t)rs.M_max * c.d_model * 4);
   LAUNCH(RMSNORM, launch_rmsnorm(xr, nullptr, rs.M_dev, rs.M_max, c.d_model, c.rms_eps, x->h, s));
   tap(x, tl, TAP_H2, x->h, (size_t)rs.M_max * c.d_model * 2);
-  LAUNCH(GEMM_GU, launch_gemm(x->h, c.d_model, x->Wgu[l], 2 * c.d_ff, c.d_model, x->f32tmp, 2 * c.d_ff, rs.M_dev,
-                              rs.M_max, GEMM_STORE, s));
+  LAUNCH(GEMM_GU, launch_gemm(x->h, c.d_model, x->max_rows, x->Wgu[l], 2 * c.d_ff, c.d_model, x->f32tmp,
+                              2 * c.d_ff, rs.M_dev, rs.M_max, GEMM_STORE, x->gws, s));
   LAUNCH(SILU, launch_silu_mul(x->f32tmp, rs.M_dev, rs.M_max, c.d_ff, x->act, s));
   tap(x, tl, TAP_ACT, x->act, (size_t)rs.M_max * c.d_ff * 2);
-  LAUNCH(GEMM_DOWN, launch_gemm(x->act, c.d_ff, x->Wd[l], c.d_model, c.d_ff, xr, c.d_model, rs.M_dev, rs.M_max,
-                                GEMM_ADD, s));
+  LAUNCH(GEMM_DOWN, launch_gemm(x->act, c.d_ff, x->max_rows, x->Wd[l], c.d_model, c.d_ff, xr, c.d_model, rs.M_dev,
+                                rs.M_max, GEMM_ADD, x->gws, s));
   tap(x, tl, TAP_X_OUT, xr, (size_t)rs.M_max * c.d_model * 4);
 }
 
@@ -428,6 +432,7 @@ focus_status focus_init(const focus_config* cfg, void* dev_arena, size_t arena_b
   }
   cudaMemsetAsync(x->st, 0, (size_t)c.max_requests * sizeof(focus_req_state), s);
   cudaMemsetAsync(x->cnt, 0, sizeof(Counters), s);
+  cudaMemsetAsync(x->gws.sem, 0, x->gws.sem_count * 4, s);
   cudaMemsetAsync(x->page_table, 0, (size_t)c.max_requests * x->max_pages_per_req * 4, s);
   cudaMemsetAsync(x->out_tokens, 0, (size_t)c.max_requests * x->max_gen * 4, s);
   for (int k = 0; k < FOCUS_PROF_KINDS; ++k) x->prof_acc[k] = focus_prof_entry{k, 0, 0.f, 0.f};
@@ -620,7 +625,8 @@ focus_status focus_step_block(focus_ctx* x, const int32_t* ids, int32_t n_req) {
   }
   // A8 final norm + LM head on S cap M, vocab reduction
   LAUNCH(RMSNORM, launch_rmsnorm(x->x2, x->srcL, ML, maxP, c.d_model, c.rms_eps, x->h, s));
-  LAUNCH(GEMM_LM, launch_gemm(x->h, c.d_model, x->Wlm, c.vocab, c.d_model, x->logits, c.vocab, ML, maxP, GEMM_STORE, s));
+  LAUNCH(GEMM_LM, launch_gemm(x->h, c.d_model, x->max_rows, x->Wlm, c.vocab, c.d_model, x->logits, c.vocab, ML, maxP,
+                              GEMM_STORE, x->gws, s));
   LAUNCH(VOCAB, launch_vocab_reduce(x->logits, ML, maxP, c.vocab, x->mask_id, x->nch_vocab, x->vpart, s));
   return cuda_status(cudaGetLastError());
 }

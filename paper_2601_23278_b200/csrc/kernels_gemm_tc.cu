@@ -1,12 +1,421 @@
-// tcgen05 / TMEM / TMA GEMM for sm_100a (placeholder until the tensor-core path lands).
+// tcgen05 / TMEM / TMA GEMM for sm_100a:  C[M x N] (fp32, store or +=) = A[M x K] . W[N x K]^T
+// A = activations (bf16, K-major rows), W = weights (bf16, [N][K] row-major = K-major).
+//
+// Persistent, warp-specialised (one CTA per SM, 256 threads):
+//   warp 0      TMA producer: A tile 128 x 64 and W tile 256 x 64 per stage (128B swizzle), 4 stages
+//   warp 1      MMA issuer: one elected thread issues tcgen05.mma.cta_group::1.kind::f16
+//               (M=128, N=256, K=16) x 4 per stage into a TMEM accumulator; tcgen05.commit releases
+//               the smem stage and, after the last k-block, signals the epilogue
+//   warp 2      TMEM allocator (512 columns = two 128 x 256 fp32 accumulators, double-buffered)
+//   warps 4..7  epilogue: tcgen05.ld 32x32b -> registers -> fp32 global (store / residual add)
+// Work units = (m tile, n tile, k split) with m fastest (CTAs sharing a weight tile run together and
+// hit L2).  M is read from device memory (ragged row counts of the FOCUS step) and the split-K factor
+// is chosen on device from the live tile count; split-K partials are reduced by the last-arriving
+// split in a fixed order (deterministic).
+#include <cuda.h>
+
+#include <mutex>
+#include <unordered_map>
+
 #include "common.cuh"
 
 namespace focus {
 
-int gemm_backend() { return 0; }
+namespace tc {
 
-bool launch_gemm_tc(const bf16*, int, const bf16*, int, int, float*, int, const int*, int, GemmMode, cudaStream_t) {
-  return false;
+constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
+constexpr int A_BYTES = BM * BK * 2;               // 16 KB
+constexpr int B_BYTES = BN * BK * 2;               // 32 KB
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;     // 48 KB
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int NUM_THREADS = 256;
+constexpr int TMEM_COLS = 512;
+constexpr int MAX_SPLIT = 4;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"((uint64_t)map), "r"(smem_u32(bar)), "r"(x), "r"(y)
+      : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// K-major operand, 128B swizzle: rows of 64 bf16 (128 B), 8-row core groups 1024 B apart.
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFFu) | (1ull << 16) | (64ull << 32) | (1ull << 46) | (2ull << 61);
+}
+
+__device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,"
+      "%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+struct Sched {
+  int m_tiles, n_tiles, split, kb_total, units;
+};
+
+// Same decision in every CTA: minimise waves x k-blocks per unit (+1 k-block of fix-up per extra split).
+__device__ __forceinline__ Sched make_sched(int M, int N, int K, int grid, int ws_tiles_cap) {
+  Sched s;
+  s.m_tiles = (M + BM - 1) / BM;
+  s.n_tiles = (N + BN - 1) / BN;
+  s.kb_total = K / BK;
+  const int tiles = s.m_tiles * s.n_tiles;
+  int best = 1;
+  long long best_cost = -1;
+  for (int sp = 1; sp <= MAX_SPLIT; ++sp) {
+    if (sp > 1 && (s.kb_total / sp < 4 || tiles * sp > ws_tiles_cap)) break;
+    const long long waves = (tiles * sp + grid - 1) / grid;
+    const long long cost = waves * ((s.kb_total + sp - 1) / sp + (sp > 1 ? 2 : 0));
+    if (best_cost < 0 || cost < best_cost) { best_cost = cost; best = sp; }
+  }
+  s.split = best;
+  s.units = tiles * best;
+  return s;
+}
+
+__device__ __forceinline__ void unit_coords(const Sched& s, int u, int& mt, int& nt, int& sp) {
+  mt = u % s.m_tiles;
+  const int r = u / s.m_tiles;
+  sp = r % s.split;
+  nt = r / s.split;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, float* __restrict__ C,
+              int ldc, int N, int K, const int* __restrict__ M_dev, int M_max, float* __restrict__ ws,
+              int* __restrict__ sem, int ws_tiles_cap) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sA = smem;                                   // STAGES x A_BYTES
+  uint8_t* sB = smem + STAGES * A_BYTES;                // STAGES x B_BYTES
+  uint64_t* bars = (uint64_t*)(smem + STAGES * STAGE_BYTES);
+  uint64_t* full = bars;                                // [STAGES]
+  uint64_t* empty = bars + STAGES;                      // [STAGES]
+  uint64_t* tfull = bars + 2 * STAGES;                  // [2]
+  uint64_t* tempty = bars + 2 * STAGES + 2;             // [2]
+  uint32_t* tmem_base_sh = (uint32_t*)(bars + 2 * STAGES + 4);
+  int* flag_sh = (int*)(tmem_base_sh + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int M = M_dev ? min(*M_dev, M_max) : M_max;
+  const Sched sc = make_sched(M, N, K, gridDim.x, ws_tiles_cap);
+
+  if (warp == 0 && lane == 0) {
+    for (int i = 0; i < STAGES; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 4); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&mapA) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&mapB) : "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_base_sh)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_base_sh;
+
+  if (warp == 0) {
+    // ---------------- TMA producer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = blockIdx.x; u < sc.units; u += gridDim.x) {
+        int mt, nt, sp;
+        unit_coords(sc, u, mt, nt, sp);
+        const int kb0 = sp * sc.kb_total / sc.split, kb1 = (sp + 1) * sc.kb_total / sc.split;
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], STAGE_BYTES);
+          tma_load_2d(sA + stage * A_BYTES, &mapA, &full[stage], kb * BK, mt * BM);
+          tma_load_2d(sB + stage * B_BYTES, &mapB, &full[stage], kb * BK, nt * BN);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer
+    if (lane == 0) {
+      const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int u = blockIdx.x; u < sc.units; u += gridDim.x, ++it) {
+        int mt, nt, sp;
+        unit_coords(sc, u, mt, nt, sp);
+        const int kb0 = sp * sc.kb_total / sc.split, kb1 = (sp + 1) * sc.kb_total / sc.split;
+        const int acc = it & 1;
+        mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + (uint32_t)(acc * BN);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sA + stage * A_BYTES), b0 = smem_u32(sB + stage * B_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)
+            mma_bf16(d, sw128_desc(a0 + k * 32), sw128_desc(b0 + k * 32), idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+          mma_commit(&empty[stage]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        mma_commit(&tfull[acc]);
+      }
+    }
+  } else if (warp >= 4) {
+    // ---------------- epilogue: warp q = warp-4 owns TMEM lanes [32q, 32q+32)
+    const int q = warp - 4;
+    const int et = threadIdx.x - 128;                   // 0..127
+    const bool vec_ok = (ldc % 4) == 0 && (((uintptr_t)C) & 15) == 0;
+    int it = 0;
+    for (int u = blockIdx.x; u < sc.units; u += gridDim.x, ++it) {
+      int mt, nt, sp;
+      unit_coords(sc, u, mt, nt, sp);
+      const int acc = it & 1;
+      mbar_wait(&tfull[acc], (it >> 1) & 1);
+      tc_fence_after();
+      const int row = mt * BM + q * 32 + lane;
+      const bool row_ok = row < M;
+      const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
+      const int tile = nt * sc.m_tiles + mt;
+      if (sc.split == 1) {
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+          float v[32];
+          tmem_ld32(taddr + c0, v);
+          const int n0 = nt * BN + c0;
+          if (row_ok) {
+            float* dst = C + (size_t)row * ldc + n0;
+            if (n0 + 32 <= N && vec_ok) {
+#pragma unroll
+              for (int i = 0; i < 32; i += 4) {
+                float4 o = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+                if (MODE == GEMM_ADD) {
+                  const float4 p = *reinterpret_cast<const float4*>(dst + i);
+                  o.x += p.x; o.y += p.y; o.z += p.z; o.w += p.w;
+                }
+                *reinterpret_cast<float4*>(dst + i) = o;
+              }
+            } else {
+              for (int i = 0; i < 32 && n0 + i < N; ++i) dst[i] = MODE == GEMM_ADD ? dst[i] + v[i] : v[i];
+            }
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+      } else {
+        // split-K: write the partial, last-arriving split reduces all partials in split order
+        float* my = ws + ((size_t)tile * sc.split + sp) * (BM * BN) + (size_t)(q * 32 + lane) * BN;
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+          float v[32];
+          tmem_ld32(taddr + c0, v);
+#pragma unroll
+          for (int i = 0; i < 32; i += 4)
+            __stcg(reinterpret_cast<float4*>(my + c0 + i), make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]));
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+        __threadfence();
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (et == 0) *flag_sh = atomicAdd(&sem[tile], 1);
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        const bool last = *flag_sh == sc.split - 1;
+        if (last) {
+          __threadfence();
+          const float* base = ws + (size_t)tile * sc.split * (BM * BN) + (size_t)(q * 32 + lane) * BN;
+          if (row_ok) {
+#pragma unroll 1
+            for (int c0 = 0; c0 < BN; c0 += 4) {
+              const int n0 = nt * BN + c0;
+              if (n0 >= N) break;
+              float4 s = __ldcg(reinterpret_cast<const float4*>(base + c0));
+              for (int p = 1; p < sc.split; ++p) {
+                const float4 t = __ldcg(reinterpret_cast<const float4*>(base + (size_t)p * (BM * BN) + c0));
+                s.x += t.x; s.y += t.y; s.z += t.z; s.w += t.w;
+              }
+              float* dst = C + (size_t)row * ldc + n0;
+              if (n0 + 4 <= N && vec_ok) {
+                if (MODE == GEMM_ADD) {
+                  const float4 p = *reinterpret_cast<const float4*>(dst);
+                  s.x += p.x; s.y += p.y; s.z += p.z; s.w += p.w;
+                }
+                *reinterpret_cast<float4*>(dst) = s;
+              } else {
+                const float sv[4] = {s.x, s.y, s.z, s.w};
+                for (int i = 0; i < 4 && n0 + i < N; ++i) dst[i] = MODE == GEMM_ADD ? dst[i] + sv[i] : sv[i];
+              }
+            }
+          }
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          if (et == 0) sem[tile] = 0;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+  }
+}
+
+// ---------------------------------------------------------------------------- host side
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiledFn)p;
+  });
+  return fn;
+}
+
+struct MapKey {
+  const void* p;
+  int rows, cols, ld, box_rows;
+  bool operator==(const MapKey& o) const {
+    return p == o.p && rows == o.rows && cols == o.cols && ld == o.ld && box_rows == o.box_rows;
+  }
+};
+struct MapKeyHash {
+  size_t operator()(const MapKey& k) const {
+    return std::hash<const void*>()(k.p) ^ ((size_t)k.rows * 1000003u) ^ ((size_t)k.cols * 7919u) ^
+           ((size_t)k.ld << 20) ^ (size_t)k.box_rows;
+  }
+};
+
+bool get_map(const void* ptr, int rows, int cols, int ld, int box_rows, CUtensorMap* out) {
+  static std::mutex mu;
+  static std::unordered_map<MapKey, CUtensorMap, MapKeyHash> cache;
+  std::lock_guard<std::mutex> g(mu);
+  const MapKey k{ptr, rows, cols, ld, box_rows};
+  auto it = cache.find(k);
+  if (it != cache.end()) { *out = it->second; return true; }
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return false;
+  CUtensorMap m;
+  const cuuint64_t gdim[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  const cuuint64_t gstride[1] = {(cuuint64_t)ld * 2};
+  const cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  if (enc(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), gdim, gstride, box, estr,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return false;
+  cache.emplace(k, m);
+  *out = m;
+  return true;
+}
+
+int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return n;
+}
+
+}  // namespace tc
+
+static int g_backend = -1;
+
+int gemm_backend() {
+  if (g_backend < 0) {
+    const char* e = getenv("FOCUS_GEMM");
+    g_backend = (e && e[0] == 's') ? 0 : 1;     // FOCUS_GEMM=simt forces the scaffolding path
+  }
+  return g_backend;
+}
+
+void gemm_set_backend(int b) { g_backend = b; }
+
+bool launch_gemm_tc(const bf16* A, int lda, int a_rows, const bf16* W, int N, int K, float* C, int ldc, const int* M_dev,
+                    int M_max, GemmMode mode, const GemmWs& ws, cudaStream_t s) {
+  using namespace tc;
+  if (M_max <= 0) return true;
+  if (K % BK || lda % 8 || a_rows < 1) return false;
+  CUtensorMap ma, mb;
+  if (!get_map(A, a_rows, K, lda, BM, &ma) || !get_map(W, N, K, K, BN, &mb)) return false;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_gemm_tc<GEMM_STORE>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    cudaFuncSetAttribute(k_gemm_tc<GEMM_ADD>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    attr = true;
+  }
+  const int max_units = ((M_max + BM - 1) / BM) * ((N + BN - 1) / BN) * MAX_SPLIT;
+  const int grid = std::max(1, std::min(num_sms(), max_units));
+  const int cap = (int)std::min<size_t>(ws.sem_count, ws.bytes / (sizeof(float) * BM * BN));
+  if (mode == GEMM_ADD)
+    k_gemm_tc<GEMM_ADD><<<grid, NUM_THREADS, SMEM_BYTES, s>>>(ma, mb, C, ldc, N, K, M_dev, M_max, ws.ptr, ws.sem, cap);
+  else
+    k_gemm_tc<GEMM_STORE><<<grid, NUM_THREADS, SMEM_BYTES, s>>>(ma, mb, C, ldc, N, K, M_dev, M_max, ws.ptr, ws.sem, cap);
+  return true;
 }
 
 }  // namespace focus
