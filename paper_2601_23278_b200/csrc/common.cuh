@@ -1,5 +1,6 @@
 // Internal declarations shared by the libfocus CUDA translation units (sm_100a only).
 #pragma once
+#include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -25,7 +26,9 @@ struct RowInfo {
 
 struct Counters {
   int M_P, M_S, M_L, invariant;
-  int pad[4];
+  int attn_rpc;     // query block rows per attention chunk (importance partials are per chunk)
+  int n_chunks;     // chunks per request (ceil(B / attn_rpc))
+  int pad[2];
 };
 
 struct VocabPartial {   // running (max, sum exp(x - max), argmax) of a vocab chunk
@@ -110,13 +113,25 @@ struct AttnArgs {
   int n_chunks;                 // query-row chunks per request (decode)
   int mp_kernel;                // MaxPool1D kernel (odd)
   float scale;                  // 1/sqrt(head_dim)
+  // tensor-core path (kernels_attn_tc.cu)
+  int layer;                    // pool layer (TMA row base = layer * kv_pages * n_kv_heads * page_size)
+  long long kv_pages;           // pages per layer
+  int split_tiles;              // 64-key tiles per key split (>= 2)
+  int max_nsplit;               // split slots per (request, chunk, kv head) in `part`
+  float* part;                  // split partials [pair][max_nsplit][128 * head_dim + 2 * 128]
+  int* sem;                     // per-pair arrival counters (zero between launches)
 };
 void launch_attention(const AttnArgs& a, cudaStream_t s);
+bool attn_tc_supported(int head_dim, int page_size);
+bool attn_tc_make_maps(const bf16* Kpool, const bf16* Vpool, size_t rows, int head_dim, int page_size,
+                       CUtensorMap* mk, CUtensorMap* mv);
+void launch_attention_tc(const CUtensorMap& mk, const CUtensorMap& mv, const AttnArgs& a, cudaStream_t s);
 
 struct SelectArgs {
   const int* req_list; int n_req;
   focus_req_state* st;
-  const float* I0p; const float* I1p; int n_parts;   // partial importance [n_req][n_parts][B]
+  const float* I0p; const float* I1p;                 // partial importance [n_req][n_chunks][n_kv_heads][B]
+  int n_chunks, n_kv_heads, attn_rpc;                 // chunk c of a request exists iff c * attn_rpc < |P|
   int B, alpha_num, alpha_den, placeholder_mode, strategy, fixed_k;
   uint64_t seed;
   const int* offP;

@@ -5,6 +5,7 @@
 // no device->host copy; ragged sizes (M_P, M_S, M_logit) live in device counters and every kernel
 // reads them, so grids are sized by host-known upper bounds (n_req * B).
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <new>
@@ -55,6 +56,13 @@ struct focus_ctx {
   // geometry
   int B, G, qkv_dim, q_dim, max_rows, max_pages_per_req, n_chunks, nch_vocab, mask_id, max_gen;
   size_t kv_layer_elems;
+  int64_t kv_pages;
+  // attention path: tcgen05 kernel (head_dim 64/128) or the SIMT kernel (other head dims)
+  bool attn_tc = false;
+  int attn_rpc = 0, split_tiles = 8, max_nsplit = 1;
+  CUtensorMap mapK, mapV;
+  float* attn_part = nullptr;
+  int* attn_sem = nullptr;
   // weights
   bf16* E = nullptr;
   bf16* Wlm = nullptr;
@@ -185,6 +193,11 @@ size_t carve(focus_ctx* x, char* base) {
   x->vpart = (VocabPartial*)take(RL * x->nch_vocab * sizeof(VocabPartial));
   x->tokconf = (TokConf*)take(RL * sizeof(TokConf));
   x->res_dev = (focus_commit_result*)take(c.max_requests * sizeof(focus_commit_result));
+  if (x->attn_tc) {
+    const size_t pairs = (size_t)c.max_requests * x->n_chunks * c.n_kv_heads;
+    x->attn_part = (float*)take(pairs * x->max_nsplit * ((size_t)128 * c.head_dim + 256) * 4);
+    x->attn_sem = (int*)take(pairs * 4);
+  }
   x->gws.bytes = (size_t)64 << 20;
   x->gws.ptr = (float*)take(x->gws.bytes);
   x->gws.sem_count = 4096;
@@ -209,9 +222,13 @@ void derive(focus_ctx* x) {
   x->max_rows = std::max(c.max_requests * c.block_size, c.max_prefill_chunk);
   x->max_pages_per_req = (c.max_seq_len + c.page_size - 1) / c.page_size;
   const int64_t pages = c.kv_pages > 0 ? c.kv_pages : (int64_t)c.max_requests * x->max_pages_per_req;
+  x->kv_pages = pages;
   x->kv_layer_elems = (size_t)pages * c.n_kv_heads * c.page_size * c.head_dim;
-  const int rpc = kAttnQRows / x->G;
-  x->n_chunks = (x->B + rpc - 1) / rpc;
+  x->attn_tc = attn_tc_supported(c.head_dim, c.page_size) && getenv("FOCUS_ATTN_SIMT") == nullptr;
+  x->attn_rpc = (x->attn_tc ? 128 : kAttnQRows) / x->G;
+  x->n_chunks = (x->B + x->attn_rpc - 1) / x->attn_rpc;
+  x->split_tiles = 8;
+  x->max_nsplit = ((c.max_seq_len + 63) / 64 + x->split_tiles - 1) / x->split_tiles + 1;
   x->nch_vocab = std::max(1, std::min(16, c.vocab / 8192));
   x->mask_id = c.vocab - 1;
   x->max_gen = c.max_seq_len;
@@ -350,7 +367,18 @@ AttnArgs attn_args(focus_ctx* x, int l, const bf16* q, int ldq, int n_req, const
   a.n_chunks = x->n_chunks;
   a.mp_kernel = x->cfg.maxpool_kernel;
   a.scale = 1.0f / std::sqrt((float)x->cfg.head_dim);
+  a.layer = l;
+  a.kv_pages = x->kv_pages;
+  a.split_tiles = x->split_tiles;
+  a.max_nsplit = x->max_nsplit;
+  a.part = x->attn_part;
+  a.sem = x->attn_sem;
   return a;
+}
+
+void run_attention(focus_ctx* x, const AttnArgs& a) {
+  if (x->attn_tc) launch_attention_tc(x->mapK, x->mapV, a, x->stream);
+  else launch_attention(a, x->stream);
 }
 
 }  // namespace
@@ -431,7 +459,25 @@ focus_status focus_init(const focus_config* cfg, void* dev_arena, size_t arena_b
     cudaStreamSynchronize(s);
   }
   cudaMemsetAsync(x->st, 0, (size_t)c.max_requests * sizeof(focus_req_state), s);
-  cudaMemsetAsync(x->cnt, 0, sizeof(Counters), s);
+  {
+    Counters c0{};
+    c0.attn_rpc = x->attn_rpc;
+    c0.n_chunks = x->n_chunks;
+    cudaMemcpyAsync(x->cnt, &c0, sizeof(c0), cudaMemcpyHostToDevice, s);
+  }
+  // KV pool zeroed once: key tiles past a request's written slots read finite zeros (P * V = 0)
+  cudaMemsetAsync(x->Kpool, 0, (size_t)c.n_layers * x->kv_layer_elems * 2, s);
+  cudaMemsetAsync(x->Vpool, 0, (size_t)c.n_layers * x->kv_layer_elems * 2, s);
+  if (x->attn_tc) {
+    cudaMemsetAsync(x->attn_sem, 0, (size_t)c.max_requests * x->n_chunks * c.n_kv_heads * 4, s);
+    const size_t rows = (size_t)c.n_layers * x->kv_pages * c.n_kv_heads * c.page_size;
+    if (!attn_tc_make_maps(x->Kpool, x->Vpool, rows, c.head_dim, c.page_size, &x->mapK, &x->mapV)) {
+      cudaStreamSynchronize(s);
+      cudaFreeHost(x->up.host);
+      delete x;
+      return FOCUS_ERR_CUDA;
+    }
+  }
   cudaMemsetAsync(x->gws.sem, 0, x->gws.sem_count * 4, s);
   cudaMemsetAsync(x->page_table, 0, (size_t)c.max_requests * x->max_pages_per_req * 4, s);
   cudaMemsetAsync(x->out_tokens, 0, (size_t)c.max_requests * x->max_gen * 4, s);
@@ -509,7 +555,7 @@ focus_status focus_kv_append(focus_ctx* x, int32_t req_id, const int32_t* prompt
       a.prefill_slot = req_id;
       a.prefill_pos0 = c0;
       a.prefill_rows = n;
-      LAUNCH(ATTN, launch_attention(a, s));
+      LAUNCH(ATTN, run_attention(x, a));
       out_mlp_piece(x, l, -1000, x->x, rs);
     }
   }
@@ -574,7 +620,7 @@ focus_status focus_step_block(focus_ctx* x, const int32_t* ids, int32_t n_req) {
   {
     AttnArgs a = attn_args(x, 0, x->qkv, x->qkv_dim, n_req, x->offP, 0);
     a.imp = x->I0p;
-    LAUNCH(ATTN, launch_attention(a, s));
+    LAUNCH(ATTN, run_attention(x, a));
   }
   out_mlp_piece(x, 0, 0, x->x, rsP);
   // A3 layer-1 projections on P, K1/V1 stored before eviction, importance-only I1
@@ -584,7 +630,7 @@ focus_status focus_step_block(focus_ctx* x, const int32_t* ids, int32_t n_req) {
     a.imp = x->I1p;
     a.imp_only = 1;
     a.out = nullptr;
-    LAUNCH(IMPORTANCE, launch_attention(a, s));
+    LAUNCH(IMPORTANCE, run_attention(x, a));
   }
   // A4 selection + compaction plan, A5 gather
   {
@@ -594,7 +640,9 @@ focus_status focus_step_block(focus_ctx* x, const int32_t* ids, int32_t n_req) {
     sa.st = x->st;
     sa.I0p = x->I0p;
     sa.I1p = x->I1p;
-    sa.n_parts = x->n_chunks * c.n_kv_heads;
+    sa.n_chunks = x->n_chunks;
+    sa.n_kv_heads = c.n_kv_heads;
+    sa.attn_rpc = x->attn_rpc;
     sa.B = x->B;
     sa.alpha_num = c.alpha_num;
     sa.alpha_den = c.alpha_den;
@@ -613,14 +661,14 @@ focus_status focus_step_block(focus_ctx* x, const int32_t* ids, int32_t n_req) {
   // A6 layer-1 suffix on S: keys = context + whole block
   {
     AttnArgs a = attn_args(x, 1, x->qS, x->q_dim, n_req, x->offS, 0);
-    LAUNCH(ATTN, launch_attention(a, s));
+    LAUNCH(ATTN, run_attention(x, a));
   }
   out_mlp_piece(x, 1, 1, x->x2, rsS);
   // A7 layers 2.. on S: keys = context + block [0, R']
   for (int l = 2; l < c.n_layers; ++l) {
     qkv_piece(x, l, l, x->x2, rsS);
     AttnArgs a = attn_args(x, l, x->qkv, x->qkv_dim, n_req, x->offS, 1);
-    LAUNCH(ATTN, launch_attention(a, s));
+    LAUNCH(ATTN, run_attention(x, a));
     out_mlp_piece(x, l, l, x->x2, rsS);
   }
   // A8 final norm + LM head on S cap M, vocab reduction

@@ -35,9 +35,12 @@ __global__ void __launch_bounds__(1024) k_select_plan(SelectArgs a) {
         const int j = lane + 32 * t;
         float i0 = 0.f, i1 = 0.f;
         if (j < B) {
-          for (int p = 0; p < a.n_parts; ++p) {
-            i0 = __fadd_rn(i0, a.I0p[((size_t)i * a.n_parts + p) * B + j]);
-            i1 = __fadd_rn(i1, a.I1p[((size_t)i * a.n_parts + p) * B + j]);
+          // partials of the chunks that hold rows (chunk-major, kv head minor), in that fixed order
+          const int n_parts = ((__popcll(P) + a.attn_rpc - 1) / a.attn_rpc) * a.n_kv_heads;
+          const size_t base = (size_t)i * a.n_chunks * a.n_kv_heads;
+          for (int p = 0; p < n_parts; ++p) {
+            i0 = __fadd_rn(i0, a.I0p[(base + p) * B + j]);
+            i1 = __fadd_rn(i1, a.I1p[(base + p) * B + j]);
           }
         }
         d[t] = __fsub_rn(i1, i0);

@@ -23,12 +23,17 @@ def oracle_state_from_gpu(g, rid: int, B: int, prompt_len: int) -> RequestState:
     return st
 
 
-def gpu_importance_sums(raw: np.ndarray, n_req: int, n_parts: int, B: int) -> np.ndarray:
-    """I_j = sum over partials in the GPU's fixed order, in fp32 (part of 'feed the GPU's I')."""
-    parts = raw.reshape(n_req, n_parts, B).astype(np.float32)
+def gpu_importance_sums(raw: np.ndarray, counters, P_masks, n_kv_heads: int, B: int) -> np.ndarray:
+    """I_j = sum over the request's partials (chunks that hold rows, kv heads) in the GPU's fixed
+    order, in fp32 (part of 'feed the GPU's I').  counters[4] = rows per chunk, counters[5] = chunks."""
+    rpc, n_chunks = int(counters[4]), int(counters[5])
+    n_req = len(P_masks)
+    parts = raw[: n_req * n_chunks * n_kv_heads * B].reshape(n_req, n_chunks * n_kv_heads, B).astype(np.float32)
     out = np.zeros((n_req, B), dtype=np.float32)
-    for p in range(n_parts):
-        out = (out + parts[:, p, :]).astype(np.float32)
+    for i, P in enumerate(P_masks):
+        n_parts = ((bin(int(P)).count("1") + rpc - 1) // rpc) * n_kv_heads
+        for p in range(n_parts):
+            out[i] = (out[i] + parts[i, p, :]).astype(np.float32)
     return out
 
 

@@ -21,6 +21,12 @@ M8B4 = ModelConfig(n_layers=4, d_model=4096, n_q_heads=32, n_kv_heads=8, head_di
                    rope_theta=1e6)
 M1P7B3 = ModelConfig(n_layers=3, d_model=2048, n_q_heads=16, n_kv_heads=8, head_dim=128, d_ff=6144, vocab=151936,
                      rope_theta=1e6)
+# small-width models with long contexts: several key splits per (request, kv head) in the tensor-core
+# attention (split merge), page sizes below / above the 64-key tile, head_dim 64 and 128, 2 query chunks
+MINI128 = ModelConfig(n_layers=3, d_model=512, n_q_heads=8, n_kv_heads=2, head_dim=128, d_ff=512, vocab=4096,
+                      rope_theta=1e6)
+MINI64 = ModelConfig(n_layers=3, d_model=512, n_q_heads=8, n_kv_heads=4, head_dim=64, d_ff=512, vocab=4096,
+                     rope_theta=1e6)
 
 
 def _bf16_close(got, want, tag, frac=0.95, tol=4e-3):
@@ -28,11 +34,17 @@ def _bf16_close(got, want, tag, frac=0.95, tol=4e-3):
     assert np.mean(got == want) > frac, (tag, np.mean(got == want))
 
 
-@pytest.mark.parametrize("model,B,nreq,prompt,taps", [(M8B4, 16, 3, 100, (0, 1, 3)), (M1P7B3, 4, 5, 70, (0, 1, 2))])
-def test_layer_stages(model, B, nreq, prompt, taps):
+@pytest.mark.parametrize("model,B,nreq,prompt,taps,page", [
+    (M8B4, 16, 3, 100, (0, 1, 3), 64),
+    (M1P7B3, 4, 5, 70, (0, 1, 2), 64),
+    (MINI128, 16, 3, 1100, (0, 1, 2), 16),
+    (MINI128, 64, 2, 700, (0, 1, 2), 32),
+    (MINI64, 32, 2, 1500, (0, 1, 2), 128),
+])
+def test_layer_stages(model, B, nreq, prompt, taps, page):
     from paper_2601_23278_b200 import FocusContext, make_config
     run = get_config("C3").with_(model=model, method=MethodConfig(block_size=B), n_requests=nreq, prompt_len=prompt,
-                                 gen_len=4 * B, page_size=64)
+                                 gen_len=4 * B, page_size=page)
     ctx = FocusContext(make_config(run, debug_taps=True))
     prompts = request_prompts(run)
     for r in range(nreq):
@@ -43,7 +55,6 @@ def test_layer_stages(model, B, nreq, prompt, taps):
     live = list(range(nreq))
     ctx.focus_step_block(live)                     # one untapped step so U / committed sets are non-trivial
     ctx.commit_results(live)
-    n_parts = ((B + 64 // G - 1) // (64 // G)) * hkv
     for l in taps:
         ctx.focus_set_tap(l)
         pre = ctx.states()
@@ -71,7 +82,7 @@ def test_layer_stages(model, B, nreq, prompt, taps):
         # importance (layers 0, 1) from the GPU's q, k over P
         if l <= 1:
             Iraw = np.frombuffer(ctx.focus_debug_export("I0" if l == 0 else "I1"), np.float32)
-            Ig = gpu_importance_sums(Iraw, nreq, n_parts, B)
+            Ig = gpu_importance_sums(Iraw, cnt, [st[r].P for r in live], hkv, B)
             for i, r in enumerate(live):
                 s = st[r]
                 if s.flush:

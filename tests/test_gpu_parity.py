@@ -69,14 +69,18 @@ def test_small_end_to_end_variants(meth):
 
 GQA_TINY = ModelConfig(n_layers=3, d_model=128, n_q_heads=8, n_kv_heads=2, head_dim=16, d_ff=256, vocab=61,
                        rope_theta=1e4)
+# head_dim 64: the tensor-core (tcgen05) attention path; GQA_TINY (head_dim 16) runs the SIMT one
+GQA_TC = ModelConfig(n_layers=3, d_model=256, n_q_heads=8, n_kv_heads=2, head_dim=64, d_ff=256, vocab=61,
+                     rope_theta=1e4)
 
 
+@pytest.mark.parametrize("model", [GQA_TINY, GQA_TC], ids=["simt", "tc"])
 @pytest.mark.parametrize("B,nreq,prompt", [(8, 6, 13), (16, 5, 40), (32, 3, 70), (64, 2, 9), (5, 7, 1)])
-def test_resynced_rules_bit_exact(B, nreq, prompt):
+def test_resynced_rules_bit_exact(B, nreq, prompt, model):
     """Each step: the oracle is re-synced to the GPU state, fed the GPU's importance partial sums and
     confidences, and must reproduce P/M, S, K, N_sigma, K_hist, R', the compaction row maps, the
     decisions and the whole post-commit state bit for bit."""
-    run = get_config("C1").with_(model=GQA_TINY, method=MethodConfig(block_size=B), n_requests=nreq,
+    run = get_config("C1").with_(model=model, method=MethodConfig(block_size=B), n_requests=nreq,
                                  prompt_len=prompt, gen_len=2 * B, page_size=16)
     ctx = _ctx(run)
     prompts = request_prompts(run)
@@ -84,7 +88,6 @@ def test_resynced_rules_bit_exact(B, nreq, prompt):
         ctx.focus_kv_append(r, prompts[r], run.gen_len)
     eng = OracleEngine(run, "gpu")
     eng.script = {}
-    n_parts = ((B + (64 // GQA_TINY.group) - 1) // (64 // GQA_TINY.group)) * GQA_TINY.n_kv_heads
     live = list(range(nreq))
     steps = 0
     outputs = {r: [] for r in range(nreq)}
@@ -93,8 +96,10 @@ def test_resynced_rules_bit_exact(B, nreq, prompt):
         ctx.focus_step_block(live)
         ctx.focus_sync()
         mid = ctx.states()
-        I0 = gpu_importance_sums(np.frombuffer(ctx.focus_debug_export("I0"), np.float32), len(live), n_parts, B)
-        I1 = gpu_importance_sums(np.frombuffer(ctx.focus_debug_export("I1"), np.float32), len(live), n_parts, B)
+        cnt = ctx.counters()
+        Pm = [mid[r].P for r in live]
+        I0 = gpu_importance_sums(np.frombuffer(ctx.focus_debug_export("I0"), np.float32), cnt, Pm, model.n_kv_heads, B)
+        I1 = gpu_importance_sums(np.frombuffer(ctx.focus_debug_export("I1"), np.float32), cnt, Pm, model.n_kv_heads, B)
         rowsS, rowsL = ctx.rows("S"), ctx.rows("L")
         res = ctx.commit_results(live)
         post = ctx.states()
@@ -148,9 +153,10 @@ def test_resynced_rules_bit_exact(B, nreq, prompt):
         assert ctx.focus_get_tokens(r) == outputs[r]
 
 
-def test_determinism_and_batch_invariance():
+@pytest.mark.parametrize("model", [GQA_TINY, GQA_TC], ids=["simt", "tc"])
+def test_determinism_and_batch_invariance(model):
     from paper_2601_23278_b200.runner import generate, prefill_all
-    run = get_config("C1").with_(model=GQA_TINY, method=MethodConfig(block_size=8), n_requests=5, gen_len=16)
+    run = get_config("C1").with_(model=model, method=MethodConfig(block_size=8), n_requests=5, gen_len=16)
     prompts = request_prompts(run)
     outs = []
     for _ in range(2):
@@ -165,8 +171,9 @@ def test_determinism_and_batch_invariance():
     assert ctx.focus_get_tokens(3) == outs[0][3]
 
 
-def test_prefill_kv_matches_dense_causal_recompute():
-    run = get_config("C1").with_(model=GQA_TINY, method=MethodConfig(block_size=8), n_requests=2, prompt_len=45,
+@pytest.mark.parametrize("model", [GQA_TINY, GQA_TC], ids=["simt", "tc"])
+def test_prefill_kv_matches_dense_causal_recompute(model):
+    run = get_config("C1").with_(model=model, method=MethodConfig(block_size=8), n_requests=2, prompt_len=45,
                                  gen_len=16, page_size=16)
     ctx = _ctx(run, max_prefill_chunk=32)            # two prefill chunks
     prompts = request_prompts(run)
@@ -184,9 +191,10 @@ def test_prefill_kv_matches_dense_causal_recompute():
                 assert np.mean(g == want) > 0.95, (l, what)
 
 
-def test_committed_kv_slots_never_rewritten():
+@pytest.mark.parametrize("model", [GQA_TINY, GQA_TC], ids=["simt", "tc"])
+def test_committed_kv_slots_never_rewritten(model):
     from paper_2601_23278_b200.runner import prefill_all
-    run = get_config("C1").with_(model=GQA_TINY, method=MethodConfig(block_size=8), n_requests=2, gen_len=16)
+    run = get_config("C1").with_(model=model, method=MethodConfig(block_size=8), n_requests=2, gen_len=16)
     ctx = _ctx(run)
     prompts = request_prompts(run)
     prefill_all(ctx, prompts, run.gen_len)
