@@ -157,8 +157,11 @@ enum {
   FOCUS_DBG_TAP_QS = 28,    /* bf16[M_S][Hq dh] compacted layer-1 queries (tap layer 1)      */
   FOCUS_DBG_HL = 29,        /* bf16[M_logit][d] final-norm rows fed to the LM head           */
   FOCUS_DBG_LAUNCHES = 30,  /* uint64: kernels launched by this context so far                */
-  FOCUS_DBG_PROFILE = 31    /* focus_prof_entry[FOCUS_PROF_KINDS] accumulated since the last
+  FOCUS_DBG_PROFILE = 31,   /* focus_prof_entry[FOCUS_PROF_KINDS] accumulated since the last
                                focus_set_profile(ctx, 1)                                       */
+  FOCUS_DBG_ATTN_TRACE = 32 /* uint64[grid][8 roles][512]: clock64 event trace of the last
+                               tensor-core attention launch of layer FOCUS_ATTN_TRACE_LAYER
+                               (env var read at focus_init; empty otherwise)                   */
 };
 
 /* Per-kernel-kind device time measured with CUDA events on the context stream around every launch

@@ -15,6 +15,7 @@ constexpr int kMaxB = 64;          // per-request masks are uint64 (focus.h)
 constexpr int kGuGroup = 128;      // gate/up rows interleaved in groups of 128 (Wgu layout)
 constexpr int kAttnQRows = 64;     // query rows (G x block rows) per attention CTA
 constexpr int kAttnKT = 32;        // keys per attention tile (SIMT path)
+constexpr int kTraceEv = 512;      // attention trace events per (CTA, role)
 
 // One processed / retained / logit row of the ragged batch.
 struct RowInfo {
@@ -96,6 +97,7 @@ struct GemmWs {                 // split-K partials + per-tile semaphores (carve
 void launch_gemm(const bf16* A, int lda, int a_rows, const bf16* W, int N, int K, float* C, int ldc,
                  const int* M_dev, int M_max, GemmMode mode, const GemmWs& ws, cudaStream_t s);
 int gemm_backend();
+int num_sms();
 void gemm_set_backend(int b);
 
 struct AttnArgs {
@@ -119,13 +121,17 @@ struct AttnArgs {
   int split_tiles;              // 64-key tiles per key split (>= 2)
   int max_nsplit;               // split slots per (request, chunk, kv head) in `part`
   float* part;                  // split partials [pair][max_nsplit][128 * head_dim + 2 * 128]
+  float* imp_scratch;           // per-CTA block-score scratch [grid][128][64] (importance epilogue)
+  unsigned long long* trace;    // debug: clock64 events [grid][8][kTraceEv] or nullptr
   int* sem;                     // per-pair arrival counters (zero between launches)
 };
 void launch_attention(const AttnArgs& a, cudaStream_t s);
-bool attn_tc_supported(int head_dim, int page_size);
+bool attn_tc_supported(int head_dim, int page_size, int group);
+bool attn_tc_make_qmap(const bf16* q, size_t rows, int ld, int group, CUtensorMap* mq);
 bool attn_tc_make_maps(const bf16* Kpool, const bf16* Vpool, size_t rows, int head_dim, int page_size,
                        CUtensorMap* mk, CUtensorMap* mv);
-void launch_attention_tc(const CUtensorMap& mk, const CUtensorMap& mv, const AttnArgs& a, cudaStream_t s);
+void launch_attention_tc(const CUtensorMap& mk, const CUtensorMap& mv, const CUtensorMap& mq, const AttnArgs& a,
+                         cudaStream_t s);
 
 struct SelectArgs {
   const int* req_list; int n_req;

@@ -60,8 +60,11 @@ struct focus_ctx {
   // attention path: tcgen05 kernel (head_dim 64/128) or the SIMT kernel (other head dims)
   bool attn_tc = false;
   int attn_rpc = 0, split_tiles = 8, max_nsplit = 1;
-  CUtensorMap mapK, mapV;
+  CUtensorMap mapK, mapV, mapQ_qkv, mapQ_qs;
   float* attn_part = nullptr;
+  float* attn_scratch = nullptr;
+  unsigned long long* attn_trace = nullptr;
+  int trace_layer = -1;
   int* attn_sem = nullptr;
   // weights
   bf16* E = nullptr;
@@ -197,6 +200,10 @@ size_t carve(focus_ctx* x, char* base) {
     const size_t pairs = (size_t)c.max_requests * x->n_chunks * c.n_kv_heads;
     x->attn_part = (float*)take(pairs * x->max_nsplit * ((size_t)128 * c.head_dim + 256) * 4);
     x->attn_sem = (int*)take(pairs * 4);
+    x->attn_scratch = (float*)take((size_t)1024 * 128 * kMaxB * 4);   // >= grid (one CTA per SM)
+    const char* tl = getenv("FOCUS_ATTN_TRACE_LAYER");
+    x->trace_layer = tl ? atoi(tl) : -1;
+    if (x->trace_layer >= 0) x->attn_trace = (unsigned long long*)take((size_t)1024 * 8 * kTraceEv * 8);
   }
   x->gws.bytes = (size_t)64 << 20;
   x->gws.ptr = (float*)take(x->gws.bytes);
@@ -224,7 +231,7 @@ void derive(focus_ctx* x) {
   const int64_t pages = c.kv_pages > 0 ? c.kv_pages : (int64_t)c.max_requests * x->max_pages_per_req;
   x->kv_pages = pages;
   x->kv_layer_elems = (size_t)pages * c.n_kv_heads * c.page_size * c.head_dim;
-  x->attn_tc = attn_tc_supported(c.head_dim, c.page_size) && getenv("FOCUS_ATTN_SIMT") == nullptr;
+  x->attn_tc = attn_tc_supported(c.head_dim, c.page_size, x->G) && getenv("FOCUS_ATTN_SIMT") == nullptr;
   x->attn_rpc = (x->attn_tc ? 128 : kAttnQRows) / x->G;
   x->n_chunks = (x->B + x->attn_rpc - 1) / x->attn_rpc;
   x->split_tiles = 8;
@@ -373,11 +380,14 @@ AttnArgs attn_args(focus_ctx* x, int l, const bf16* q, int ldq, int n_req, const
   a.max_nsplit = x->max_nsplit;
   a.part = x->attn_part;
   a.sem = x->attn_sem;
+  a.imp_scratch = x->attn_scratch;
+  a.trace = (l == x->trace_layer && x->cfg.debug_taps >= 0) ? x->attn_trace : nullptr;
   return a;
 }
 
 void run_attention(focus_ctx* x, const AttnArgs& a) {
-  if (x->attn_tc) launch_attention_tc(x->mapK, x->mapV, a, x->stream);
+  if (a.trace) cudaMemsetAsync(a.trace, 0, (size_t)num_sms() * 8 * kTraceEv * 8, x->stream);
+  if (x->attn_tc) launch_attention_tc(x->mapK, x->mapV, a.q == x->qS ? x->mapQ_qs : x->mapQ_qkv, a, x->stream);
   else launch_attention(a, x->stream);
 }
 
@@ -471,7 +481,9 @@ focus_status focus_init(const focus_config* cfg, void* dev_arena, size_t arena_b
   if (x->attn_tc) {
     cudaMemsetAsync(x->attn_sem, 0, (size_t)c.max_requests * x->n_chunks * c.n_kv_heads * 4, s);
     const size_t rows = (size_t)c.n_layers * x->kv_pages * c.n_kv_heads * c.page_size;
-    if (!attn_tc_make_maps(x->Kpool, x->Vpool, rows, c.head_dim, c.page_size, &x->mapK, &x->mapV)) {
+    if (!attn_tc_make_maps(x->Kpool, x->Vpool, rows, c.head_dim, c.page_size, &x->mapK, &x->mapV) ||
+        !attn_tc_make_qmap(x->qkv, x->max_rows, x->qkv_dim, x->G, &x->mapQ_qkv) ||
+        !attn_tc_make_qmap(x->qS, x->max_rows, x->q_dim, x->G, &x->mapQ_qs)) {
       cudaStreamSynchronize(s);
       cudaFreeHost(x->up.host);
       delete x;
@@ -775,6 +787,7 @@ focus_status focus_debug_export(focus_ctx* x, int32_t what, int32_t req_id, int3
     case FOCUS_DBG_LOGITS: src = x->logits; bytes = (size_t)cnt.M_L * c.vocab * 4; break;
     case FOCUS_DBG_TOKCONF: src = x->tokconf; bytes = (size_t)cnt.M_L * sizeof(TokConf); break;
     case FOCUS_DBG_HL: src = x->h; bytes = (size_t)cnt.M_L * c.d_model * 2; break;
+    case FOCUS_DBG_ATTN_TRACE: src = x->attn_trace; bytes = x->attn_trace ? (size_t)num_sms() * 8 * kTraceEv * 8 : 0; break;
     case FOCUS_DBG_LAUNCHES:
       if (cap < 8) return FOCUS_ERR_IO;
       std::memcpy(dst, &x->launches, 8);

@@ -14,18 +14,21 @@
 // (deterministic).
 //
 // Persistent CTA (one per SM), 384 threads, warp-specialised:
-//   warp 0      TMA producer: K and V tiles (64 keys x head_dim, 128-B swizzle) into a 4-stage ring
+//   warp 0 / 2  TMA producers: K tiles / V tiles (64 keys x head_dim, 128-B swizzle) into a 4-slot K
+//               ring (freed when QK^T completes) and a 3-slot V ring (freed when PV completes)
 //   warp 1      MMA issuer: S = Q K^T (M=128, N=64, K=head_dim) into a double-buffered TMEM S tile,
 //               then O += P V (M=128, N=head_dim, K=64; V as an MN-major operand) into a
 //               double-buffered TMEM O accumulator (one buffer per unit in flight)
-//   warp 2      TMEM allocator
-//   warp 3      Q loader: cp.async of the unit's q rows into a swizzled smem tile (double-buffered)
-//   warps 4-7   softmax: one TMEM lane (= one query row) per thread; online softmax in the log2
-//               domain with lazy O rescaling (only when the running max grows by > 8), P -> smem as
-//               bf16; records the block-column scores for the importance epilogue
+//   warp 3      TMEM allocator + Q loader: cp.async of the unit's q rows into a swizzled smem tile (double-buffered)
+//   warps 4-7   softmax: warp 4+q owns TMEM lane quadrant q and reads its (<= 32) real rows 16 lanes
+//               at a time (16x256b shape: 4 threads per row, 16 columns each); online softmax in the
+//               log2 domain with lazy O rescaling (only when the running max grows by > 8), P -> a
+//               double-buffered smem tile as bf16; block-column scores -> per-CTA scratch for the
+//               importance epilogue
 //   warps 8-11  epilogue: O / l -> bf16 output rows (or split partials + fixed-order merge)
-// Query rows are spread over the 4 TMEM lane quadrants (row qi -> lane (qi%4)*32 + qi/4) so that the
-// ~30-60 real rows of a decode unit use all four SM sub-partitions.
+// Q tile lane L = g * (128/G) + r holds query head g of block row r (G <= 4), so with G = 4 every TMEM
+// lane quadrant (SM sub-partition) gets one head's rows and the ~30-60 real rows of a decode unit
+// keep all four softmax warps busy.
 #include <math_constants.h>
 
 #include "tc_ptx.cuh"
@@ -37,7 +40,8 @@ using namespace tc;
 
 constexpr int KT = 64;            // keys per tile
 constexpr int QR = 128;           // query rows per unit (MMA M)
-constexpr int ST = 4;             // K/V pipeline stages
+constexpr int SK = 4;             // K ring slots (released when QK^T completes)
+constexpr int SV = 3;             // V ring slots (released when PV completes)
 constexpr int NTHREADS = 384;
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kRescaleThresh = 8.0f;   // log2 units
@@ -49,7 +53,6 @@ struct Cfg {
   static constexpr int Q_BYTES = NH * HALF_BYTES;
   static constexpr int KH_BYTES = KT * 128;           // one half of a K or V tile (8 KB)
   static constexpr int K_BYTES = NH * KH_BYTES;
-  static constexpr int STAGE_BYTES = 2 * K_BYTES;     // K + V
   static constexpr int P_BYTES = QR * KT * 2;         // 16 KB
   static constexpr int TMEM_COLS = (2 * DH + 2 * KT) <= 256 ? 256 : 512;
   static constexpr int O_COL = 0;                     // O buffers at [0, DH), [DH, 2DH)
@@ -57,14 +60,25 @@ struct Cfg {
   static constexpr uint32_t IDESC_QK = idesc_bf16(QR, KT, false, false);
   static constexpr uint32_t IDESC_PV = idesc_bf16(QR, DH, false, true);
   static constexpr int OFF_Q = 0;
-  static constexpr int OFF_KV = OFF_Q + 2 * Q_BYTES;
-  static constexpr int OFF_P = OFF_KV + ST * STAGE_BYTES;
-  static constexpr int OFF_BAR = OFF_P + P_BYTES;
-  static constexpr int N_BARS = 2 * ST + 2 * 2 + 2 * 2 + 2 + 2 * 2 + 2;
+  static constexpr int OFF_K = OFF_Q + 2 * Q_BYTES;
+  static constexpr int OFF_V = OFF_K + SK * K_BYTES;
+  static constexpr int OFF_P = OFF_V + SV * K_BYTES;
+  static constexpr int OFF_BAR = OFF_P + 2 * P_BYTES;
+  static constexpr int N_BARS = 2 * SK + 2 * SV + 9 * 2;
   static constexpr int OFF_STAT = OFF_BAR + 8 * N_BARS + 8;
   static constexpr int OFF_RED = OFF_STAT + 2 * QR * 8;
   static constexpr int OFF_PRE = OFF_RED + 4 * kMaxB * 4;
   static constexpr int SMEM_BYTES = OFF_PRE + 2 * 1028 * 4 + 64 + 1024;
+};
+
+// debug trace: role r of this CTA appends clock64 stamps (event kind in the top 8 bits)
+struct Tracer {
+  unsigned long long* p;
+  int n;
+  __device__ __forceinline__ Tracer(unsigned long long* base, int role) : p(base ? base + ((size_t)blockIdx.x * 8 + role) * kTraceEv : nullptr), n(0) {}
+  __device__ __forceinline__ void ev(int kind) {
+    if (p && n < kTraceEv) p[n++] = ((unsigned long long)kind << 56) | (clock64() & ((1ull << 56) - 1));
+  }
 };
 
 struct Unit {
@@ -138,32 +152,37 @@ __device__ __forceinline__ Unit decode_unit(const AttnArgs& a, int u, const int*
     x.pos_base = 0;
   }
   x.nq = x.nr * G;
-  const int t0 = x.kbeg / KT, t1 = (x.kend + KT - 1) / KT;
-  x.t_hi = t1 - (x.nsplit - 1 - x.sp) * a.split_tiles;
-  x.t_lo = max(t0, x.t_hi - a.split_tiles);
+  // tiles split evenly; the last split (which holds the block tiles) gets the larger share
+  const int t0 = x.kbeg / KT, nt = (x.kend + KT - 1) / KT - t0;
+  x.t_lo = t0 + (x.sp * nt) / x.nsplit;
+  x.t_hi = t0 + ((x.sp + 1) * nt) / x.nsplit;
   x.pair = (x.i * a.n_chunks + x.chunk) * H + x.kvh;
   return x;
 }
 
 template <int DH, bool IMP_ONLY>
 __global__ void __launch_bounds__(NTHREADS, 1)
-    k_attn_tc(const __grid_constant__ CUtensorMap mapK, const __grid_constant__ CUtensorMap mapV, AttnArgs a) {
+    k_attn_tc(const __grid_constant__ CUtensorMap mapK, const __grid_constant__ CUtensorMap mapV,
+              const __grid_constant__ CUtensorMap mapQ, AttnArgs a) {
   using C = Cfg<DH>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* sQ = smem + C::OFF_Q;
-  uint8_t* sKV = smem + C::OFF_KV;
+  uint8_t* sK = smem + C::OFF_K;
+  uint8_t* sV = smem + C::OFF_V;
   uint8_t* sP = smem + C::OFF_P;
   uint64_t* bars = (uint64_t*)(smem + C::OFF_BAR);
-  uint64_t* kvfull = bars;                 // [ST]
-  uint64_t* kvempty = bars + ST;           // [ST]
-  uint64_t* qfull = bars + 2 * ST;         // [2]
+  uint64_t* kfull = bars;                  // [SK]
+  uint64_t* kempty = kfull + SK;           // [SK]
+  uint64_t* vfull = kempty + SK;           // [SV]
+  uint64_t* vempty = vfull + SV;           // [SV]
+  uint64_t* qfull = vempty + SV;           // [2]
   uint64_t* qempty = qfull + 2;            // [2]
   uint64_t* sfull = qempty + 2;            // [2]
   uint64_t* sfree = sfull + 2;             // [2]
-  uint64_t* pfull = sfree + 2;             // [1]
-  uint64_t* pvdone = pfull + 1;            // [1]
-  uint64_t* ofull = pvdone + 1;            // [2]
+  uint64_t* pfull = sfree + 2;             // [2] (per P buffer)
+  uint64_t* pvdone = pfull + 2;            // [2] (per P buffer)
+  uint64_t* ofull = pvdone + 2;            // [2]
   uint64_t* ofree = ofull + 2;             // [2]
   uint64_t* statfull = ofree + 2;          // [2]
   uint32_t* tmem_sh = (uint32_t*)(bars + C::N_BARS);
@@ -195,22 +214,23 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
   }
   if (threadIdx.x == 0) {
-    for (int i = 0; i < ST; ++i) { mbar_init(&kvfull[i], 1); mbar_init(&kvempty[i], 1); }
+    for (int i = 0; i < SK; ++i) { mbar_init(&kfull[i], 1); mbar_init(&kempty[i], 1); }
+    for (int i = 0; i < SV; ++i) { mbar_init(&vfull[i], 1); mbar_init(&vempty[i], 1); }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&qfull[i], 1); mbar_init(&qempty[i], 1);
       mbar_init(&sfull[i], 1); mbar_init(&sfree[i], 4);
       mbar_init(&ofull[i], 1); mbar_init(&ofree[i], 4);
       mbar_init(&statfull[i], 4);
     }
-    mbar_init(pfull, 4);
-    mbar_init(pvdone, 1);
+    for (int i = 0; i < 2; ++i) { mbar_init(&pfull[i], 4); mbar_init(&pvdone[i], 1); }
     fence_barrier_init();
   }
   if (warp == 1 && lane == 0) {
+    prefetch_map(&mapQ);
     prefetch_map(&mapK);
     if (!IMP_ONLY) prefetch_map(&mapV);
   }
-  if (warp == 2) tmem_alloc<C::TMEM_COLS>(tmem_sh);
+  if (warp == 3) tmem_alloc<C::TMEM_COLS>(tmem_sh);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -229,34 +249,43 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     if (lane == 31) pre[n_ent] = inc;
   }
   __syncthreads();
+  if (threadIdx.x == 0 && a.trace) a.trace[((size_t)blockIdx.x * 8 + 7) * kTraceEv] = clock64();
   const int total = pre[n_ent];
   const uint32_t tmem = *tmem_sh;
 
-  if (warp == 0) {
-    // ================================================================ TMA producer
+  if (warp == 0 || (warp == 2 && !IMP_ONLY)) {
+    // ================================================================ TMA producers
+    // warp 0 lane 0 streams K tiles, warp 2 lane 0 streams V tiles (separate rings: K is consumed by
+    // QK^T about two tiles before V is consumed by PV, so each ring prefetches its own distance)
     if (lane == 0) {
+      const bool isK = warp == 0;
+      const int NS = isK ? SK : SV;
+      uint64_t* fullb = isK ? kfull : vfull;
+      uint64_t* emptyb = isK ? kempty : vempty;
+      uint8_t* ring = isK ? sK : sV;
+      const CUtensorMap* map = isK ? &mapK : &mapV;
       const int ps = a.kv.page_size;
       const int pr = min(ps, KT);                  // keys per TMA box
       const size_t layer_rows = (size_t)a.kv_pages * H * ps;
       uint32_t g = 0;
+      Tracer tr(a.trace, isK ? 0 : 1);
       for (int u = blockIdx.x; u < total; u += gridDim.x) {
+        tr.ev(0);
         const Unit x = decode_unit(a, u, pre, nsp, n_ent, G, rpc);
+        tr.ev(9);
         for (int t = x.t_lo; t < x.t_hi; ++t, ++g) {
-          const int stage = g % ST;
-          mbar_wait(&kvempty[stage], ((g / ST) & 1) ^ 1);
-          mbar_expect_tx(&kvfull[stage], IMP_ONLY ? C::K_BYTES : C::STAGE_BYTES);
-          uint8_t* dK = sKV + stage * C::STAGE_BYTES;
-          uint8_t* dV = dK + C::K_BYTES;
+          const int slot = g % NS;
+          mbar_wait(&emptyb[slot], ((g / NS) & 1) ^ 1);
+          tr.ev(1);
+          mbar_expect_tx(&fullb[slot], C::K_BYTES);
+          uint8_t* dst = ring + slot * C::K_BYTES;
           for (int pc = 0; pc < KT / pr; ++pc) {
             const int pos = t * KT + pc * pr;
             const int pidx = min(pos / ps, a.kv.max_pages - 1);
             const int page = a.kv.page_table[(size_t)x.slot * a.kv.max_pages + pidx];
             const int row = (int)((size_t)a.layer * layer_rows + ((size_t)page * H + x.kvh) * ps + pos % ps);
 #pragma unroll
-            for (int h = 0; h < C::NH; ++h) {
-              tma_load_2d(dK + h * C::KH_BYTES + pc * pr * 128, &mapK, &kvfull[stage], h * 64, row);
-              if (!IMP_ONLY) tma_load_2d(dV + h * C::KH_BYTES + pc * pr * 128, &mapV, &kvfull[stage], h * 64, row);
-            }
+            for (int h = 0; h < C::NH; ++h) tma_load_2d(dst + h * C::KH_BYTES + pc * pr * 128, map, &fullb[slot], h * 64, row);
           }
         }
       }
@@ -267,35 +296,45 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       uint32_t g = 0, it = 0;
       // deferred PV of the previous tile (issued after the next QK so softmax overlaps the tensor pipe)
       bool pend = false;
-      uint32_t p_g = 0, p_stage = 0, p_ob = 0, p_it = 0;
+      uint32_t p_g = 0, p_ob = 0, p_it = 0;
       bool p_first = false, p_last = false;
       auto issue_pv = [&]() {
-        mbar_wait(pfull, p_g & 1);
+        const uint32_t pb = p_g & 1;
+        mbar_wait(&pfull[pb], (p_g >> 1) & 1);
         if (p_first) mbar_wait(&ofree[p_ob], ((p_it >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d = tmem + C::O_COL + p_ob * DH;
-        const uint32_t pa = smem_u32(sP);
-        const uint32_t vb = smem_u32(sKV + p_stage * C::STAGE_BYTES + C::K_BYTES);
+        const uint32_t pa = smem_u32(sP + pb * C::P_BYTES);
+        const uint32_t vs = p_g % SV;
+        mbar_wait(&vfull[vs], (p_g / SV) & 1);
+        tc_fence_after();
+        const uint32_t vb = smem_u32(sV + vs * C::K_BYTES);
 #pragma unroll
         for (int kk = 0; kk < KT / 16; ++kk)
           mma_bf16(d, desc_kmajor_sw128(pa + kk * 32), desc_mnmajor_sw128(vb + kk * 16 * 128, C::KH_BYTES),
                    C::IDESC_PV, (p_first && kk == 0) ? 0u : 1u);
-        mma_commit(&kvempty[p_stage]);
-        mma_commit(pvdone);
+        mma_commit(&vempty[vs]);
+        mma_commit(&pvdone[pb]);
         if (p_last) mma_commit(&ofull[p_ob]);
       };
+      Tracer tr(a.trace, 2);
       for (int u = blockIdx.x; u < total; u += gridDim.x, ++it) {
+        tr.ev(0);
         const Unit x = decode_unit(a, u, pre, nsp, n_ent, G, rpc);
+        tr.ev(9);
         const uint32_t ob = it & 1;
         mbar_wait(&qfull[ob], (it >> 1) & 1);
+        tr.ev(2);
         tc_fence_after();
         const uint32_t qa = smem_u32(sQ + ob * C::Q_BYTES);
         for (int t = x.t_lo; t < x.t_hi; ++t, ++g) {
-          const uint32_t stage = g % ST, sb = g & 1;
-          mbar_wait(&kvfull[stage], (g / ST) & 1);
+          const uint32_t ks = g % SK, sb = g & 1;
+          mbar_wait(&kfull[ks], (g / SK) & 1);
+          tr.ev(3);
           mbar_wait(&sfree[sb], ((g >> 1) & 1) ^ 1);
+          tr.ev(4);
           tc_fence_after();
-          const uint32_t kb = smem_u32(sKV + stage * C::STAGE_BYTES);
+          const uint32_t kb = smem_u32(sK + ks * C::K_BYTES);
           const uint32_t d = tmem + C::S_COL + sb * KT;
 #pragma unroll
           for (int kk = 0; kk < DH / 16; ++kk) {
@@ -304,14 +343,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                      C::IDESC_QK, kk > 0 ? 1u : 0u);
           }
           mma_commit(&sfull[sb]);
+          mma_commit(&kempty[ks]);
           if (t + 1 == x.t_hi) mma_commit(&qempty[ob]);
-          if (IMP_ONLY) {
-            mma_commit(&kvempty[stage]);
-            continue;
-          }
-          if (pend) issue_pv();
+          if (IMP_ONLY) continue;
+          if (pend) { issue_pv(); tr.ev(5); }
           pend = true;
-          p_g = g; p_stage = stage; p_ob = ob; p_it = it;
+          p_g = g; p_ob = ob; p_it = it;
           p_first = t == x.t_lo;
           p_last = t + 1 == x.t_hi;
         }
@@ -319,148 +356,214 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       if (!IMP_ONLY && pend) issue_pv();
     }
   } else if (warp == 3) {
-    // ================================================================ Q loader
-    uint32_t it = 0;
-    for (int u = blockIdx.x; u < total; u += gridDim.x, ++it) {
-      const Unit x = decode_unit(a, u, pre, nsp, n_ent, G, rpc);
-      const uint32_t ob = it & 1;
-      mbar_wait(&qempty[ob], ((it >> 1) & 1) ^ 1);
-      uint8_t* q = sQ + ob * C::Q_BYTES;
-      constexpr int CPR = DH / 8;                  // 16-B chunks per row
-      for (int idx = lane; idx < QR * CPR; idx += 32) {
-        const int L = idx / CPR, cc = idx % CPR;
-        const int h = cc >> 3, c = cc & 7;
-        const int qi = (L & 31) * 4 + (L >> 5);
-        uint8_t* dst = q + h * C::HALF_BYTES + sw128_off(L, c);
-        if (qi < x.nq) {
-          const int row = x.r0 + qi / G, head = x.kvh * G + qi % G;
-          const bf16* src = a.q + (size_t)row * a.ldq + head * DH + h * 64 + c * 8;
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-        } else {
-          *reinterpret_cast<uint4*>(dst) = make_uint4(0, 0, 0, 0);
-        }
+    // ================================================================ Q loader (TMA)
+    // Q tile lane L holds head g = L / rpc of block row r = L % rpc of the unit: for each head and
+    // 64-column half, one box of rpc consecutive q rows (rows past the unit belong to other requests
+    // or are zero-filled out of bounds; their outputs are discarded).
+    if (lane == 0) {
+      uint32_t it = 0;
+      Tracer tr(a.trace, 3);
+      for (int u = blockIdx.x; u < total; u += gridDim.x, ++it) {
+        tr.ev(0);
+        const Unit x = decode_unit(a, u, pre, nsp, n_ent, G, rpc);
+        tr.ev(9);
+        const uint32_t ob = it & 1;
+        mbar_wait(&qempty[ob], ((it >> 1) & 1) ^ 1);
+        tr.ev(1);
+        mbar_expect_tx(&qfull[ob], C::Q_BYTES);
+        uint8_t* q = sQ + ob * C::Q_BYTES;
+        for (int gq = 0; gq < G; ++gq)
+#pragma unroll
+          for (int h = 0; h < C::NH; ++h)
+            tma_load_2d(q + h * C::HALF_BYTES + gq * rpc * 128, &mapQ, &qfull[ob], (x.kvh * G + gq) * DH + h * 64, x.r0);
       }
-      asm volatile("cp.async.wait_all;" ::: "memory");
-      fence_proxy_async();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&qfull[ob]);
     }
   } else if (warp >= 4 && warp < 8) {
     // ================================================================ softmax (+ importance)
+    // Warp 4+q owns TMEM lane quadrant q.  Its real rows sit in lanes 0.. of the quadrant; they are
+    // read 16 lanes at a time with the 16x256b shape, so 4 threads share a row (16 of the 64 columns
+    // each) and every lane of the warp works on a real row.
     const int q4 = warp & 3;
-    const int L = q4 * 32 + lane;                  // TMEM lane = smem Q/P row of this thread
-    const int qi = lane * 4 + q4;                  // logical query row
+    const int t0 = lane & 3, t1 = lane >> 2;
     const float sl2 = a.scale * kLog2e;
+    float* scr = a.imp_scratch + (size_t)blockIdx.x * QR * kMaxB;
     uint32_t g = 0, it = 0;
+    Tracer tr(warp == 4 && lane == 0 ? a.trace : nullptr, 4);
     for (int u = blockIdx.x; u < total; u += gridDim.x, ++it) {
+      tr.ev(0);
       const Unit x = decode_unit(a, u, pre, nsp, n_ent, G, rpc);
+      tr.ev(9);
       const uint32_t ob = it & 1;
-      const bool active = q4 < x.nq;               // warp-uniform: quadrant has a real row
-      const bool real = qi < x.nq;
-      const int lim = a.ext_mode == 2 ? x.pos_base + qi / G : x.kend - 1;   // last visible key
-      float m_used = -CUDART_INF_F, l = 0.f;
-      float sc[kMaxB];
+      const int rows_q = min(32, max(0, x.nr - (32 * q4) % rpc));  // real rows: a prefix of the quadrant
+      const int ngrp = rows_q > 16 ? 2 : (rows_q > 0 ? 1 : 0);      // warp-uniform
+      const int lim_min = a.ext_mode == 2 ? x.pos_base : x.kend - 1;
+      int lim[2][2];
+      bool real[2][2];
+#pragma unroll
+      for (int gr = 0; gr < 2; ++gr)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int rr = (q4 * 32 + gr * 16 + t1 + 8 * h) % rpc;   // block row of this lane
+          real[gr][h] = rr < x.nr;
+          lim[gr][h] = a.ext_mode == 2 ? x.pos_base + rr : x.kend - 1;
+        }
+      float m_used[2][2], l[2][2];
+#pragma unroll
+      for (int gr = 0; gr < 2; ++gr)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) { m_used[gr][h] = -CUDART_INF_F; l[gr][h] = 0.f; }
       for (int t = x.t_lo; t < x.t_hi; ++t, ++g) {
         const uint32_t sb = g & 1;
         mbar_wait(&sfull[sb], (g >> 1) & 1);
+        tr.ev(1);
         tc_fence_after();
-        uint32_t r[KT];
-        if (active) {
-          const uint32_t ta = tmem + ((uint32_t)(q4 * 32) << 16) + C::S_COL + sb * KT;
-          tmem_ld32_nowait(ta, r);
-          tmem_ld32_nowait(ta + 32, r + 32);
-          tmem_wait_ld();
-        }
+        uint32_t r[2][32];
+#pragma unroll
+        for (int gr = 0; gr < 2; ++gr)
+          if (gr < ngrp)
+            tmem_ld16x256_x8(tmem + ((uint32_t)(q4 * 32 + gr * 16) << 16) + C::S_COL + sb * KT, r[gr]);
+        tmem_wait_ld();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&sfree[sb]);
         const int k0 = t * KT;
-        if (x.want_imp && real) {
+        if (x.want_imp) {                          // block-column scores for the Eq.2 epilogue
 #pragma unroll
-          for (int c = 0; c < KT; ++c) {
-            const int j = k0 + c - x.s0;
-            if (j >= 0 && j < a.B) sc[j] = __uint_as_float(r[c]) * a.scale;
-          }
+          for (int gr = 0; gr < 2; ++gr)
+            if (gr < ngrp)
+#pragma unroll
+              for (int h = 0; h < 2; ++h)
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+#pragma unroll
+                  for (int e = 0; e < 2; ++e) {
+                    const int jb = k0 + 8 * j + 2 * t0 + e - x.s0;
+                    if (real[gr][h] && jb >= 0 && jb < a.B)
+                      scr[(q4 * 32 + gr * 16 + t1 + 8 * h) * kMaxB + jb] = __uint_as_float(r[gr][4 * j + 2 * h + e]) * a.scale;
+                  }
         }
         if (IMP_ONLY) continue;
-        // online softmax (log2 domain), lazy rescale
-        float mt = -CUDART_INF_F;
-        if (real) {
+        const bool full = k0 >= x.kbeg && k0 + KT - 1 <= lim_min;
+        const uint32_t pb = g & 1;
+        uint32_t pk[2][2][8];
+        bool resc_any = false;
+        float alpha[2][2];
 #pragma unroll
-          for (int c = 0; c < KT; ++c) {
-            const int p = k0 + c;
-            const bool ok = p >= x.kbeg && p <= lim;
-            const float v = ok ? __uint_as_float(r[c]) * sl2 : -CUDART_INF_F;
-            r[c] = __float_as_uint(v);
-            mt = fmaxf(mt, v);
-          }
-        }
-        float alpha = 1.f;
-        bool resc = false;
-        if (mt > m_used + kRescaleThresh || (m_used == -CUDART_INF_F && mt > -CUDART_INF_F)) {
-          const float mn = fmaxf(mt, m_used);
-          alpha = exp2f(m_used - mn);             // 0 when m_used = -inf
-          m_used = mn;
-          resc = true;
-        }
-        uint32_t pk[KT / 2];
-        float rs = 0.f;
-        if (real) {
+        for (int gr = 0; gr < 2; ++gr) {
+          if (gr >= ngrp) continue;
 #pragma unroll
-          for (int c = 0; c < KT; c += 2) {
-            const float p0 = exp2f(__uint_as_float(r[c]) - m_used);
-            const float p1 = exp2f(__uint_as_float(r[c + 1]) - m_used);
-            const __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
-            const float2 bf = __bfloat1622float2(b2);
-            rs += bf.x + bf.y;                      // sum what the tensor core will multiply
-            pk[c / 2] = *reinterpret_cast<const uint32_t*>(&b2);
-          }
-        } else {
+          for (int h = 0; h < 2; ++h) {
+            float mx = -CUDART_INF_F;
+            if (!full) {
 #pragma unroll
-          for (int c = 0; c < KT / 2; ++c) pk[c] = 0u;
-        }
-        l = l * alpha + rs;
-        if (g > 0) mbar_wait(pvdone, (g - 1) & 1);   // PV of the previous tile done: P free, O stable
-        if (active) {
+              for (int j = 0; j < 8; ++j)
 #pragma unroll
-          for (int c = 0; c < 8; ++c)
-            *reinterpret_cast<uint4*>(sP + sw128_off(L, c)) =
-                make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
-          const bool any = __any_sync(0xffffffffu, resc && real) && t > x.t_lo;
-          if (any) {
-            tc_fence_after();
-            const float f = (resc && real) ? alpha : 1.f;
-#pragma unroll 1
-            for (int c0 = 0; c0 < DH; c0 += 32) {
-              const uint32_t ta = tmem + ((uint32_t)(q4 * 32) << 16) + C::O_COL + ob * DH + c0;
-              float v[32];
-              tmem_ld32(ta, v);
-#pragma unroll
-              for (int e = 0; e < 32; ++e) v[e] *= f;
-              tmem_st32(ta, v);
+                for (int e = 0; e < 2; ++e) {
+                  const int c = k0 + 8 * j + 2 * t0 + e;
+                  if (c < x.kbeg || c > lim[gr][h]) r[gr][4 * j + 2 * h + e] = __float_as_uint(-CUDART_INF_F);
+                }
             }
-            tmem_wait_st();
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              mx = fmaxf(mx, fmaxf(__uint_as_float(r[gr][4 * j + 2 * h]), __uint_as_float(r[gr][4 * j + 2 * h + 1])));
+            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+            const float mt = mx * sl2;
+            float al = 1.f;
+            float mu = m_used[gr][h];
+            if (mt > mu + kRescaleThresh || (mu == -CUDART_INF_F && mt > -CUDART_INF_F)) {
+              const float mn = fmaxf(mt, mu);
+              al = ex2(mu - mn);                   // 0 when mu = -inf
+              m_used[gr][h] = mn;
+              resc_any |= real[gr][h] && t > x.t_lo;
+            }
+            alpha[gr][h] = al;
+            const float nm = m_used[gr][h] == -CUDART_INF_F ? 0.f : -m_used[gr][h];
+            float sum = 0.f;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              float p0 = ex2(fmaf(__uint_as_float(r[gr][4 * j + 2 * h]), sl2, nm));
+              float p1 = ex2(fmaf(__uint_as_float(r[gr][4 * j + 2 * h + 1]), sl2, nm));
+              if (!real[gr][h]) { p0 = 0.f; p1 = 0.f; }
+              sum += p0 + p1;
+              const __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
+              pk[gr][h][j] = *reinterpret_cast<const uint32_t*>(&b2);
+            }
+            l[gr][h] = l[gr][h] * al + sum;
           }
+        }
+        resc_any = __any_sync(0xffffffffu, resc_any);
+        tr.ev(2);
+        if (g >= 2) mbar_wait(&pvdone[pb], ((g >> 1) & 1) ^ 1);   // PV of tile g-2 done: P buffer free
+        tr.ev(3);
+        const uint32_t pbase = smem_u32(sP + pb * C::P_BYTES);
+#pragma unroll
+        for (int gr = 0; gr < 2; ++gr) {
+          if (gr >= ngrp) continue;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int Lr = q4 * 32 + gr * 16 + t1 + 8 * h;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) sts32(pbase + sw128_off(Lr, j) + 4 * t0, pk[gr][h][j]);
+          }
+        }
+        if (resc_any) {                            // O *= alpha for rows whose running max moved (lazy)
+          mbar_wait(&pvdone[(g - 1) & 1], ((g - 1) >> 1) & 1);   // PV of tile g-1 done: O stable
+          tc_fence_after();
+#pragma unroll
+          for (int gr = 0; gr < 2; ++gr) {
+            if (gr >= ngrp) continue;
+#pragma unroll 1
+            for (int c0 = 0; c0 < DH; c0 += 64) {
+              const uint32_t ta = tmem + ((uint32_t)(q4 * 32 + gr * 16) << 16) + C::O_COL + ob * DH + c0;
+              uint32_t v[32];
+              tmem_ld16x256_x8(ta, v);
+              tmem_wait_ld();
+#pragma unroll
+              for (int j = 0; j < 8; ++j)
+#pragma unroll
+                for (int h = 0; h < 2; ++h)
+#pragma unroll
+                  for (int e = 0; e < 2; ++e)
+                    v[4 * j + 2 * h + e] = __float_as_uint(__uint_as_float(v[4 * j + 2 * h + e]) * alpha[gr][h]);
+              tmem_st16x256_x8(ta, v);
+            }
+          }
+          tmem_wait_st();
         }
         fence_proxy_async();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(pfull);
+        if (lane == 0) mbar_arrive(&pfull[pb]);
+        tr.ev(4);
       }
       if (!IMP_ONLY) {
-        // per-row statistics for the epilogue (buffer ob is free once unit it-2's epilogue is done)
+        // row sums over the 4 threads of a row; per-row statistics for the epilogue (buffer ob is
+        // free once the epilogue of unit it-2 is done)
         mbar_wait(&ofree[ob], ((it >> 1) & 1) ^ 1);
-        stat[ob * QR + L] = make_float2(m_used, l);
+#pragma unroll
+        for (int gr = 0; gr < 2; ++gr)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            float ls = l[gr][h];
+            ls += __shfl_xor_sync(0xffffffffu, ls, 1);
+            ls += __shfl_xor_sync(0xffffffffu, ls, 2);
+            if (gr < ngrp && t0 == 0) stat[ob * QR + q4 * 32 + gr * 16 + t1 + 8 * h] = make_float2(m_used[gr][h], ls);
+          }
         __syncwarp();
         if (lane == 0) mbar_arrive(&statfull[ob]);
       }
       if (x.want_imp) {
         // Eq.2: per query row, MaxPool1D (k = mp_kernel, -inf outside P; A-I3, A-I5) over the block
         // scores, softmax over P, then the sum over rows and heads (fixed order: lanes, then warps).
+        __syncwarp();
         const int B = a.B, rad = a.mp_kernel / 2;
+        const int L = q4 * 32 + lane;
+        const bool rr = L % rpc < x.nr;
+        const float* sc = scr + L * kMaxB;
         float w[kMaxB];
         float mx = -CUDART_INF_F;
-        if (real) {
+        if (rr) {
           for (int j = 0; j < B; ++j) {
             float v = -CUDART_INF_F;
             if ((x.P >> j) & 1ull) {
@@ -480,12 +583,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           for (int j = 0; j < B; ++j) w[j] = w[j] / z;
         }
         for (int j = 0; j < B; ++j) {
-          float v = real ? w[j] : 0.f;
+          float v = rr ? w[j] : 0.f;
           for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
           if (lane == 0) red[q4 * kMaxB + j] = v;
         }
         named_bar(1, 128);
-        if (warp == 4 && lane < 32) {
+        if (warp == 4) {
           for (int j = lane; j < B; j += 32) {
             const float v = ((red[j] + red[kMaxB + j]) + red[2 * kMaxB + j]) + red[3 * kMaxB + j];
             a.imp[(size_t)x.pair * B + j] = v;
@@ -498,15 +601,19 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     // ================================================================ epilogue
     const int q4 = warp & 3;
     const int L = q4 * 32 + lane;
-    const int qi = lane * 4 + q4;
     const int et = threadIdx.x - 256;
     uint32_t it = 0;
+    Tracer tr(warp == 8 && lane == 0 ? a.trace : nullptr, 5);
     for (int u = blockIdx.x; u < total; u += gridDim.x, ++it) {
+      tr.ev(0);
       const Unit x = decode_unit(a, u, pre, nsp, n_ent, G, rpc);
+      tr.ev(9);
       const uint32_t ob = it & 1;
-      const bool active = q4 < x.nq, real = qi < x.nq;
+      const bool active = (32 * q4) % rpc < x.nr, real = L % rpc < x.nr;
+      const int qi = L;                            // partial-buffer row index
       mbar_wait(&ofull[ob], (it >> 1) & 1);
       mbar_wait(&statfull[ob], (it >> 1) & 1);
+      tr.ev(1);
       tc_fence_after();
       const float2 ml = stat[ob * QR + L];
       float o[DH];
@@ -518,7 +625,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&ofree[ob]);
-      const int row = x.r0 + qi / G, head = x.kvh * G + qi % G;
+      const int row = x.r0 + L % rpc, head = x.kvh * G + L / rpc;
       if (x.nsplit == 1) {
         if (real) {
           const float inv = 1.0f / ml.y;
@@ -585,7 +692,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
   }
   __syncthreads();
-  if (warp == 2) {
+  if (warp == 3) {
     tc_fence_after();
     tmem_free<C::TMEM_COLS>(tmem);
   }
@@ -593,9 +700,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 
 }  // namespace attn
 
-bool attn_tc_supported(int head_dim, int page_size) {
+bool attn_tc_supported(int head_dim, int page_size, int group) {
   return (head_dim == 64 || head_dim == 128) && page_size >= 8 && page_size <= 4096 &&
-         (page_size & (page_size - 1)) == 0;
+         (page_size & (page_size - 1)) == 0 && (group == 1 || group == 2 || group == 4);
+}
+
+// Query-row tensor map: q buffer [rows][ld] bf16, box = 64 columns x (128 / group) rows.
+bool attn_tc_make_qmap(const bf16* q, size_t rows, int ld, int group, CUtensorMap* mq) {
+  return make_tma_2d_bf16(q, rows, ld, ld, 64, 128 / group, mq);
 }
 
 // KV pool tensor maps: the whole pool (all layers) viewed as [rows][head_dim] bf16.
@@ -607,17 +719,19 @@ bool attn_tc_make_maps(const bf16* Kpool, const bf16* Vpool, size_t rows, int he
 }
 
 template <int DH, bool IMP>
-static void launch_tc(const CUtensorMap& mk, const CUtensorMap& mv, const AttnArgs& a, int grid, cudaStream_t s) {
+static void launch_tc(const CUtensorMap& mk, const CUtensorMap& mv, const CUtensorMap& mq, const AttnArgs& a, int grid,
+                      cudaStream_t s) {
   constexpr int smem = attn::Cfg<DH>::SMEM_BYTES;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(attn::k_attn_tc<DH, IMP>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
-  attn::k_attn_tc<DH, IMP><<<grid, attn::NTHREADS, smem, s>>>(mk, mv, a);
+  attn::k_attn_tc<DH, IMP><<<grid, attn::NTHREADS, smem, s>>>(mk, mv, mq, a);
 }
 
-void launch_attention_tc(const CUtensorMap& mk, const CUtensorMap& mv, const AttnArgs& a, cudaStream_t s) {
+void launch_attention_tc(const CUtensorMap& mk, const CUtensorMap& mv, const CUtensorMap& mq, const AttnArgs& a,
+                         cudaStream_t s) {
   const int G = a.n_q_heads / a.kv.n_kv_heads;
   const int rpc = attn::QR / G;
   int max_units;
@@ -626,9 +740,9 @@ void launch_attention_tc(const CUtensorMap& mk, const CUtensorMap& mv, const Att
   if (max_units <= 0) return;
   const int grid = std::max(1, std::min(num_sms(), max_units));
   if (a.kv.head_dim == 128) {
-    if (a.imp_only) launch_tc<128, true>(mk, mv, a, grid, s); else launch_tc<128, false>(mk, mv, a, grid, s);
+    if (a.imp_only) launch_tc<128, true>(mk, mv, mq, a, grid, s); else launch_tc<128, false>(mk, mv, mq, a, grid, s);
   } else {
-    if (a.imp_only) launch_tc<64, true>(mk, mv, a, grid, s); else launch_tc<64, false>(mk, mv, a, grid, s);
+    if (a.imp_only) launch_tc<64, true>(mk, mv, mq, a, grid, s); else launch_tc<64, false>(mk, mv, mq, a, grid, s);
   }
 }
 

@@ -21,7 +21,7 @@ FOCUS_ERR_NOMEM, FOCUS_ERR_STATE, FOCUS_ERR_CUDA = 5, 6, 7
 
 DBG = dict(STATE=1, COUNTERS=2, ROWS_P=3, ROWS_S=4, ROWS_L=5, I0=6, I1=7, LOGITS=8, TOKCONF=9, KV_K=10, KV_V=11,
            TAP_X_IN=20, TAP_H=21, TAP_QKV=22, TAP_ATTN=23, TAP_X_MID=24, TAP_H2=25, TAP_ACT=26, TAP_X_OUT=27,
-           TAP_QS=28, HL=29, LAUNCHES=30, PROFILE=31)
+           TAP_QS=28, HL=29, LAUNCHES=30, PROFILE=31, ATTN_TRACE=32)
 PROF_KINDS = ["setup", "embed", "rmsnorm", "gemm_qkv", "rope_store", "attention", "importance", "gemm_o",
               "gemm_gu", "silu_mul", "gemm_down", "select", "gather", "gemm_lm", "vocab_reduce", "commit"]
 

@@ -1,6 +1,6 @@
 set -x
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || { tail -30 gpurun_out/build.log; exit 1; }
-timeout 180 python -m pytest tests/test_gpu_layers.py -x -q -k "M8B4 or test_layer_stages and 0" 2>&1 | tail -15
+timeout 300 python -m pytest tests/test_gpu_layers.py -x -q 2>&1 | tail -15
 timeout 600 python -m pytest tests -m gpu -q -x 2>&1 | tail -25
 timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc $?"
 head -c 4000 gpurun_out/bench.json; tail -5 gpurun_out/bench.err
