@@ -86,12 +86,22 @@ void launch_gather_rows(const float* x, const bf16* qkv, int qkv_dim, int q_dim,
                         const int* M_dev, int M_max, int d, float* x_out, bf16* q_out, cudaStream_t s);
 
 // GEMM: C[M x N] (fp32) = A[M x K] (bf16, row stride lda) . W[N x K]^T (bf16), store or accumulate.
-enum GemmMode { GEMM_STORE = 0, GEMM_ADD = 1 };
+enum GemmMode { GEMM_STORE = 0, GEMM_ADD = 1, GEMM_SWIGLU = 2, GEMM_QKV_ROPE = 3 };
 struct GemmWs {                 // split-K partials + per-tile semaphores (carved from the arena)
   float* ptr;
   size_t bytes;
   int* sem;
   size_t sem_count;
+};
+// Fused-epilogue parameters (tensor-core GEMM only).
+struct GemmEpi {
+  bf16* out; int ldo;                  // SWIGLU: act [M][d_ff]; QKV_ROPE: qkv [M][(Hq+2Hkv) dh]
+  const RowInfo* rows;                 // QKV_ROPE: per-row (slot, j, pos) for RoPE angle and KV slot
+  const float* rcos; const float* rsin;
+  const focus_req_state* st;
+  KVView kv;
+  int n_q_heads;
+  Counters* cnt;
 };
 // a_rows: allocated rows of A (TMA bounds); M_dev/M_max: live / maximum rows of this call.
 void launch_gemm(const bf16* A, int lda, int a_rows, const bf16* W, int N, int K, float* C, int ldc,
@@ -127,7 +137,8 @@ struct AttnArgs {
 };
 void launch_attention(const AttnArgs& a, cudaStream_t s);
 bool attn_tc_supported(int head_dim, int page_size, int group);
-bool attn_tc_make_qmap(const bf16* q, size_t rows, int ld, int group, CUtensorMap* mq);
+bool attn_tc_make_qmap(const bf16* q, size_t rows, int ld, int n_heads, int group, CUtensorMap* mq);
+int attn_tc_rows_per_chunk(int group);
 bool attn_tc_make_maps(const bf16* Kpool, const bf16* Vpool, size_t rows, int head_dim, int page_size,
                        CUtensorMap* mk, CUtensorMap* mv);
 void launch_attention_tc(const CUtensorMap& mk, const CUtensorMap& mv, const CUtensorMap& mq, const AttnArgs& a,

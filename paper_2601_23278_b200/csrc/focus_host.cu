@@ -19,7 +19,8 @@ namespace focus {
 void launch_gemm_simt(const bf16* A, int lda, const bf16* W, int N, int K, float* C, int ldc, const int* M_dev,
                       int M_max, GemmMode mode, cudaStream_t s);
 bool launch_gemm_tc(const bf16* A, int lda, int a_rows, const bf16* W, int N, int K, float* C, int ldc,
-                    const int* M_dev, int M_max, GemmMode mode, const GemmWs& ws, cudaStream_t s);
+                    const int* M_dev, int M_max, GemmMode mode, const GemmWs& ws, cudaStream_t s,
+                    const GemmEpi* epi = nullptr);
 
 void launch_gemm(const bf16* A, int lda, int a_rows, const bf16* W, int N, int K, float* C, int ldc, const int* M_dev,
                  int M_max, GemmMode mode, const GemmWs& ws, cudaStream_t s) {
@@ -232,10 +233,11 @@ void derive(focus_ctx* x) {
   x->kv_pages = pages;
   x->kv_layer_elems = (size_t)pages * c.n_kv_heads * c.page_size * c.head_dim;
   x->attn_tc = attn_tc_supported(c.head_dim, c.page_size, x->G) && getenv("FOCUS_ATTN_SIMT") == nullptr;
-  x->attn_rpc = (x->attn_tc ? 128 : kAttnQRows) / x->G;
+  x->attn_rpc = x->attn_tc ? attn_tc_rows_per_chunk(x->G) : kAttnQRows / x->G;
   x->n_chunks = (x->B + x->attn_rpc - 1) / x->attn_rpc;
-  x->split_tiles = 8;
-  x->max_nsplit = ((c.max_seq_len + 63) / 64 + x->split_tiles - 1) / x->split_tiles + 1;
+  x->split_tiles = 16;                         // 128-key tiles per split (the kernel may enlarge it)
+  if (const char* e = getenv("FOCUS_ATTN_SPLIT_TILES")) x->split_tiles = std::max(2, atoi(e));
+  x->max_nsplit = ((c.max_seq_len + 127) / 128 + x->split_tiles - 1) / x->split_tiles + 1;
   x->nch_vocab = std::max(1, std::min(16, c.vocab / 8192));
   x->mask_id = c.vocab - 1;
   x->max_gen = c.max_seq_len;
@@ -331,10 +333,22 @@ void qkv_piece(focus_ctx* x, int l, int tl, float* xr, const RowSpace& rs) {
   tap(x, tl, TAP_X_IN, xr, (size_t)rs.M_max * c.d_model * 4);
   LAUNCH(RMSNORM, launch_rmsnorm(xr, nullptr, rs.M_dev, rs.M_max, c.d_model, c.rms_eps, x->h, s));
   tap(x, tl, TAP_H, x->h, (size_t)rs.M_max * c.d_model * 2);
-  LAUNCH(GEMM_QKV, launch_gemm(x->h, c.d_model, x->max_rows, x->Wqkv[l], x->qkv_dim, c.d_model, x->f32tmp,
-                               x->qkv_dim, rs.M_dev, rs.M_max, GEMM_STORE, x->gws, s));
-  LAUNCH(ROPE_STORE, launch_rope_store(x->f32tmp, rs.rows, rs.M_dev, rs.M_max, c.n_q_heads, x->rope_cos,
-                                       x->rope_sin, x->st, kv_view(x, l), x->qkv, x->cnt, s));
+  // tensor-core GEMM with the RoPE + paged-KV-store epilogue (head_dim 128); otherwise GEMM -> fp32 ->
+  // k_rope_store
+  GemmEpi e{};
+  e.out = x->qkv; e.ldo = x->qkv_dim; e.rows = rs.rows; e.rcos = x->rope_cos; e.rsin = x->rope_sin;
+  e.st = x->st; e.kv = kv_view(x, l); e.n_q_heads = c.n_q_heads; e.cnt = x->cnt;
+  bool fused = false;
+  LAUNCH(GEMM_QKV, fused = gemm_backend() == 1 &&
+                           launch_gemm_tc(x->h, c.d_model, x->max_rows, x->Wqkv[l], x->qkv_dim, c.d_model, nullptr, 0,
+                                          rs.M_dev, rs.M_max, GEMM_QKV_ROPE, x->gws, s, &e));
+  if (!fused) {
+    --x->launches;                            // the fused attempt launched nothing
+    LAUNCH(GEMM_QKV, launch_gemm(x->h, c.d_model, x->max_rows, x->Wqkv[l], x->qkv_dim, c.d_model, x->f32tmp,
+                                 x->qkv_dim, rs.M_dev, rs.M_max, GEMM_STORE, x->gws, s));
+    LAUNCH(ROPE_STORE, launch_rope_store(x->f32tmp, rs.rows, rs.M_dev, rs.M_max, c.n_q_heads, x->rope_cos,
+                                         x->rope_sin, x->st, kv_view(x, l), x->qkv, x->cnt, s));
+  }
   tap(x, tl, TAP_QKV, x->qkv, (size_t)rs.M_max * x->qkv_dim * 2);
   tap(x, tl, TAP_ROWS, rs.rows, (size_t)rs.M_max * sizeof(RowInfo));
 }
@@ -348,9 +362,19 @@ void out_mlp_piece(focus_ctx* x, int l, int tl, float* xr, const RowSpace& rs) {
   tap(x, tl, TAP_X_MID, xr, (size_t)rs.M_max * c.d_model * 4);
   LAUNCH(RMSNORM, launch_rmsnorm(xr, nullptr, rs.M_dev, rs.M_max, c.d_model, c.rms_eps, x->h, s));
   tap(x, tl, TAP_H2, x->h, (size_t)rs.M_max * c.d_model * 2);
-  LAUNCH(GEMM_GU, launch_gemm(x->h, c.d_model, x->max_rows, x->Wgu[l], 2 * c.d_ff, c.d_model, x->f32tmp,
-                              2 * c.d_ff, rs.M_dev, rs.M_max, GEMM_STORE, x->gws, s));
-  LAUNCH(SILU, launch_silu_mul(x->f32tmp, rs.M_dev, rs.M_max, c.d_ff, x->act, s));
+  // tensor-core GEMM with the SwiGLU epilogue; otherwise GEMM -> fp32 -> k_silu_mul
+  GemmEpi e{};
+  e.out = x->act; e.ldo = c.d_ff;
+  bool fused = false;
+  LAUNCH(GEMM_GU, fused = gemm_backend() == 1 &&
+                          launch_gemm_tc(x->h, c.d_model, x->max_rows, x->Wgu[l], 2 * c.d_ff, c.d_model, nullptr, 0,
+                                         rs.M_dev, rs.M_max, GEMM_SWIGLU, x->gws, s, &e));
+  if (!fused) {
+    --x->launches;
+    LAUNCH(GEMM_GU, launch_gemm(x->h, c.d_model, x->max_rows, x->Wgu[l], 2 * c.d_ff, c.d_model, x->f32tmp,
+                                2 * c.d_ff, rs.M_dev, rs.M_max, GEMM_STORE, x->gws, s));
+    LAUNCH(SILU, launch_silu_mul(x->f32tmp, rs.M_dev, rs.M_max, c.d_ff, x->act, s));
+  }
   tap(x, tl, TAP_ACT, x->act, (size_t)rs.M_max * c.d_ff * 2);
   LAUNCH(GEMM_DOWN, launch_gemm(x->act, c.d_ff, x->max_rows, x->Wd[l], c.d_model, c.d_ff, xr, c.d_model, rs.M_dev,
                                 rs.M_max, GEMM_ADD, x->gws, s));
@@ -482,8 +506,8 @@ focus_status focus_init(const focus_config* cfg, void* dev_arena, size_t arena_b
     cudaMemsetAsync(x->attn_sem, 0, (size_t)c.max_requests * x->n_chunks * c.n_kv_heads * 4, s);
     const size_t rows = (size_t)c.n_layers * x->kv_pages * c.n_kv_heads * c.page_size;
     if (!attn_tc_make_maps(x->Kpool, x->Vpool, rows, c.head_dim, c.page_size, &x->mapK, &x->mapV) ||
-        !attn_tc_make_qmap(x->qkv, x->max_rows, x->qkv_dim, x->G, &x->mapQ_qkv) ||
-        !attn_tc_make_qmap(x->qS, x->max_rows, x->q_dim, x->G, &x->mapQ_qs)) {
+        !attn_tc_make_qmap(x->qkv, x->max_rows, x->qkv_dim, c.n_q_heads, x->G, &x->mapQ_qkv) ||
+        !attn_tc_make_qmap(x->qS, x->max_rows, x->q_dim, c.n_q_heads, x->G, &x->mapQ_qs)) {
       cudaStreamSynchronize(s);
       cudaFreeHost(x->up.host);
       delete x;

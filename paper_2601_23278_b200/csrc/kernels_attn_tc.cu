@@ -1,34 +1,37 @@
 // Block-diffusion paged attention on the 5th-generation tensor cores (tcgen05 / TMEM / TMA), with
 // the Eq.2 token-importance epilogue fused in (§3.1 Eq.2, App.E).
 //
-// Work unit = (request i of the call, query-row chunk, kv head, key split).  The unit's query rows
-// are the G = Hq/Hkv heads of up to 128/G block rows (GQA packing: one K/V stream serves the whole
-// group); they form one M = 128 MMA tile.  Keys (block-diffusion mask):
+// Decode attention here has few query rows per (request, kv head) — the G = Hq/Hkv heads of the
+// retained block rows, ~30-60 at the SDAR-8B shapes — and a long key stream, so the kernel is
+// "swap-AB": keys sit on the MMA M side and query rows on N,
+//     S^T [128 keys x NQ rows] = K_tile [128 x d_h] . Q^T            (tcgen05.mma, A = K, B = Q, K-major)
+//     O^T [d_h x NQ]          += V_tile^T [d_h x 128] . P^T          (A = V as MN-major, B = P^T MN-major)
+// with NQ = the unit's query rows rounded up to 16 (MMA N), so each softmax thread owns one key and
+// every lane does useful work, and the accumulators are tiny (NQ TMEM columns).
+//
+// Work unit = (request i of the call, query-row chunk, kv head, key split): up to 64 query rows
+// (GQA packing: one K/V stream serves the G heads of 64/G block rows).  Keys (block-diffusion mask,
+// P:102-103):
 //   ext_mode 0  context [0, s) + the whole block [s, s+B)          (layer 0, layer-1 suffix; A-K2/A-K3)
 //   ext_mode 1  context + block [s, s+R']                          (layers >= 2; A-K1)
 //   ext_mode 2  causal prefill (row at position p sees [0, p])      (focus_kv_append; A-K5)
 //   imp_only    block keys [s, s+B) only, no output                  (layer-1 importance, A-I8)
-// Keys stream in 64-key tiles straight from the paged pool by TMA (no gather copy); a request's key
-// range is cut into splits of `split_tiles` tiles so the persistent grid stays busy, and split
-// partials (unnormalised O, running max, sum) are merged by the last-arriving split in split order
+// Keys stream in 128-key tiles straight from the paged pool by TMA (no gather copy).  A request's
+// tiles are cut into balanced splits so the persistent grid stays busy; split partials
+// (unnormalised O, running max, sum) are merged by the last-arriving split in split order
 // (deterministic).
 //
 // Persistent CTA (one per SM), 384 threads, warp-specialised:
-//   warp 0 / 2  TMA producers: K tiles / V tiles (64 keys x head_dim, 128-B swizzle) into a 4-slot K
-//               ring (freed when QK^T completes) and a 3-slot V ring (freed when PV completes)
-//   warp 1      MMA issuer: S = Q K^T (M=128, N=64, K=head_dim) into a double-buffered TMEM S tile,
-//               then O += P V (M=128, N=head_dim, K=64; V as an MN-major operand) into a
-//               double-buffered TMEM O accumulator (one buffer per unit in flight)
-//   warp 3      TMEM allocator + Q loader: cp.async of the unit's q rows into a swizzled smem tile (double-buffered)
-//   warps 4-7   softmax: warp 4+q owns TMEM lane quadrant q and reads its (<= 32) real rows 16 lanes
-//               at a time (16x256b shape: 4 threads per row, 16 columns each); online softmax in the
-//               log2 domain with lazy O rescaling (only when the running max grows by > 8), P -> a
-//               double-buffered smem tile as bf16; block-column scores -> per-CTA scratch for the
-//               importance epilogue
-//   warps 8-11  epilogue: O / l -> bf16 output rows (or split partials + fixed-order merge)
-// Q tile lane L = g * (128/G) + r holds query head g of block row r (G <= 4), so with G = 4 every TMEM
-// lane quadrant (SM sub-partition) gets one head's rows and the ~30-60 real rows of a decode unit
-// keep all four softmax warps busy.
+//   warp 0 / 2  TMA producers: K tiles / V tiles (128 keys x 128, 128-B swizzle), 2-slot rings each
+//               (K is freed when QK^T completes, V when PV completes)
+//   warp 1      MMA issuer (one thread): S^T into a double-buffered TMEM tile, O^T += V^T P^T into a
+//               double-buffered TMEM accumulator (one per unit in flight)
+//   warp 3      TMEM allocator + Q loader (one 3-D TMA box per 64-column half: rows n = r*G + g)
+//   warps 4-7   softmax, thread = key: online softmax in the log2 domain with a lazy running max
+//               (the max only moves when a score exceeds it by > 2^8; then a cross-warp max, O^T
+//               column rescale and sum rescale), P^T -> double-buffered smem as bf16; block-column
+//               scores -> per-CTA scratch and the Eq.2 epilogue
+//   warps 8-11  epilogue, thread = d_h lane of O^T: O/l -> bf16 rows (or split partials + merge)
 #include <math_constants.h>
 
 #include "tc_ptx.cuh"
@@ -38,56 +41,64 @@ namespace attn {
 
 using namespace tc;
 
-constexpr int KT = 64;            // keys per tile
-constexpr int QR = 128;           // query rows per unit (MMA M)
-constexpr int SK = 4;             // K ring slots (released when QK^T completes)
-constexpr int SV = 3;             // V ring slots (released when PV completes)
+constexpr int DH = 128;           // head_dim of the tensor-core path
+constexpr int KT = 128;           // keys per tile (MMA M)
+constexpr int NQM = 64;           // max query rows per unit (MMA N)
+constexpr int SK = 2;             // K ring slots
+constexpr int SV = 2;             // V ring slots
+constexpr int UCAP = 40;          // unit descriptors per CTA kept in smem
 constexpr int NTHREADS = 384;
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kRescaleThresh = 8.0f;   // log2 units
 
-template <int DH>
-struct Cfg {
-  static constexpr int NH = DH / 64;                  // 64-column (128-B) halves of head_dim
-  static constexpr int HALF_BYTES = QR * 128;         // one half of the Q tile (16 KB)
-  static constexpr int Q_BYTES = NH * HALF_BYTES;
-  static constexpr int KH_BYTES = KT * 128;           // one half of a K or V tile (8 KB)
-  static constexpr int K_BYTES = NH * KH_BYTES;
-  static constexpr int P_BYTES = QR * KT * 2;         // 16 KB
-  static constexpr int TMEM_COLS = (2 * DH + 2 * KT) <= 256 ? 256 : 512;
-  static constexpr int O_COL = 0;                     // O buffers at [0, DH), [DH, 2DH)
-  static constexpr int S_COL = 2 * DH;                // S buffers at [2DH, 2DH+KT), [2DH+KT, 2DH+2KT)
-  static constexpr uint32_t IDESC_QK = idesc_bf16(QR, KT, false, false);
-  static constexpr uint32_t IDESC_PV = idesc_bf16(QR, DH, false, true);
-  static constexpr int OFF_Q = 0;
-  static constexpr int OFF_K = OFF_Q + 2 * Q_BYTES;
-  static constexpr int OFF_V = OFF_K + SK * K_BYTES;
-  static constexpr int OFF_P = OFF_V + SV * K_BYTES;
-  static constexpr int OFF_BAR = OFF_P + 2 * P_BYTES;
-  static constexpr int N_BARS = 2 * SK + 2 * SV + 9 * 2;
-  static constexpr int OFF_STAT = OFF_BAR + 8 * N_BARS + 8;
-  static constexpr int OFF_RED = OFF_STAT + 2 * QR * 8;
-  static constexpr int OFF_PRE = OFF_RED + 4 * kMaxB * 4;
-  static constexpr int SMEM_BYTES = OFF_PRE + 2 * 1028 * 4 + 64 + 1024;
+constexpr int HALF_Q = NQM * 128;               // 8 KB: one 64-column half of the Q tile
+constexpr int Q_BYTES = 2 * HALF_Q;             // 16 KB
+constexpr int HALF_KV = KT * 128;               // 16 KB: one 64-column half of a K / V tile
+constexpr int KV_BYTES = 2 * HALF_KV;           // 32 KB
+constexpr int P_CHUNK = (KT / 8) * 128;         // 2 KB: 8 query rows x 128 keys of P^T
+constexpr int P_BYTES = (NQM / 8) * P_CHUNK;    // 16 KB
+constexpr int TMEM_COLS = 512;
+constexpr int O_COL = 0;                        // O^T buffers [0, 64), [64, 128)
+constexpr int S_COL = 2 * NQM;                  // S^T buffers [128, 192), [192, 256)
+constexpr int L_COL = 4 * NQM;                  // row-sum buffers [256, 320), [320, 384): ONES . P^T
+constexpr int MAXS = 16;                        // split partials merged through smem
+constexpr int OFF_Q = 0;
+constexpr int OFF_K = OFF_Q + 2 * Q_BYTES;
+constexpr int OFF_V = OFF_K + SK * KV_BYTES;
+constexpr int OFF_P = OFF_V + SV * KV_BYTES;
+constexpr int OFF_BAR = OFF_P + 2 * P_BYTES;
+constexpr int N_BARS = 2 * SK + 2 * SV + 2 * 9;
+constexpr int OFF_MISC = OFF_BAR + 8 * N_BARS + 16;
+constexpr int OFF_M = OFF_MISC;                 // float [NQM] running max (log2 units)
+constexpr int OFF_ALPHA = OFF_M + NQM * 4;      // float [NQM]
+constexpr int OFF_THR = OFF_ALPHA + NQM * 4;    // float [NQM] raw-score rescale threshold (+inf: padding row)
+constexpr int OFF_NM = OFF_THR + NQM * 4;       // float [NQM] -m (0 while m = -inf)
+constexpr int OFF_STAT = OFF_NM + NQM * 4;      // float [2][NQM] m for the epilogue (split merge)
+constexpr int OFF_RED = OFF_STAT + 2 * NQM * 4; // float [4][64]
+constexpr int OFF_FLAG = OFF_RED + 4 * 64 * 4;  // int [2][4]
+constexpr int OFF_ONES = OFF_FLAG + 64;         // 128 B of bf16 ones (A operand of the row-sum MMA)
+constexpr int OFF_MERGE = OFF_ONES + 128;       // float [MAXS + 1][NQM] split-merge scales + 1/l
+constexpr int OFF_UTAB = OFF_MERGE + (MAXS + 1) * NQM * 4;
+constexpr int SMEM_BYTES = OFF_UTAB + UCAP * 80 + 1024;
+
+struct Unit {
+  int i, chunk, kvh, sp, nsplit, slot, r0, nr, nq, kbeg, kend, t_lo, t_hi, s0, pos_base, pair;
+  uint64_t P;
+  int want_imp, pad;
 };
+static_assert(sizeof(Unit) == 80, "unit descriptor size");
 
 // debug trace: role r of this CTA appends clock64 stamps (event kind in the top 8 bits)
 struct Tracer {
   unsigned long long* p;
   int n;
-  __device__ __forceinline__ Tracer(unsigned long long* base, int role) : p(base ? base + ((size_t)blockIdx.x * 8 + role) * kTraceEv : nullptr), n(0) {}
+  __device__ __forceinline__ Tracer(unsigned long long* base, int role)
+      : p(base ? base + ((size_t)blockIdx.x * 8 + role) * kTraceEv : nullptr), n(0) {}
   __device__ __forceinline__ void ev(int kind) {
     if (p && n < kTraceEv) p[n++] = ((unsigned long long)kind << 56) | (clock64() & ((1ull << 56) - 1));
   }
 };
 
-struct Unit {
-  int i, chunk, kvh, sp, nsplit, slot, r0, nr, nq, kbeg, kend, t_lo, t_hi, s0, pos_base, pair;
-  uint64_t P;
-  bool want_imp;
-};
-
-// Tiles [t0, t1) of request list index i (or the prefill chunk) and its split count.
 __device__ __forceinline__ void key_range(const AttnArgs& a, int i, int& kbeg, int& kend, int& s0) {
   const focus_req_state& s = a.st[a.req_list[i]];
   s0 = s.s;
@@ -95,7 +106,7 @@ __device__ __forceinline__ void key_range(const AttnArgs& a, int i, int& kbeg, i
   else { kbeg = 0; kend = a.ext_mode == 0 ? s.s + a.B : s.s + s.R_new + 1; }
 }
 
-__device__ __forceinline__ int req_units(const AttnArgs& a, int i, int rpc, int& nsplit) {
+__device__ __forceinline__ int req_units(const AttnArgs& a, int i, int rpc, int tps, int& nsplit) {
   const int rows = a.row_off[i + 1] - a.row_off[i];
   nsplit = 0;
   if (rows <= 0) return 0;
@@ -104,13 +115,11 @@ __device__ __forceinline__ int req_units(const AttnArgs& a, int i, int rpc, int&
   int kbeg, kend, s0;
   key_range(a, i, kbeg, kend, s0);
   const int nt = (kend + KT - 1) / KT - kbeg / KT;
-  nsplit = a.imp_only ? 1 : (nt + a.split_tiles - 1) / a.split_tiles;
-  const int nch = (rows + rpc - 1) / rpc;
-  return nch * a.kv.n_kv_heads * nsplit;
+  nsplit = a.imp_only ? 1 : min(MAXS, (nt + tps - 1) / tps);
+  return ((rows + rpc - 1) / rpc) * a.kv.n_kv_heads * nsplit;
 }
 
-__device__ __forceinline__ Unit decode_unit(const AttnArgs& a, int u, const int* pre, const int* nsp, int n_ent, int G,
-                                            int rpc) {
+__device__ Unit decode_unit(const AttnArgs& a, int u, const int* pre, const int* nsp, int n_ent, int G, int rpc) {
   Unit x;
   const int H = a.kv.n_kv_heads;
   if (a.ext_mode == 2) {
@@ -126,7 +135,7 @@ __device__ __forceinline__ Unit decode_unit(const AttnArgs& a, int u, const int*
     x.kend = a.prefill_pos0 + x.r0 + x.nr;
     x.s0 = 0;
     x.P = 0;
-    x.want_imp = false;
+    x.want_imp = 0;
     x.pos_base = a.prefill_pos0 + x.r0;
   } else {
     int lo = 0, hi = n_ent - 1;                        // largest i with pre[i] <= u
@@ -157,21 +166,263 @@ __device__ __forceinline__ Unit decode_unit(const AttnArgs& a, int u, const int*
   x.t_lo = t0 + (x.sp * nt) / x.nsplit;
   x.t_hi = t0 + ((x.sp + 1) * nt) / x.nsplit;
   x.pair = (x.i * a.n_chunks + x.chunk) * H + x.kvh;
+  x.pad = 0;
   return x;
 }
 
-template <int DH, bool IMP_ONLY>
+// Transposed butterfly over a warp: on entry lane l holds v[0..31] (one value per row); on exit
+// lane j holds op-reduce over the 32 lanes of row j.  31 shuffles for 32 rows.
+template <bool MAX>
+__device__ __forceinline__ float warp_transpose_reduce(float (&v)[32], int lane) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    const bool up = (lane & o) != 0;
+#pragma unroll
+    for (int i = 0; i < o; ++i) {
+      const float send = up ? v[i] : v[i + o];
+      const float keep = up ? v[i + o] : v[i];
+      const float recv = __shfl_xor_sync(0xffffffffu, send, o);
+      v[i] = MAX ? fmaxf(keep, recv) : keep + recv;
+    }
+  }
+  return v[0];
+}
+
+// ---------------------------------------------------------------- softmax warps
+struct SoftSmem {
+  float* m;          // [NQM] running max (log2 units)
+  float* alpha;      // [NQM] rescale factor of the current tile
+  float* thr;        // [NQM] raw-score threshold above which the running max must move
+  float* nm;         // [NQM] -m (0 while m = -inf)
+  float* stat;       // [2][NQM] m of the finished unit (split merge)
+  float* red;        // [4][64]
+  int* flags;        // [2][4]
+  uint8_t* sP;
+  uint64_t *sfull, *sfree, *pfull, *pvdone, *ofree, *statfull;
+};
+struct SoftThread {
+  int L, lane, q4, G;
+  uint32_t tmem, lane_base;
+  float sl2;
+  float* scr;
+};
+
+// One unit on the softmax warps (thread = key lane L of each 128-key tile).  NCH = 16-row chunks of
+// query rows.  Per tile: (1) does any score exceed its row threshold (running max + 2^8)?  (rare after
+// the first tile) -> exact tile max per row, new running max, O^T / L^T column rescale; (2) P^T =
+// exp2(s * scale * log2e - m) in bf16 into the P^T buffer.  Row sums come from the tensor core.
+template <int NCH, bool CAUSAL, bool IMP_ONLY>
+__device__ __forceinline__ void softmax_unit(const AttnArgs& a, const Unit& xr, int it, uint32_t& g,
+                                             const SoftThread& th, const SoftSmem& ss, Tracer& tr) {
+  const int L = th.L, lane = th.lane, nq = xr.nq;
+  const uint32_t ob = it & 1;
+  named_bar(1, 128);                               // previous unit's readers of m/thr/nm are done
+  if (L < NQM) {
+    ss.m[L] = -CUDART_INF_F;
+    ss.thr[L] = L < nq ? -CUDART_INF_F : CUDART_INF_F;
+    ss.nm[L] = 0.f;
+  }
+  named_bar(1, 128);
+  for (int t = xr.t_lo; t < xr.t_hi; ++t, ++g) {
+    const uint32_t sb = g & 1, pb = g & 1;
+    mbar_wait(&ss.sfull[sb], (g >> 1) & 1);
+    tr.ev(1);
+    tc_fence_after();
+    const int k = t * KT + L;
+    const bool kvalid = k >= xr.kbeg && k < xr.kend;
+    const uint32_t sbase = th.tmem + th.lane_base + S_COL + sb * NQM;
+    uint32_t r[NCH][16];
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) tmem_ld32x16(sbase + 16 * c, r[c]);
+    tmem_wait_ld();
+    tc_fence_before();                             // S^T is in registers: the tile may be overwritten
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&ss.sfree[sb]);
+    // ---- (1) threshold check
+    bool need = false;
+    if (kvalid) {
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) {
+#pragma unroll
+        for (int e4 = 0; e4 < 16; e4 += 4) {
+          const float4 t4 = *reinterpret_cast<const float4*>(ss.thr + 16 * c + e4);
+          const float tv[4] = {t4.x, t4.y, t4.z, t4.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const bool vis = !CAUSAL || k <= xr.pos_base + (16 * c + e4 + e) / th.G;
+            need |= vis && __uint_as_float(r[c][e4 + e]) > tv[e];
+          }
+        }
+      }
+    }
+    if (xr.want_imp && kvalid && k >= xr.s0 && k < xr.s0 + a.B) {   // block-column scores (Eq.2 epilogue)
+#pragma unroll
+      for (int c = 0; c < NCH; ++c)
+#pragma unroll
+        for (int e = 0; e < 16; ++e)
+          if (16 * c + e < nq) th.scr[(16 * c + e) * kMaxB + (k - xr.s0)] = __uint_as_float(r[c][e]) * a.scale;
+    }
+    if (IMP_ONLY) continue;
+    const int anyw = __any_sync(0xffffffffu, need);
+    if (lane == 0) ss.flags[(g & 1) * 4 + th.q4] = anyw;
+    named_bar(1, 128);
+    const int* fl = ss.flags + (g & 1) * 4;
+    if (fl[0] | fl[1] | fl[2] | fl[3]) {
+      // ---- slow path: exact tile max per row (transposed butterfly + 4-warp combine)
+#pragma unroll
+      for (int rd = 0; rd < (NCH + 1) / 2; ++rd) {
+        float v[32];
+#pragma unroll
+        for (int cc = 0; cc < 2; ++cc) {
+          const int c = rd * 2 + cc;
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            bool ok = c < NCH && kvalid;
+            if (CAUSAL) ok = ok && k <= xr.pos_base + (16 * c + e) / th.G;
+            v[cc * 16 + e] = ok ? __uint_as_float(r[c < NCH ? c : 0][e]) * th.sl2 : -CUDART_INF_F;
+          }
+        }
+        ss.red[th.q4 * 64 + rd * 32 + lane] = warp_transpose_reduce<true>(v, lane);
+      }
+      named_bar(1, 128);
+      if (L < NQM) {
+        float al = 1.f;
+        if (L < nq && L < NCH * 16) {
+          const float mt = fmaxf(fmaxf(ss.red[L], ss.red[64 + L]), fmaxf(ss.red[128 + L], ss.red[192 + L]));
+          const float mo = ss.m[L];
+          if (mt > mo + kRescaleThresh || (mo == -CUDART_INF_F && mt > -CUDART_INF_F)) {
+            const float mn = fmaxf(mt, mo);
+            al = ex2(mo - mn);                     // 0 when mo = -inf
+            ss.m[L] = mn;
+            ss.nm[L] = -mn;
+            ss.thr[L] = (mn + kRescaleThresh) / th.sl2;
+          }
+        }
+        ss.alpha[L] = al;
+      }
+      named_bar(1, 128);
+      if (t > xr.t_lo) {                           // O^T and L^T columns *= alpha (PV of tile g-1 done)
+        mbar_wait(&ss.pvdone[(g - 1) & 1], ((g - 1) >> 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int buf = 0; buf < 2; ++buf) {
+          const uint32_t base = th.tmem + th.lane_base + (buf == 0 ? O_COL : L_COL) + ob * NQM;
+#pragma unroll
+          for (int c = 0; c < NCH; ++c) {
+            uint32_t q[16];
+            tmem_ld32x16(base + 16 * c, q);
+            tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 16; ++e) q[e] = __float_as_uint(__uint_as_float(q[e]) * ss.alpha[16 * c + e]);
+            tmem_st32x16(base + 16 * c, q);
+          }
+        }
+        tmem_wait_st();
+      }
+    }
+    // ---- (2) P^T = exp2(s * scale*log2e - m) as bf16 into the MN-major P^T buffer
+    tr.ev(2);
+    if (g >= 2) mbar_wait(&ss.pvdone[pb], ((g >> 1) & 1) ^ 1);   // PV of tile g-2 done: buffer free
+    tr.ev(3);
+    const uint32_t pdst = smem_u32(ss.sP + pb * P_BYTES) + (L >> 3) * 128 + (L & 7) * 16;
+    if (kvalid) {
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) {
+        uint32_t pk[8];
+#pragma unroll
+        for (int e4 = 0; e4 < 16; e4 += 4) {
+          const float4 n4 = *reinterpret_cast<const float4*>(ss.nm + 16 * c + e4);
+          const float nv[4] = {n4.x, n4.y, n4.z, n4.w};
+          float p[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            p[e] = ex2(fmaf(__uint_as_float(r[c][e4 + e]), th.sl2, nv[e]));
+            if (CAUSAL && k > xr.pos_base + (16 * c + e4 + e) / th.G) p[e] = 0.f;
+          }
+          const __nv_bfloat162 b0 = __floats2bfloat162_rn(p[0], p[1]);
+          const __nv_bfloat162 b1 = __floats2bfloat162_rn(p[2], p[3]);
+          pk[e4 / 2] = *reinterpret_cast<const uint32_t*>(&b0);
+          pk[e4 / 2 + 1] = *reinterpret_cast<const uint32_t*>(&b1);
+        }
+        sts128(pdst + (2 * c) * P_CHUNK, make_uint4(pk[0], pk[1], pk[2], pk[3]));
+        sts128(pdst + (2 * c + 1) * P_CHUNK, make_uint4(pk[4], pk[5], pk[6], pk[7]));
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) {
+        sts128(pdst + (2 * c) * P_CHUNK, make_uint4(0, 0, 0, 0));
+        sts128(pdst + (2 * c + 1) * P_CHUNK, make_uint4(0, 0, 0, 0));
+      }
+    }
+    tc_fence_before();
+    fence_proxy_async();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&ss.pfull[pb]);
+    tr.ev(4);
+  }
+  if (!IMP_ONLY) {
+    mbar_wait(&ss.ofree[ob], ((it >> 1) & 1) ^ 1);   // epilogue of unit it-2 is done with stat[ob]
+    tr.ev(5);
+    if (L < NQM) ss.stat[ob * NQM + L] = ss.m[L];
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&ss.statfull[ob]);
+  }
+}
+
+// Eq.2 on the block scores of the unit (scratch rows = query rows n = r*G + g): per row MaxPool1D
+// (k = mp_kernel, -inf outside P; A-I3, A-I5), softmax over P, then the sum over rows and heads in a
+// fixed order (lanes, then warps) -> one partial per (request, chunk, kv head).
+__device__ __noinline__ void importance_epilogue(const AttnArgs& a, const Unit& xr, const SoftThread& th,
+                                                 const SoftSmem& ss) {
+  named_bar(1, 128);                               // all block scores of the unit are in scratch
+  const int B = a.B, rad = a.mp_kernel / 2, L = th.L, lane = th.lane;
+  const uint64_t P = xr.P;
+  const bool rr = L < xr.nq;
+  const float* sc = th.scr + L * kMaxB;
+  float w[kMaxB];
+  float mx = -CUDART_INF_F;
+  if (rr) {
+    for (int j = 0; j < B; ++j) {
+      float v = -CUDART_INF_F;
+      if ((P >> j) & 1ull) {
+        const int lo = max(0, j - rad), hi = min(B - 1, j + rad);
+        for (int jj = lo; jj <= hi; ++jj)
+          if ((P >> jj) & 1ull) v = fmaxf(v, sc[jj]);
+      }
+      w[j] = v;
+      mx = fmaxf(mx, v);
+    }
+    float z = 0.f;
+    for (int j = 0; j < B; ++j) {
+      const float e = w[j] == -CUDART_INF_F ? 0.f : expf(w[j] - mx);
+      w[j] = e;
+      z += e;
+    }
+    for (int j = 0; j < B; ++j) w[j] = w[j] / z;
+  }
+  for (int j = 0; j < B; ++j) {
+    float v = rr ? w[j] : 0.f;
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) ss.red[th.q4 * 64 + j] = v;
+  }
+  named_bar(1, 128);
+  if (th.q4 == 0)
+    for (int j = lane; j < B; j += 32)
+      a.imp[(size_t)xr.pair * B + j] = ((ss.red[j] + ss.red[64 + j]) + ss.red[128 + j]) + ss.red[192 + j];
+  named_bar(1, 128);                               // red[] reuse
+}
+
+template <bool IMP_ONLY>
 __global__ void __launch_bounds__(NTHREADS, 1)
     k_attn_tc(const __grid_constant__ CUtensorMap mapK, const __grid_constant__ CUtensorMap mapV,
               const __grid_constant__ CUtensorMap mapQ, AttnArgs a) {
-  using C = Cfg<DH>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  uint8_t* sQ = smem + C::OFF_Q;
-  uint8_t* sK = smem + C::OFF_K;
-  uint8_t* sV = smem + C::OFF_V;
-  uint8_t* sP = smem + C::OFF_P;
-  uint64_t* bars = (uint64_t*)(smem + C::OFF_BAR);
+  uint8_t* sQ = smem + OFF_Q;
+  uint8_t* sK = smem + OFF_K;
+  uint8_t* sV = smem + OFF_V;
+  uint8_t* sP = smem + OFF_P;
+  uint64_t* bars = (uint64_t*)(smem + OFF_BAR);
   uint64_t* kfull = bars;                  // [SK]
   uint64_t* kempty = kfull + SK;           // [SK]
   uint64_t* vfull = kempty + SK;           // [SV]
@@ -179,84 +430,101 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   uint64_t* qfull = vempty + SV;           // [2]
   uint64_t* qempty = qfull + 2;            // [2]
   uint64_t* sfull = qempty + 2;            // [2]
-  uint64_t* sfree = sfull + 2;             // [2]
-  uint64_t* pfull = sfree + 2;             // [2] (per P buffer)
-  uint64_t* pvdone = pfull + 2;            // [2] (per P buffer)
+  uint64_t* sfree = sfull + 2;             // [2]  (4 softmax warps)
+  uint64_t* pfull = sfree + 2;             // [2]  (4 softmax warps)
+  uint64_t* pvdone = pfull + 2;            // [2]
   uint64_t* ofull = pvdone + 2;            // [2]
-  uint64_t* ofree = ofull + 2;             // [2]
-  uint64_t* statfull = ofree + 2;          // [2]
-  uint32_t* tmem_sh = (uint32_t*)(bars + C::N_BARS);
+  uint64_t* ofree = ofull + 2;             // [2]  (4 epilogue warps)
+  uint64_t* statfull = ofree + 2;          // [2]  (4 softmax warps)
+  uint32_t* tmem_sh = (uint32_t*)(bars + N_BARS);
   int* flag_sh = (int*)(tmem_sh + 1);
-  float2* stat = (float2*)(smem + C::OFF_STAT);   // [2][QR] (m_used, l)
-  float* red = (float*)(smem + C::OFF_RED);       // [4][64]
-  int* pre = (int*)(smem + C::OFF_PRE);           // [n_ent + 1]
-  int* nsp = pre + 1028;                          // [n_ent]
+  SoftSmem ss;
+  ss.m = (float*)(smem + OFF_M);
+  ss.alpha = (float*)(smem + OFF_ALPHA);
+  ss.thr = (float*)(smem + OFF_THR);
+  ss.nm = (float*)(smem + OFF_NM);
+  ss.stat = (float*)(smem + OFF_STAT);
+  ss.red = (float*)(smem + OFF_RED);
+  ss.flags = (int*)(smem + OFF_FLAG);
+  ss.sP = sP;
+  ss.sfull = sfull; ss.sfree = sfree; ss.pfull = pfull; ss.pvdone = pvdone; ss.ofree = ofree; ss.statfull = statfull;
+  float* merge = (float*)(smem + OFF_MERGE);
+  uint16_t* ones = (uint16_t*)(smem + OFF_ONES);
+  Unit* utab = (Unit*)(smem + OFF_UTAB);
+  int* pre = (int*)sP;                     // setup only (aliases the P^T buffers)
+  int* nsp = pre + 1028;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int H = a.kv.n_kv_heads;
   const int G = a.n_q_heads / H;
-  const int rpc = QR / G;
+  const int rpc = NQM / G;
 
-  // ---- unit table: per-request unit counts and their exclusive prefix (smem)
+  // ---- unit table: per-request unit counts, exclusive prefix, then this CTA's unit descriptors
   const int n_ent = a.ext_mode == 2 ? 1 : a.n_req;
-  if (a.ext_mode == 2) {
-    if (threadIdx.x == 0) {
-      nsp[0] = 1;
-      pre[0] = 0;
-      pre[1] = ((a.prefill_rows + rpc - 1) / rpc) * H;
+  int tps = max(2, a.split_tiles);
+  int total;
+  for (;;) {
+    if (a.ext_mode == 2) {
+      if (threadIdx.x == 0) { nsp[0] = 1; pre[1] = ((a.prefill_rows + rpc - 1) / rpc) * H; }
+    } else {
+      for (int i = threadIdx.x; i < n_ent; i += NTHREADS) {
+        int ns;
+        pre[i + 1] = req_units(a, i, rpc, tps, ns);
+        nsp[i] = ns;
+      }
     }
-  } else {
-    for (int i = threadIdx.x; i < n_ent; i += NTHREADS) {
-      int ns;
-      const int nu = req_units(a, i, rpc, ns);
-      nsp[i] = ns;
-      pre[i + 1] = nu;
+    __syncthreads();
+    if (warp == 0) {                               // exclusive scan of unit counts
+      const int per = (n_ent + 31) / 32;
+      const int b0 = min(n_ent, lane * per), b1 = min(n_ent, b0 + per);
+      int loc = 0;
+      for (int i = b0; i < b1; ++i) loc += pre[i + 1];
+      int inc = loc;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += v;
+      }
+      int run = inc - loc;
+      for (int i = b0; i < b1; ++i) { const int c = pre[i + 1]; pre[i] = run; run += c; }
+      if (lane == 31) pre[n_ent] = inc;
     }
+    __syncthreads();
+    total = pre[n_ent];
+    if (total <= UCAP * (int)gridDim.x || a.ext_mode == 2 || a.imp_only || tps >= (1 << 20)) break;
+    tps *= 2;                                      // too many units for the descriptor table
+    __syncthreads();
   }
+  const int n_my = total > (int)blockIdx.x ? min(UCAP, (total - 1 - (int)blockIdx.x) / (int)gridDim.x + 1) : 0;
+  for (int k = threadIdx.x; k < n_my; k += NTHREADS)
+    utab[k] = decode_unit(a, blockIdx.x + k * gridDim.x, pre, nsp, n_ent, G, rpc);
+  if (threadIdx.x < 64) ones[threadIdx.x] = 0x3F80;   // bf16 1.0
   if (threadIdx.x == 0) {
     for (int i = 0; i < SK; ++i) { mbar_init(&kfull[i], 1); mbar_init(&kempty[i], 1); }
     for (int i = 0; i < SV; ++i) { mbar_init(&vfull[i], 1); mbar_init(&vempty[i], 1); }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&qfull[i], 1); mbar_init(&qempty[i], 1);
       mbar_init(&sfull[i], 1); mbar_init(&sfree[i], 4);
+      mbar_init(&pfull[i], 4); mbar_init(&pvdone[i], 1);
       mbar_init(&ofull[i], 1); mbar_init(&ofree[i], 4);
       mbar_init(&statfull[i], 4);
     }
-    for (int i = 0; i < 2; ++i) { mbar_init(&pfull[i], 4); mbar_init(&pvdone[i], 1); }
     fence_barrier_init();
   }
+  fence_proxy_async();                             // the ones block is read by the tensor core
   if (warp == 1 && lane == 0) {
     prefetch_map(&mapQ);
     prefetch_map(&mapK);
     if (!IMP_ONLY) prefetch_map(&mapV);
   }
-  if (warp == 3) tmem_alloc<C::TMEM_COLS>(tmem_sh);
+  if (warp == 3) tmem_alloc<TMEM_COLS>(tmem_sh);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (a.ext_mode != 2 && warp == 0) {             // exclusive scan of unit counts (warp 0)
-    const int per = (n_ent + 31) / 32;
-    const int b0 = min(n_ent, lane * per), b1 = min(n_ent, b0 + per);
-    int loc = 0;
-    for (int i = b0; i < b1; ++i) loc += pre[i + 1];
-    int inc = loc;
-    for (int o = 1; o < 32; o <<= 1) {
-      const int v = __shfl_up_sync(0xffffffffu, inc, o);
-      if (lane >= o) inc += v;
-    }
-    int run = inc - loc;
-    for (int i = b0; i < b1; ++i) { const int c = pre[i + 1]; pre[i] = run; run += c; }
-    if (lane == 31) pre[n_ent] = inc;
-  }
-  __syncthreads();
   if (threadIdx.x == 0 && a.trace) a.trace[((size_t)blockIdx.x * 8 + 7) * kTraceEv] = clock64();
-  const int total = pre[n_ent];
   const uint32_t tmem = *tmem_sh;
 
   if (warp == 0 || (warp == 2 && !IMP_ONLY)) {
-    // ================================================================ TMA producers
-    // warp 0 lane 0 streams K tiles, warp 2 lane 0 streams V tiles (separate rings: K is consumed by
-    // QK^T about two tiles before V is consumed by PV, so each ring prefetches its own distance)
+    // ================================================================ TMA producers (K / V)
     if (lane == 0) {
       const bool isK = warp == 0;
       const int NS = isK ? SK : SV;
@@ -267,447 +535,281 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       const int ps = a.kv.page_size;
       const int pr = min(ps, KT);                  // keys per TMA box
       const size_t layer_rows = (size_t)a.kv_pages * H * ps;
-      uint32_t g = 0;
       Tracer tr(a.trace, isK ? 0 : 1);
-      for (int u = blockIdx.x; u < total; u += gridDim.x) {
+      uint32_t g = 0;
+      for (int k = 0; k < n_my; ++k) {
+        const Unit& x = utab[k];
         tr.ev(0);
-        const Unit x = decode_unit(a, u, pre, nsp, n_ent, G, rpc);
-        tr.ev(9);
         for (int t = x.t_lo; t < x.t_hi; ++t, ++g) {
           const int slot = g % NS;
           mbar_wait(&emptyb[slot], ((g / NS) & 1) ^ 1);
           tr.ev(1);
-          mbar_expect_tx(&fullb[slot], C::K_BYTES);
-          uint8_t* dst = ring + slot * C::K_BYTES;
+          mbar_expect_tx(&fullb[slot], KV_BYTES);
+          uint8_t* dst = ring + slot * KV_BYTES;
           for (int pc = 0; pc < KT / pr; ++pc) {
             const int pos = t * KT + pc * pr;
             const int pidx = min(pos / ps, a.kv.max_pages - 1);
             const int page = a.kv.page_table[(size_t)x.slot * a.kv.max_pages + pidx];
             const int row = (int)((size_t)a.layer * layer_rows + ((size_t)page * H + x.kvh) * ps + pos % ps);
-#pragma unroll
-            for (int h = 0; h < C::NH; ++h) tma_load_2d(dst + h * C::KH_BYTES + pc * pr * 128, map, &fullb[slot], h * 64, row);
+            tma_load_2d(dst + pc * pr * 128, map, &fullb[slot], 0, row);
+            tma_load_2d(dst + HALF_KV + pc * pr * 128, map, &fullb[slot], 64, row);
           }
         }
       }
     }
   } else if (warp == 1) {
     // ================================================================ MMA issuer
+    // Two cursors over the CTA's flattened tile sequence: QK^T runs up to two tiles ahead of PV (the
+    // S^T tile is double-buffered and freed as soon as the softmax has read it), so the K ring is
+    // released early and the TMA keeps streaming while the softmax works.
     if (lane == 0) {
-      uint32_t g = 0, it = 0;
-      // deferred PV of the previous tile (issued after the next QK so softmax overlaps the tensor pipe)
-      bool pend = false;
-      uint32_t p_g = 0, p_ob = 0, p_it = 0;
-      bool p_first = false, p_last = false;
-      auto issue_pv = [&]() {
-        const uint32_t pb = p_g & 1;
-        mbar_wait(&pfull[pb], (p_g >> 1) & 1);
-        if (p_first) mbar_wait(&ofree[p_ob], ((p_it >> 1) & 1) ^ 1);
+      Tracer tr(a.trace, 2);
+      int qu = 0, qt = n_my > 0 ? utab[0].t_lo : 0;   // QK cursor (unit, tile)
+      int pu = 0, pt = qt;                            // PV cursor
+      uint32_t qg = 0, pg = 0;
+      auto qk_ready = [&]() { return qu < n_my; };
+      auto issue_qk = [&]() {
+        const Unit& x = utab[qu];
+        const uint32_t ob = qu & 1;
+        if (qt == x.t_lo) {
+          mbar_wait(&qfull[ob], (qu >> 1) & 1);
+          tr.ev(2);
+        }
+        const uint32_t ks = qg % SK, sb = qg & 1;
+        mbar_wait(&kfull[ks], (qg / SK) & 1);
+        mbar_wait(&sfree[sb], ((qg >> 1) & 1) ^ 1);
         tc_fence_after();
-        const uint32_t d = tmem + C::O_COL + p_ob * DH;
-        const uint32_t pa = smem_u32(sP + pb * C::P_BYTES);
-        const uint32_t vs = p_g % SV;
-        mbar_wait(&vfull[vs], (p_g / SV) & 1);
-        tc_fence_after();
-        const uint32_t vb = smem_u32(sV + vs * C::K_BYTES);
+        const int NQ = (x.nq + 15) & ~15;
+        const uint32_t idesc_qk = idesc_bf16(KT, NQ, false, false);
+        const uint32_t qa = smem_u32(sQ + ob * Q_BYTES);
+        const uint32_t kb = smem_u32(sK + ks * KV_BYTES);
+        const uint32_t d = tmem + S_COL + sb * NQM;
 #pragma unroll
-        for (int kk = 0; kk < KT / 16; ++kk)
-          mma_bf16(d, desc_kmajor_sw128(pa + kk * 32), desc_mnmajor_sw128(vb + kk * 16 * 128, C::KH_BYTES),
-                   C::IDESC_PV, (p_first && kk == 0) ? 0u : 1u);
+        for (int kk = 0; kk < DH / 16; ++kk) {
+          const int h = kk >> 2, w = (kk & 3) * 32;
+          mma_bf16(d, desc_kmajor_sw128(kb + h * HALF_KV + w), desc_kmajor_sw128(qa + h * HALF_Q + w), idesc_qk,
+                   kk > 0 ? 1u : 0u);
+        }
+        mma_commit(&sfull[sb]);
+        mma_commit(&kempty[ks]);
+        ++qg;
+        if (++qt == x.t_hi) {
+          mma_commit(&qempty[ob]);
+          if (++qu < n_my) qt = utab[qu].t_lo;
+        }
+      };
+      auto issue_pv = [&]() {
+        const Unit& x = utab[pu];
+        const uint32_t ob = pu & 1, pb = pg & 1;
+        const bool first = pt == x.t_lo, last = pt + 1 == x.t_hi;
+        const int NQ = (x.nq + 15) & ~15;
+        const uint32_t idesc_pv = idesc_bf16(DH, NQ, true, true);
+        const uint32_t idesc_l = idesc_bf16(128, NQ, false, true);
+        mbar_wait(&pfull[pb], (pg >> 1) & 1);
+        tr.ev(5);
+        if (first) mbar_wait(&ofree[ob], ((pu >> 1) & 1) ^ 1);
+        const uint32_t vs = pg % SV;
+        mbar_wait(&vfull[vs], (pg / SV) & 1);
+        tc_fence_after();
+        const uint32_t dO = tmem + O_COL + ob * NQM;
+        const uint32_t dl = tmem + L_COL + ob * NQM;
+        const uint32_t vb = smem_u32(sV + vs * KV_BYTES);
+        const uint32_t pa = smem_u32(sP + pb * P_BYTES);
+        const uint64_t ones_desc = desc_kmajor_noswz(smem_u32(ones), 0, 0);
+#pragma unroll
+        for (int kk = 0; kk < KT / 16; ++kk) {
+          const uint64_t pdesc = desc_mnmajor_noswz(pa + kk * 256, 128, P_CHUNK);
+          const uint32_t acc = (first && kk == 0) ? 0u : 1u;
+          mma_bf16(dO, desc_mnmajor_sw128(vb + kk * 16 * 128, HALF_KV), pdesc, idesc_pv, acc);
+          // row sums on the tensor core: L^T[lane][n] += sum_k 1 * P^T[k][n] (every lane holds l_n)
+          mma_bf16(dl, ones_desc, pdesc, idesc_l, acc);
+        }
         mma_commit(&vempty[vs]);
         mma_commit(&pvdone[pb]);
-        if (p_last) mma_commit(&ofull[p_ob]);
+        if (last) mma_commit(&ofull[ob]);
+        ++pg;
+        if (++pt == x.t_hi && ++pu < n_my) pt = utab[pu].t_lo;
       };
-      Tracer tr(a.trace, 2);
-      for (int u = blockIdx.x; u < total; u += gridDim.x, ++it) {
-        tr.ev(0);
-        const Unit x = decode_unit(a, u, pre, nsp, n_ent, G, rpc);
-        tr.ev(9);
-        const uint32_t ob = it & 1;
-        mbar_wait(&qfull[ob], (it >> 1) & 1);
-        tr.ev(2);
-        tc_fence_after();
-        const uint32_t qa = smem_u32(sQ + ob * C::Q_BYTES);
-        for (int t = x.t_lo; t < x.t_hi; ++t, ++g) {
-          const uint32_t ks = g % SK, sb = g & 1;
-          mbar_wait(&kfull[ks], (g / SK) & 1);
-          tr.ev(3);
-          mbar_wait(&sfree[sb], ((g >> 1) & 1) ^ 1);
-          tr.ev(4);
-          tc_fence_after();
-          const uint32_t kb = smem_u32(sK + ks * C::K_BYTES);
-          const uint32_t d = tmem + C::S_COL + sb * KT;
-#pragma unroll
-          for (int kk = 0; kk < DH / 16; ++kk) {
-            const int h = kk >> 2, w = (kk & 3) * 32;
-            mma_bf16(d, desc_kmajor_sw128(qa + h * C::HALF_BYTES + w), desc_kmajor_sw128(kb + h * C::KH_BYTES + w),
-                     C::IDESC_QK, kk > 0 ? 1u : 0u);
-          }
-          mma_commit(&sfull[sb]);
-          mma_commit(&kempty[ks]);
-          if (t + 1 == x.t_hi) mma_commit(&qempty[ob]);
-          if (IMP_ONLY) continue;
-          if (pend) { issue_pv(); tr.ev(5); }
-          pend = true;
-          p_g = g; p_ob = ob; p_it = it;
-          p_first = t == x.t_lo;
-          p_last = t + 1 == x.t_hi;
+      tr.ev(0);
+      if (!IMP_ONLY) {
+        while (pu < n_my) {
+          while (qk_ready() && qg < pg + 2) issue_qk();
+          issue_pv();
         }
+      } else {
+        while (qk_ready()) issue_qk();
       }
-      if (!IMP_ONLY && pend) issue_pv();
     }
   } else if (warp == 3) {
-    // ================================================================ Q loader (TMA)
-    // Q tile lane L holds head g = L / rpc of block row r = L % rpc of the unit: for each head and
-    // 64-column half, one box of rpc consecutive q rows (rows past the unit belong to other requests
-    // or are zero-filled out of bounds; their outputs are discarded).
+    // ================================================================ Q loader (TMA, 3-D boxes)
+    // Q tile row n = r * G + g holds head kvh*G + g of block row r0 + r: per 64-column half one box
+    // {64 columns, G heads, rpc rows} (rows past the unit belong to other requests or are zero-filled
+    // out of bounds; their results are discarded).
     if (lane == 0) {
-      uint32_t it = 0;
       Tracer tr(a.trace, 3);
-      for (int u = blockIdx.x; u < total; u += gridDim.x, ++it) {
-        tr.ev(0);
-        const Unit x = decode_unit(a, u, pre, nsp, n_ent, G, rpc);
-        tr.ev(9);
+      for (int it = 0; it < n_my; ++it) {
+        const Unit& x = utab[it];
         const uint32_t ob = it & 1;
+        tr.ev(0);
         mbar_wait(&qempty[ob], ((it >> 1) & 1) ^ 1);
         tr.ev(1);
-        mbar_expect_tx(&qfull[ob], C::Q_BYTES);
-        uint8_t* q = sQ + ob * C::Q_BYTES;
-        for (int gq = 0; gq < G; ++gq)
-#pragma unroll
-          for (int h = 0; h < C::NH; ++h)
-            tma_load_2d(q + h * C::HALF_BYTES + gq * rpc * 128, &mapQ, &qfull[ob], (x.kvh * G + gq) * DH + h * 64, x.r0);
+        mbar_expect_tx(&qfull[ob], Q_BYTES);
+        uint8_t* q = sQ + ob * Q_BYTES;
+        tma_load_3d(q, &mapQ, &qfull[ob], 0, x.kvh * G, x.r0);
+        tma_load_3d(q + HALF_Q, &mapQ, &qfull[ob], 64, x.kvh * G, x.r0);
       }
     }
   } else if (warp >= 4 && warp < 8) {
     // ================================================================ softmax (+ importance)
-    // Warp 4+q owns TMEM lane quadrant q.  Its real rows sit in lanes 0.. of the quadrant; they are
-    // read 16 lanes at a time with the 16x256b shape, so 4 threads share a row (16 of the 64 columns
-    // each) and every lane of the warp works on a real row.
-    const int q4 = warp & 3;
-    const int t0 = lane & 3, t1 = lane >> 2;
-    const float sl2 = a.scale * kLog2e;
-    float* scr = a.imp_scratch + (size_t)blockIdx.x * QR * kMaxB;
-    uint32_t g = 0, it = 0;
-    Tracer tr(warp == 4 && lane == 0 ? a.trace : nullptr, 4);
-    for (int u = blockIdx.x; u < total; u += gridDim.x, ++it) {
+    SoftThread th;
+    th.L = threadIdx.x - 128;                      // key lane of the tile (= TMEM lane of S^T)
+    th.lane = lane;
+    th.q4 = warp & 3;
+    th.tmem = tmem;
+    th.lane_base = (uint32_t)(th.q4 * 32) << 16;
+    th.sl2 = a.scale * kLog2e;
+    th.G = G;
+    th.scr = a.imp_scratch + (size_t)blockIdx.x * NQM * kMaxB;
+    Tracer tr(th.L == 0 ? a.trace : nullptr, 4);
+    uint32_t g = 0;
+    const bool causal = a.ext_mode == 2;
+    for (int it = 0; it < n_my; ++it) {
+      const Unit& xr = utab[it];
+      const int nch = (xr.nq + 15) >> 4;           // 16-row chunks (1..4)
       tr.ev(0);
-      const Unit x = decode_unit(a, u, pre, nsp, n_ent, G, rpc);
-      tr.ev(9);
-      const uint32_t ob = it & 1;
-      const int rows_q = min(32, max(0, x.nr - (32 * q4) % rpc));  // real rows: a prefix of the quadrant
-      const int ngrp = rows_q > 16 ? 2 : (rows_q > 0 ? 1 : 0);      // warp-uniform
-      const int lim_min = a.ext_mode == 2 ? x.pos_base : x.kend - 1;
-      int lim[2][2];
-      bool real[2][2];
-#pragma unroll
-      for (int gr = 0; gr < 2; ++gr)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int rr = (q4 * 32 + gr * 16 + t1 + 8 * h) % rpc;   // block row of this lane
-          real[gr][h] = rr < x.nr;
-          lim[gr][h] = a.ext_mode == 2 ? x.pos_base + rr : x.kend - 1;
+      if (causal) {
+        switch (nch) {
+          case 1: softmax_unit<1, true, IMP_ONLY>(a, xr, it, g, th, ss, tr); break;
+          case 2: softmax_unit<2, true, IMP_ONLY>(a, xr, it, g, th, ss, tr); break;
+          case 3: softmax_unit<3, true, IMP_ONLY>(a, xr, it, g, th, ss, tr); break;
+          default: softmax_unit<4, true, IMP_ONLY>(a, xr, it, g, th, ss, tr); break;
         }
-      float m_used[2][2], l[2][2];
-#pragma unroll
-      for (int gr = 0; gr < 2; ++gr)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) { m_used[gr][h] = -CUDART_INF_F; l[gr][h] = 0.f; }
-      for (int t = x.t_lo; t < x.t_hi; ++t, ++g) {
-        const uint32_t sb = g & 1;
-        mbar_wait(&sfull[sb], (g >> 1) & 1);
-        tr.ev(1);
-        tc_fence_after();
-        uint32_t r[2][32];
-#pragma unroll
-        for (int gr = 0; gr < 2; ++gr)
-          if (gr < ngrp)
-            tmem_ld16x256_x8(tmem + ((uint32_t)(q4 * 32 + gr * 16) << 16) + C::S_COL + sb * KT, r[gr]);
-        tmem_wait_ld();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&sfree[sb]);
-        const int k0 = t * KT;
-        if (x.want_imp) {                          // block-column scores for the Eq.2 epilogue
-#pragma unroll
-          for (int gr = 0; gr < 2; ++gr)
-            if (gr < ngrp)
-#pragma unroll
-              for (int h = 0; h < 2; ++h)
-#pragma unroll
-                for (int j = 0; j < 8; ++j)
-#pragma unroll
-                  for (int e = 0; e < 2; ++e) {
-                    const int jb = k0 + 8 * j + 2 * t0 + e - x.s0;
-                    if (real[gr][h] && jb >= 0 && jb < a.B)
-                      scr[(q4 * 32 + gr * 16 + t1 + 8 * h) * kMaxB + jb] = __uint_as_float(r[gr][4 * j + 2 * h + e]) * a.scale;
-                  }
+      } else {
+        switch (nch) {
+          case 1: softmax_unit<1, false, IMP_ONLY>(a, xr, it, g, th, ss, tr); break;
+          case 2: softmax_unit<2, false, IMP_ONLY>(a, xr, it, g, th, ss, tr); break;
+          case 3: softmax_unit<3, false, IMP_ONLY>(a, xr, it, g, th, ss, tr); break;
+          default: softmax_unit<4, false, IMP_ONLY>(a, xr, it, g, th, ss, tr); break;
         }
-        if (IMP_ONLY) continue;
-        const bool full = k0 >= x.kbeg && k0 + KT - 1 <= lim_min;
-        const uint32_t pb = g & 1;
-        uint32_t pk[2][2][8];
-        bool resc_any = false;
-        float alpha[2][2];
-#pragma unroll
-        for (int gr = 0; gr < 2; ++gr) {
-          if (gr >= ngrp) continue;
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            float mx = -CUDART_INF_F;
-            if (!full) {
-#pragma unroll
-              for (int j = 0; j < 8; ++j)
-#pragma unroll
-                for (int e = 0; e < 2; ++e) {
-                  const int c = k0 + 8 * j + 2 * t0 + e;
-                  if (c < x.kbeg || c > lim[gr][h]) r[gr][4 * j + 2 * h + e] = __float_as_uint(-CUDART_INF_F);
-                }
-            }
-#pragma unroll
-            for (int j = 0; j < 8; ++j)
-              mx = fmaxf(mx, fmaxf(__uint_as_float(r[gr][4 * j + 2 * h]), __uint_as_float(r[gr][4 * j + 2 * h + 1])));
-            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-            const float mt = mx * sl2;
-            float al = 1.f;
-            float mu = m_used[gr][h];
-            if (mt > mu + kRescaleThresh || (mu == -CUDART_INF_F && mt > -CUDART_INF_F)) {
-              const float mn = fmaxf(mt, mu);
-              al = ex2(mu - mn);                   // 0 when mu = -inf
-              m_used[gr][h] = mn;
-              resc_any |= real[gr][h] && t > x.t_lo;
-            }
-            alpha[gr][h] = al;
-            const float nm = m_used[gr][h] == -CUDART_INF_F ? 0.f : -m_used[gr][h];
-            float sum = 0.f;
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              float p0 = ex2(fmaf(__uint_as_float(r[gr][4 * j + 2 * h]), sl2, nm));
-              float p1 = ex2(fmaf(__uint_as_float(r[gr][4 * j + 2 * h + 1]), sl2, nm));
-              if (!real[gr][h]) { p0 = 0.f; p1 = 0.f; }
-              sum += p0 + p1;
-              const __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
-              pk[gr][h][j] = *reinterpret_cast<const uint32_t*>(&b2);
-            }
-            l[gr][h] = l[gr][h] * al + sum;
-          }
-        }
-        resc_any = __any_sync(0xffffffffu, resc_any);
-        tr.ev(2);
-        if (g >= 2) mbar_wait(&pvdone[pb], ((g >> 1) & 1) ^ 1);   // PV of tile g-2 done: P buffer free
-        tr.ev(3);
-        const uint32_t pbase = smem_u32(sP + pb * C::P_BYTES);
-#pragma unroll
-        for (int gr = 0; gr < 2; ++gr) {
-          if (gr >= ngrp) continue;
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int Lr = q4 * 32 + gr * 16 + t1 + 8 * h;
-#pragma unroll
-            for (int j = 0; j < 8; ++j) sts32(pbase + sw128_off(Lr, j) + 4 * t0, pk[gr][h][j]);
-          }
-        }
-        if (resc_any) {                            // O *= alpha for rows whose running max moved (lazy)
-          mbar_wait(&pvdone[(g - 1) & 1], ((g - 1) >> 1) & 1);   // PV of tile g-1 done: O stable
-          tc_fence_after();
-#pragma unroll
-          for (int gr = 0; gr < 2; ++gr) {
-            if (gr >= ngrp) continue;
-#pragma unroll 1
-            for (int c0 = 0; c0 < DH; c0 += 64) {
-              const uint32_t ta = tmem + ((uint32_t)(q4 * 32 + gr * 16) << 16) + C::O_COL + ob * DH + c0;
-              uint32_t v[32];
-              tmem_ld16x256_x8(ta, v);
-              tmem_wait_ld();
-#pragma unroll
-              for (int j = 0; j < 8; ++j)
-#pragma unroll
-                for (int h = 0; h < 2; ++h)
-#pragma unroll
-                  for (int e = 0; e < 2; ++e)
-                    v[4 * j + 2 * h + e] = __float_as_uint(__uint_as_float(v[4 * j + 2 * h + e]) * alpha[gr][h]);
-              tmem_st16x256_x8(ta, v);
-            }
-          }
-          tmem_wait_st();
-        }
-        fence_proxy_async();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&pfull[pb]);
-        tr.ev(4);
       }
-      if (!IMP_ONLY) {
-        // row sums over the 4 threads of a row; per-row statistics for the epilogue (buffer ob is
-        // free once the epilogue of unit it-2 is done)
-        mbar_wait(&ofree[ob], ((it >> 1) & 1) ^ 1);
-#pragma unroll
-        for (int gr = 0; gr < 2; ++gr)
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            float ls = l[gr][h];
-            ls += __shfl_xor_sync(0xffffffffu, ls, 1);
-            ls += __shfl_xor_sync(0xffffffffu, ls, 2);
-            if (gr < ngrp && t0 == 0) stat[ob * QR + q4 * 32 + gr * 16 + t1 + 8 * h] = make_float2(m_used[gr][h], ls);
-          }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&statfull[ob]);
-      }
-      if (x.want_imp) {
-        // Eq.2: per query row, MaxPool1D (k = mp_kernel, -inf outside P; A-I3, A-I5) over the block
-        // scores, softmax over P, then the sum over rows and heads (fixed order: lanes, then warps).
-        __syncwarp();
-        const int B = a.B, rad = a.mp_kernel / 2;
-        const int L = q4 * 32 + lane;
-        const bool rr = L % rpc < x.nr;
-        const float* sc = scr + L * kMaxB;
-        float w[kMaxB];
-        float mx = -CUDART_INF_F;
-        if (rr) {
-          for (int j = 0; j < B; ++j) {
-            float v = -CUDART_INF_F;
-            if ((x.P >> j) & 1ull) {
-              const int lo = max(0, j - rad), hi = min(B - 1, j + rad);
-              for (int jj = lo; jj <= hi; ++jj)
-                if ((x.P >> jj) & 1ull) v = fmaxf(v, sc[jj]);
-            }
-            w[j] = v;
-            mx = fmaxf(mx, v);
-          }
-          float z = 0.f;
-          for (int j = 0; j < B; ++j) {
-            const float e = w[j] == -CUDART_INF_F ? 0.f : expf(w[j] - mx);
-            w[j] = e;
-            z += e;
-          }
-          for (int j = 0; j < B; ++j) w[j] = w[j] / z;
-        }
-        for (int j = 0; j < B; ++j) {
-          float v = rr ? w[j] : 0.f;
-          for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-          if (lane == 0) red[q4 * kMaxB + j] = v;
-        }
-        named_bar(1, 128);
-        if (warp == 4) {
-          for (int j = lane; j < B; j += 32) {
-            const float v = ((red[j] + red[kMaxB + j]) + red[2 * kMaxB + j]) + red[3 * kMaxB + j];
-            a.imp[(size_t)x.pair * B + j] = v;
-          }
-        }
-        named_bar(1, 128);
-      }
+      if (xr.want_imp) importance_epilogue(a, xr, th, ss);
     }
   } else if (warp >= 8 && !IMP_ONLY) {
-    // ================================================================ epilogue
-    const int q4 = warp & 3;
-    const int L = q4 * 32 + lane;
-    const int et = threadIdx.x - 256;
-    uint32_t it = 0;
-    Tracer tr(warp == 8 && lane == 0 ? a.trace : nullptr, 5);
-    for (int u = blockIdx.x; u < total; u += gridDim.x, ++it) {
-      tr.ev(0);
-      const Unit x = decode_unit(a, u, pre, nsp, n_ent, G, rpc);
-      tr.ev(9);
+    // ================================================================ epilogue (thread = d_h lane)
+    const int d = threadIdx.x - 256;
+    const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+    Tracer tr(d == 0 ? a.trace : nullptr, 5);
+    for (int it = 0; it < n_my; ++it) {
+      const Unit& xr = utab[it];
+      const int nq = xr.nq, nch = (nq + 15) >> 4;
       const uint32_t ob = it & 1;
-      const bool active = (32 * q4) % rpc < x.nr, real = L % rpc < x.nr;
-      const int qi = L;                            // partial-buffer row index
+      tr.ev(0);
       mbar_wait(&ofull[ob], (it >> 1) & 1);
       mbar_wait(&statfull[ob], (it >> 1) & 1);
       tr.ev(1);
       tc_fence_after();
-      const float2 ml = stat[ob * QR + L];
-      float o[DH];
-      if (active) {
+      if (xr.nsplit == 1) {
+        // O / l straight to the bf16 output rows, 16 query rows at a time
+#pragma unroll 1
+        for (int c = 0; c < nch; ++c) {
+          uint32_t r[16], rl[16];
+          tmem_ld32x16(tmem + lane_base + O_COL + ob * NQM + 16 * c, r);
+          tmem_ld32x16(tmem + lane_base + L_COL + ob * NQM + 16 * c, rl);
+          tmem_wait_ld();
 #pragma unroll
-        for (int c0 = 0; c0 < DH; c0 += 32)
-          tmem_ld32(tmem + ((uint32_t)(q4 * 32) << 16) + C::O_COL + ob * DH + c0, o + c0);
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&ofree[ob]);
-      const int row = x.r0 + L % rpc, head = x.kvh * G + L / rpc;
-      if (x.nsplit == 1) {
-        if (real) {
-          const float inv = 1.0f / ml.y;
-          bf16* dst = a.out + (size_t)row * a.ldo + head * DH;
-#pragma unroll
-          for (int c = 0; c < DH; c += 8) {
-            uint4 pk;
-            __nv_bfloat162 b0 = __floats2bfloat162_rn(o[c] * inv, o[c + 1] * inv);
-            __nv_bfloat162 b1 = __floats2bfloat162_rn(o[c + 2] * inv, o[c + 3] * inv);
-            __nv_bfloat162 b2 = __floats2bfloat162_rn(o[c + 4] * inv, o[c + 5] * inv);
-            __nv_bfloat162 b3 = __floats2bfloat162_rn(o[c + 6] * inv, o[c + 7] * inv);
-            pk.x = *reinterpret_cast<uint32_t*>(&b0); pk.y = *reinterpret_cast<uint32_t*>(&b1);
-            pk.z = *reinterpret_cast<uint32_t*>(&b2); pk.w = *reinterpret_cast<uint32_t*>(&b3);
-            *reinterpret_cast<uint4*>(dst + c) = pk;
+          for (int e = 0; e < 16; ++e) {
+            const int n = 16 * c + e;
+            if (n < nq) {
+              const int row = xr.r0 + n / G, head = xr.kvh * G + n % G;
+              a.out[(size_t)row * a.ldo + head * DH + d] =
+                  __float2bfloat16_rn(__uint_as_float(r[e]) / __uint_as_float(rl[e]));
+            }
           }
         }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&ofree[ob]);
+        tr.ev(2);
       } else {
         // split partial -> workspace; the last-arriving split merges all partials in split order
-        const size_t slot_floats = (size_t)QR * DH + 2 * QR;
-        float* base = a.part + (size_t)x.pair * a.max_nsplit * slot_floats;
-        if (real) {
-          float* po = base + (size_t)x.sp * slot_floats + (size_t)qi * DH;
+        const size_t slot_floats = (size_t)NQM * DH + 2 * NQM;
+        float* base = a.part + (size_t)xr.pair * a.max_nsplit * slot_floats;
+        float* po = base + (size_t)xr.sp * slot_floats;
+#pragma unroll 1
+        for (int c = 0; c < nch; ++c) {
+          uint32_t r[16], rl[16];
+          tmem_ld32x16(tmem + lane_base + O_COL + ob * NQM + 16 * c, r);
+          tmem_ld32x16(tmem + lane_base + L_COL + ob * NQM + 16 * c, rl);
+          tmem_wait_ld();
+          float ld = 0.f;
 #pragma unroll
-          for (int c = 0; c < DH; c += 4) __stcg(reinterpret_cast<float4*>(po + c), make_float4(o[c], o[c + 1], o[c + 2], o[c + 3]));
-          __stcg(reinterpret_cast<float2*>(base + (size_t)x.sp * slot_floats + (size_t)QR * DH + 2 * qi), ml);
+          for (int e = 0; e < 16; ++e) {
+            if (16 * c + e < nq) __stcg(po + (16 * c + e) * DH + d, __uint_as_float(r[e]));
+            if (16 * c + e == d) ld = __uint_as_float(rl[e]);
+          }
+          if (d >= 16 * c && d < 16 * c + 16 && d < nq)
+            __stcg(reinterpret_cast<float2*>(po + NQM * DH) + d, make_float2(ss.stat[ob * NQM + d], ld));
         }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&ofree[ob]);
         __threadfence();
         named_bar(2, 128);
-        if (et == 0) *flag_sh = atomicAdd(&a.sem[x.pair], 1);
+        if (d == 0) *flag_sh = atomicAdd(&a.sem[xr.pair], 1);
         named_bar(2, 128);
-        const bool last = *flag_sh == x.nsplit - 1;
-        named_bar(2, 128);
+        const bool last = *flag_sh == xr.nsplit - 1;
         if (last) {
           __threadfence();
-          if (real) {
+          // per-row split scales f_s = 2^(m_s - m) / sum_s' l_s' 2^(m_s' - m), in split order
+          if (d < nq) {
             float m = -CUDART_INF_F;
-            for (int s = 0; s < x.nsplit; ++s) {
-              const float2 v = __ldcg(reinterpret_cast<const float2*>(base + (size_t)s * slot_floats + (size_t)QR * DH + 2 * qi));
-              m = fmaxf(m, v.x);
-            }
+            for (int s2 = 0; s2 < xr.nsplit; ++s2)
+              m = fmaxf(m, __ldcg(reinterpret_cast<const float2*>(base + (size_t)s2 * slot_floats + NQM * DH) + d).x);
             float lsum = 0.f;
-#pragma unroll
-            for (int c = 0; c < DH; ++c) o[c] = 0.f;
-            for (int s = 0; s < x.nsplit; ++s) {
-              const float2 v = __ldcg(reinterpret_cast<const float2*>(base + (size_t)s * slot_floats + (size_t)QR * DH + 2 * qi));
-              const float f = v.x == -CUDART_INF_F ? 0.f : exp2f(v.x - m);
-              lsum += v.y * f;
-              const float* po = base + (size_t)s * slot_floats + (size_t)qi * DH;
-#pragma unroll
-              for (int c = 0; c < DH; c += 4) {
-                const float4 pv = __ldcg(reinterpret_cast<const float4*>(po + c));
-                o[c] += pv.x * f; o[c + 1] += pv.y * f; o[c + 2] += pv.z * f; o[c + 3] += pv.w * f;
-              }
+            for (int s2 = 0; s2 < xr.nsplit; ++s2) {
+              const float2 ml = __ldcg(reinterpret_cast<const float2*>(base + (size_t)s2 * slot_floats + NQM * DH) + d);
+              const float f = ml.x == -CUDART_INF_F ? 0.f : ex2(ml.x - m);
+              merge[s2 * NQM + d] = f;
+              lsum += ml.y * f;
             }
-            const float inv = 1.0f / lsum;
-            bf16* dst = a.out + (size_t)row * a.ldo + head * DH;
-#pragma unroll
-            for (int c = 0; c < DH; c += 2)
-              *reinterpret_cast<__nv_bfloat162*>(dst + c) = __floats2bfloat162_rn(o[c] * inv, o[c + 1] * inv);
+            merge[MAXS * NQM + d] = 1.0f / lsum;
           }
-          if (et == 0) a.sem[x.pair] = 0;
+          named_bar(2, 128);
+#pragma unroll 4
+          for (int n = 0; n < nq; ++n) {
+            float acc = 0.f;
+            for (int s2 = 0; s2 < xr.nsplit; ++s2)
+              acc += __ldcg(base + (size_t)s2 * slot_floats + n * DH + d) * merge[s2 * NQM + n];
+            const int row = xr.r0 + n / G, head = xr.kvh * G + n % G;
+            a.out[(size_t)row * a.ldo + head * DH + d] = __float2bfloat16_rn(acc * merge[MAXS * NQM + n]);
+          }
+          if (d == 0) a.sem[xr.pair] = 0;
         }
+        named_bar(2, 128);                         // merge[] / flag reuse
       }
     }
   }
   __syncthreads();
   if (warp == 3) {
     tc_fence_after();
-    tmem_free<C::TMEM_COLS>(tmem);
+    tmem_free<TMEM_COLS>(tmem);
   }
 }
 
 }  // namespace attn
 
 bool attn_tc_supported(int head_dim, int page_size, int group) {
-  return (head_dim == 64 || head_dim == 128) && page_size >= 8 && page_size <= 4096 &&
-         (page_size & (page_size - 1)) == 0 && (group == 1 || group == 2 || group == 4);
+  return head_dim == attn::DH && page_size >= 8 && page_size <= 4096 && (page_size & (page_size - 1)) == 0 &&
+         (group == 1 || group == 2 || group == 4);
 }
 
-// Query-row tensor map: q buffer [rows][ld] bf16, box = 64 columns x (128 / group) rows.
-bool attn_tc_make_qmap(const bf16* q, size_t rows, int ld, int group, CUtensorMap* mq) {
-  return make_tma_2d_bf16(q, rows, ld, ld, 64, 128 / group, mq);
+int attn_tc_rows_per_chunk(int group) { return attn::NQM / group; }
+
+// Query-row tensor map: q buffer [rows][ld] bf16 viewed as {head_dim, heads, rows}; box = 64 columns x
+// G heads x (64 / G) rows, so one box fills a 64-column half of the unit's Q tile (row n = r*G + g).
+bool attn_tc_make_qmap(const bf16* q, size_t rows, int ld, int n_heads, int group, CUtensorMap* mq) {
+  return make_tma_3d_bf16(q, attn::DH, n_heads, rows, (uint64_t)attn::DH * 2, (uint64_t)ld * 2, 64, group,
+                          attn::NQM / group, mq);
 }
 
 // KV pool tensor maps: the whole pool (all layers) viewed as [rows][head_dim] bf16.
@@ -718,32 +820,28 @@ bool attn_tc_make_maps(const bf16* Kpool, const bf16* Vpool, size_t rows, int he
          make_tma_2d_bf16(Vpool, rows, head_dim, head_dim, 64, box_rows, mv);
 }
 
-template <int DH, bool IMP>
+template <bool IMP>
 static void launch_tc(const CUtensorMap& mk, const CUtensorMap& mv, const CUtensorMap& mq, const AttnArgs& a, int grid,
                       cudaStream_t s) {
-  constexpr int smem = attn::Cfg<DH>::SMEM_BYTES;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(attn::k_attn_tc<DH, IMP>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(attn::k_attn_tc<IMP>, cudaFuncAttributeMaxDynamicSharedMemorySize, attn::SMEM_BYTES);
     attr = true;
   }
-  attn::k_attn_tc<DH, IMP><<<grid, attn::NTHREADS, smem, s>>>(mk, mv, mq, a);
+  attn::k_attn_tc<IMP><<<grid, attn::NTHREADS, attn::SMEM_BYTES, s>>>(mk, mv, mq, a);
 }
 
 void launch_attention_tc(const CUtensorMap& mk, const CUtensorMap& mv, const CUtensorMap& mq, const AttnArgs& a,
                          cudaStream_t s) {
   const int G = a.n_q_heads / a.kv.n_kv_heads;
-  const int rpc = attn::QR / G;
+  const int rpc = attn::NQM / G;
   int max_units;
   if (a.ext_mode == 2) max_units = ((a.prefill_rows + rpc - 1) / rpc) * a.kv.n_kv_heads;
   else max_units = a.n_req * a.n_chunks * a.kv.n_kv_heads * (a.imp_only ? 1 : a.max_nsplit);
   if (max_units <= 0) return;
   const int grid = std::max(1, std::min(num_sms(), max_units));
-  if (a.kv.head_dim == 128) {
-    if (a.imp_only) launch_tc<128, true>(mk, mv, mq, a, grid, s); else launch_tc<128, false>(mk, mv, mq, a, grid, s);
-  } else {
-    if (a.imp_only) launch_tc<64, true>(mk, mv, mq, a, grid, s); else launch_tc<64, false>(mk, mv, mq, a, grid, s);
-  }
+  if (a.imp_only) launch_tc<true>(mk, mv, mq, a, grid, s);
+  else launch_tc<false>(mk, mv, mq, a, grid, s);
 }
 
 }  // namespace focus

@@ -1,4 +1,7 @@
-// tcgen05 / TMEM / TMA GEMM for sm_100a:  C[M x N] (fp32, store or +=) = A[M x K] . W[N x K]^T
+// tcgen05 / TMEM / TMA GEMM for sm_100a:  acc[M x N] (fp32) = A[M x K] . W[N x K]^T, with epilogues
+//   GEMM_STORE / GEMM_ADD  C = acc / C += acc (fp32; residual add for the O and down projections)
+//   GEMM_SWIGLU            act = bf16(silu(gate) * up) from the interleaved gate|up tile (no fp32 round trip)
+//   GEMM_QKV_ROPE          q|k|v = bf16(RoPE(acc)) + paged KV store of k and v (head_dim 128)
 // A = activations (bf16, K-major rows), W = weights (bf16, [N][K] row-major = K-major).
 //
 // Persistent, warp-specialised (one CTA per SM, 256 threads):
@@ -7,7 +10,7 @@
 //               (M=128, N=256, K=16) x 4 per stage into a TMEM accumulator; tcgen05.commit releases
 //               the smem stage and, after the last k-block, signals the epilogue
 //   warp 2      TMEM allocator (512 columns = two 128 x 256 fp32 accumulators, double-buffered)
-//   warps 4..7  epilogue: tcgen05.ld 32x32b -> registers -> fp32 global (store / residual add)
+//   warps 4..7  epilogue: tcgen05.ld 32x32b -> registers -> the mode's emitter (thread = output row)
 // Work units = (m tile, n tile, k split) with m fastest (CTAs sharing a weight tile run together and
 // hit L2).  M is read from device memory (ragged row counts of the FOCUS step) and the split-K factor
 // is chosen on device from the live tile count; split-K partials are reduced by the last-arriving
@@ -61,11 +64,127 @@ __device__ __forceinline__ void unit_coords(const Sched& s, int u, int& mt, int&
   nt = r / s.split;
 }
 
+// ---------------------------------------------------------------- epilogue emitters
+// `chunk(c0, v)` yields 32 consecutive fp32 accumulator columns [c0, c0+32) of this thread's row of the
+// tile (TMEM or merged split partials); it must be called uniformly by the whole warp.
+template <int MODE, typename Chunk>
+__device__ __forceinline__ void epilogue_tile(Chunk&& chunk, int row, bool row_ok, int nt, int N, float* __restrict__ C,
+                                              int ldc, const GemmEpi& epi) {
+  if constexpr (MODE == GEMM_STORE || MODE == GEMM_ADD) {
+    const bool vec_ok = (ldc % 4) == 0 && (((uintptr_t)C) & 15) == 0;
+#pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += 32) {
+      float v[32];
+      chunk(c0, v);
+      const int n0 = nt * BN + c0;
+      if (row_ok && n0 < N) {
+        float* dst = C + (size_t)row * ldc + n0;
+        if (n0 + 32 <= N && vec_ok) {
+#pragma unroll
+          for (int i = 0; i < 32; i += 4) {
+            float4 o = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+            if (MODE == GEMM_ADD) {
+              const float4 p = *reinterpret_cast<const float4*>(dst + i);
+              o.x += p.x; o.y += p.y; o.z += p.z; o.w += p.w;
+            }
+            *reinterpret_cast<float4*>(dst + i) = o;
+          }
+        } else {
+          for (int i = 0; i < 32 && n0 + i < N; ++i) dst[i] = MODE == GEMM_ADD ? dst[i] + v[i] : v[i];
+        }
+      }
+    }
+  } else if constexpr (MODE == GEMM_SWIGLU) {
+    // tile nt = gate rows [128 nt, 128 nt + 128) | up rows (W_gu interleaved by kGuGroup = BN / 2):
+    // act[row][128 nt + c] = bf16(silu(gate_c) * up_c)
+    static_assert(BN == 2 * kGuGroup, "gate/up interleave must match the tile");
+#pragma unroll 1
+    for (int c0 = 0; c0 < kGuGroup; c0 += 32) {
+      float gv[32], uv[32];
+      chunk(c0, gv);
+      chunk(c0 + kGuGroup, uv);
+      if (row_ok) {
+        bf16* dst = epi.out + (size_t)row * epi.ldo + nt * kGuGroup + c0;
+#pragma unroll
+        for (int i = 0; i < 32; i += 8) {
+          uint4 pk;
+          uint32_t* w = reinterpret_cast<uint32_t*>(&pk);
+#pragma unroll
+          for (int e = 0; e < 8; e += 2) {
+            const float a0 = gv[i + e] / (1.0f + expf(-gv[i + e])) * uv[i + e];
+            const float a1 = gv[i + e + 1] / (1.0f + expf(-gv[i + e + 1])) * uv[i + e + 1];
+            const __nv_bfloat162 b = __floats2bfloat162_rn(a0, a1);
+            w[e / 2] = *reinterpret_cast<const uint32_t*>(&b);
+          }
+          *reinterpret_cast<uint4*>(dst + i) = pk;
+        }
+      }
+    }
+  } else {
+    // GEMM_QKV_ROPE (head_dim 128): the tile holds 2 heads of the fused q|k|v output.  q and k heads
+    // are rotated (rotate-half pairs (c, c+64), angle pos * theta^(-2c/dh) from the fp64-built table),
+    // rounded to bf16 and written to the qkv rows; k and v heads are also stored at the row's paged
+    // KV slot (the "sparse KV fill").  Writing a committed block slot raises the invariant flag.
+    RowInfo ri{0, -1, 0, 0};
+    if (row_ok) ri = epi.rows[row];
+    if (row_ok && ri.j >= 0 && ((epi.st[ri.slot].committed >> ri.j) & 1ull)) atomicExch(&epi.cnt->invariant, 1);
+    const int hkv = epi.kv.n_kv_heads;
+#pragma unroll 1
+    for (int hh = 0; hh < BN / 128; ++hh) {
+      const int head = nt * (BN / 128) + hh;              // 0..Hq-1 q, then k, then v
+      const bool is_v = head >= epi.n_q_heads + hkv;
+      const bool is_k = !is_v && head >= epi.n_q_heads;
+#pragma unroll 1
+      for (int c0 = 0; c0 < 64; c0 += 32) {
+        float lo[32], hi[32];
+        chunk(hh * 128 + c0, lo);
+        chunk(hh * 128 + c0 + 64, hi);
+        if (!row_ok) continue;
+        if (!is_v) {
+          const float* cr = epi.rcos + (size_t)ri.pos * 64 + c0;
+          const float* sr = epi.rsin + (size_t)ri.pos * 64 + c0;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const float c = cr[i], sn = sr[i];
+            const float y1 = lo[i] * c - hi[i] * sn;
+            const float y2 = hi[i] * c + lo[i] * sn;
+            lo[i] = y1;
+            hi[i] = y2;
+          }
+        }
+        uint4 plo[4], phi[4];
+#pragma unroll
+        for (int i = 0; i < 32; i += 2) {
+          const __nv_bfloat162 bl = __floats2bfloat162_rn(lo[i], lo[i + 1]);
+          const __nv_bfloat162 bh = __floats2bfloat162_rn(hi[i], hi[i + 1]);
+          reinterpret_cast<uint32_t*>(plo)[i / 2] = *reinterpret_cast<const uint32_t*>(&bl);
+          reinterpret_cast<uint32_t*>(phi)[i / 2] = *reinterpret_cast<const uint32_t*>(&bh);
+        }
+        bf16* dst = epi.out + (size_t)row * epi.ldo + head * 128 + c0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          reinterpret_cast<uint4*>(dst)[i] = plo[i];
+          reinterpret_cast<uint4*>(dst + 64)[i] = phi[i];
+        }
+        if (is_k || is_v) {
+          const int kvh = head - epi.n_q_heads - (is_v ? hkv : 0);
+          bf16* pool = (is_v ? epi.kv.V : epi.kv.K) + kv_offset(epi.kv, ri.slot, ri.pos, kvh) + c0;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            reinterpret_cast<uint4*>(pool)[i] = plo[i];
+            reinterpret_cast<uint4*>(pool + 64)[i] = phi[i];
+          }
+        }
+      }
+    }
+  }
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, float* __restrict__ C,
               int ldc, int N, int K, const int* __restrict__ M_dev, int M_max, float* __restrict__ ws,
-              int* __restrict__ sem, int ws_tiles_cap) {
+              int* __restrict__ sem, int ws_tiles_cap, const GemmEpi epi) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* sA = smem;                                   // STAGES x A_BYTES
@@ -146,10 +265,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
     }
   } else if (warp >= 4) {
-    // ---------------- epilogue: warp q = warp-4 owns TMEM lanes [32q, 32q+32)
+    // ---------------- epilogue: warp q = warp-4 owns TMEM lanes [32q, 32q+32) (thread = output row)
     const int q = warp - 4;
     const int et = threadIdx.x - 128;                   // 0..127
-    const bool vec_ok = (ldc % 4) == 0 && (((uintptr_t)C) & 15) == 0;
     int it = 0;
     for (int u = blockIdx.x; u < sc.units; u += gridDim.x, ++it) {
       int mt, nt, sp;
@@ -162,28 +280,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
       const int tile = nt * sc.m_tiles + mt;
       if (sc.split == 1) {
-#pragma unroll 1
-        for (int c0 = 0; c0 < BN; c0 += 32) {
-          float v[32];
-          tmem_ld32(taddr + c0, v);
-          const int n0 = nt * BN + c0;
-          if (row_ok) {
-            float* dst = C + (size_t)row * ldc + n0;
-            if (n0 + 32 <= N && vec_ok) {
-#pragma unroll
-              for (int i = 0; i < 32; i += 4) {
-                float4 o = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-                if (MODE == GEMM_ADD) {
-                  const float4 p = *reinterpret_cast<const float4*>(dst + i);
-                  o.x += p.x; o.y += p.y; o.z += p.z; o.w += p.w;
-                }
-                *reinterpret_cast<float4*>(dst + i) = o;
-              }
-            } else {
-              for (int i = 0; i < 32 && n0 + i < N; ++i) dst[i] = MODE == GEMM_ADD ? dst[i] + v[i] : v[i];
-            }
-          }
-        }
+        // accumulator chunks straight from TMEM (warp-collective loads)
+        auto chunk = [&](int c0, float* v) { tmem_ld32(taddr + c0, v); };
+        epilogue_tile<MODE>(chunk, row, row_ok, nt, N, C, ldc, epi);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -206,32 +305,22 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (et == 0) *flag_sh = atomicAdd(&sem[tile], 1);
         asm volatile("bar.sync 1, 128;" ::: "memory");
         const bool last = *flag_sh == sc.split - 1;
+        asm volatile("bar.sync 1, 128;" ::: "memory");
         if (last) {
           __threadfence();
           const float* base = ws + (size_t)tile * sc.split * (BM * BN) + (size_t)(q * 32 + lane) * BN;
-          if (row_ok) {
-#pragma unroll 1
-            for (int c0 = 0; c0 < BN; c0 += 4) {
-              const int n0 = nt * BN + c0;
-              if (n0 >= N) break;
-              float4 s = __ldcg(reinterpret_cast<const float4*>(base + c0));
+          auto chunk = [&](int c0, float* v) {
+#pragma unroll
+            for (int i = 0; i < 32; i += 4) {
+              float4 s4 = __ldcg(reinterpret_cast<const float4*>(base + c0 + i));
               for (int p = 1; p < sc.split; ++p) {
-                const float4 t = __ldcg(reinterpret_cast<const float4*>(base + (size_t)p * (BM * BN) + c0));
-                s.x += t.x; s.y += t.y; s.z += t.z; s.w += t.w;
+                const float4 t = __ldcg(reinterpret_cast<const float4*>(base + (size_t)p * (BM * BN) + c0 + i));
+                s4.x += t.x; s4.y += t.y; s4.z += t.z; s4.w += t.w;
               }
-              float* dst = C + (size_t)row * ldc + n0;
-              if (n0 + 4 <= N && vec_ok) {
-                if (MODE == GEMM_ADD) {
-                  const float4 p = *reinterpret_cast<const float4*>(dst);
-                  s.x += p.x; s.y += p.y; s.z += p.z; s.w += p.w;
-                }
-                *reinterpret_cast<float4*>(dst) = s;
-              } else {
-                const float sv[4] = {s.x, s.y, s.z, s.w};
-                for (int i = 0; i < 4 && n0 + i < N; ++i) dst[i] = MODE == GEMM_ADD ? dst[i] + sv[i] : sv[i];
-              }
+              v[i] = s4.x; v[i + 1] = s4.y; v[i + 2] = s4.z; v[i + 3] = s4.w;
             }
-          }
+          };
+          epilogue_tile<MODE>(chunk, row, row_ok, nt, N, C, ldc, epi);
           asm volatile("bar.sync 1, 128;" ::: "memory");
           if (et == 0) sem[tile] = 0;
         }
@@ -289,25 +378,39 @@ int gemm_backend() {
 void gemm_set_backend(int b) { g_backend = b; }
 
 bool launch_gemm_tc(const bf16* A, int lda, int a_rows, const bf16* W, int N, int K, float* C, int ldc, const int* M_dev,
-                    int M_max, GemmMode mode, const GemmWs& ws, cudaStream_t s) {
+                    int M_max, GemmMode mode, const GemmWs& ws, cudaStream_t s, const GemmEpi* epi) {
   using namespace tc;
   if (M_max <= 0) return true;
   if (K % BK || lda % 8 || a_rows < 1) return false;
+  if ((mode == GEMM_SWIGLU || mode == GEMM_QKV_ROPE) && (!epi || N % BN)) return false;
+  if (mode == GEMM_QKV_ROPE && epi->kv.head_dim != 128) return false;
   CUtensorMap ma, mb;
   if (!get_map(A, a_rows, K, lda, BM, &ma) || !get_map(W, N, K, K, BN, &mb)) return false;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_gemm_tc<GEMM_STORE>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     cudaFuncSetAttribute(k_gemm_tc<GEMM_ADD>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    cudaFuncSetAttribute(k_gemm_tc<GEMM_SWIGLU>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    cudaFuncSetAttribute(k_gemm_tc<GEMM_QKV_ROPE>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     attr = true;
   }
   const int max_units = ((M_max + BM - 1) / BM) * ((N + BN - 1) / BN) * MAX_SPLIT;
   const int grid = std::max(1, std::min(num_sms(), max_units));
   const int cap = (int)std::min<size_t>(ws.sem_count, ws.bytes / (sizeof(float) * BM * BN));
-  if (mode == GEMM_ADD)
-    k_gemm_tc<GEMM_ADD><<<grid, NUM_THREADS, SMEM_BYTES, s>>>(ma, mb, C, ldc, N, K, M_dev, M_max, ws.ptr, ws.sem, cap);
-  else
-    k_gemm_tc<GEMM_STORE><<<grid, NUM_THREADS, SMEM_BYTES, s>>>(ma, mb, C, ldc, N, K, M_dev, M_max, ws.ptr, ws.sem, cap);
+  const GemmEpi e = epi ? *epi : GemmEpi{};
+  switch (mode) {
+    case GEMM_ADD:
+      k_gemm_tc<GEMM_ADD><<<grid, NUM_THREADS, SMEM_BYTES, s>>>(ma, mb, C, ldc, N, K, M_dev, M_max, ws.ptr, ws.sem, cap, e);
+      break;
+    case GEMM_SWIGLU:
+      k_gemm_tc<GEMM_SWIGLU><<<grid, NUM_THREADS, SMEM_BYTES, s>>>(ma, mb, C, ldc, N, K, M_dev, M_max, ws.ptr, ws.sem, cap, e);
+      break;
+    case GEMM_QKV_ROPE:
+      k_gemm_tc<GEMM_QKV_ROPE><<<grid, NUM_THREADS, SMEM_BYTES, s>>>(ma, mb, C, ldc, N, K, M_dev, M_max, ws.ptr, ws.sem, cap, e);
+      break;
+    default:
+      k_gemm_tc<GEMM_STORE><<<grid, NUM_THREADS, SMEM_BYTES, s>>>(ma, mb, C, ldc, N, K, M_dev, M_max, ws.ptr, ws.sem, cap, e);
+  }
   return true;
 }
 

@@ -69,8 +69,8 @@ def test_small_end_to_end_variants(meth):
 
 GQA_TINY = ModelConfig(n_layers=3, d_model=128, n_q_heads=8, n_kv_heads=2, head_dim=16, d_ff=256, vocab=61,
                        rope_theta=1e4)
-# head_dim 64: the tensor-core (tcgen05) attention path; GQA_TINY (head_dim 16) runs the SIMT one
-GQA_TC = ModelConfig(n_layers=3, d_model=256, n_q_heads=8, n_kv_heads=2, head_dim=64, d_ff=256, vocab=61,
+# head_dim 128: the tensor-core (tcgen05) attention path; GQA_TINY (head_dim 16) runs the SIMT one
+GQA_TC = ModelConfig(n_layers=3, d_model=256, n_q_heads=8, n_kv_heads=2, head_dim=128, d_ff=256, vocab=61,
                      rope_theta=1e4)
 
 
