@@ -236,7 +236,7 @@ def run_focus(args):
                           "timed_steps_from": f"step {args.warmup + 1} of the decode (context {run.prompt_len}+)",
                           "prefill_s": round(prefill_s, 2)},
                "e2e": {"value": round(e2e_val, 2), "unit": UNIT, "h2d_bytes_per_step": 4 * n_req,
-                       "d2h_bytes_per_step": n_req * __import__("ctypes").sizeof(focus_commit_result),
+                       "d2h_bytes_per_step": n_req * __import__("ctypes").sizeof(focus_commit_result) + 32,
                        "steps": e2e_steps},
                "gpu_launches": int(launches), "roofline": roofline, "kernels": kernels,
                "clocks": clk.summary(), "decoded_in_window": int(dec_all), "per_rank": stats}

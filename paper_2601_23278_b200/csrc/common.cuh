@@ -105,7 +105,7 @@ struct GemmEpi {
 };
 // a_rows: allocated rows of A (TMA bounds); M_dev/M_max: live / maximum rows of this call.
 void launch_gemm(const bf16* A, int lda, int a_rows, const bf16* W, int N, int K, float* C, int ldc,
-                 const int* M_dev, int M_max, GemmMode mode, const GemmWs& ws, cudaStream_t s);
+                 const int* M_dev, int M_max, GemmMode mode, const GemmWs& ws, cudaStream_t s, int m_est = 0);
 int gemm_backend();
 int num_sms();
 void gemm_set_backend(int b);

@@ -20,11 +20,12 @@ void launch_gemm_simt(const bf16* A, int lda, const bf16* W, int N, int K, float
                       int M_max, GemmMode mode, cudaStream_t s);
 bool launch_gemm_tc(const bf16* A, int lda, int a_rows, const bf16* W, int N, int K, float* C, int ldc,
                     const int* M_dev, int M_max, GemmMode mode, const GemmWs& ws, cudaStream_t s,
-                    const GemmEpi* epi = nullptr);
+                    const GemmEpi* epi = nullptr, int m_est = 0);
 
 void launch_gemm(const bf16* A, int lda, int a_rows, const bf16* W, int N, int K, float* C, int ldc, const int* M_dev,
-                 int M_max, GemmMode mode, const GemmWs& ws, cudaStream_t s) {
-  if (gemm_backend() == 1 && launch_gemm_tc(A, lda, a_rows, W, N, K, C, ldc, M_dev, M_max, mode, ws, s)) return;
+                 int M_max, GemmMode mode, const GemmWs& ws, cudaStream_t s, int m_est) {
+  if (gemm_backend() == 1 && launch_gemm_tc(A, lda, a_rows, W, N, K, C, ldc, M_dev, M_max, mode, ws, s, nullptr, m_est))
+    return;
   launch_gemm_simt(A, lda, W, N, K, C, ldc, M_dev, M_max, mode, s);
 }
 }  // namespace focus
@@ -91,6 +92,7 @@ struct focus_ctx {
   TokConf* tokconf = nullptr;
   focus_commit_result* res_dev = nullptr;
   GemmWs gws{};
+  Counters* cnt_host = nullptr;   // pinned mirror of the device counters (previous step)
   void* taps[kTapCount] = {};
   size_t tap_bytes[kTapCount] = {};
   // host state
@@ -325,6 +327,7 @@ struct RowSpace {             // the rows a layer piece runs on
   const int* M_dev;           // device row count (nullptr: M_host exact)
   int M_max;
   const RowInfo* rows;
+  int M_est;                  // host estimate of the live count (last step's counter; tile-shape choice only)
 };
 
 void qkv_piece(focus_ctx* x, int l, int tl, float* xr, const RowSpace& rs) {
@@ -341,11 +344,11 @@ void qkv_piece(focus_ctx* x, int l, int tl, float* xr, const RowSpace& rs) {
   bool fused = false;
   LAUNCH(GEMM_QKV, fused = gemm_backend() == 1 &&
                            launch_gemm_tc(x->h, c.d_model, x->max_rows, x->Wqkv[l], x->qkv_dim, c.d_model, nullptr, 0,
-                                          rs.M_dev, rs.M_max, GEMM_QKV_ROPE, x->gws, s, &e));
+                                          rs.M_dev, rs.M_max, GEMM_QKV_ROPE, x->gws, s, &e, rs.M_est));
   if (!fused) {
     --x->launches;                            // the fused attempt launched nothing
     LAUNCH(GEMM_QKV, launch_gemm(x->h, c.d_model, x->max_rows, x->Wqkv[l], x->qkv_dim, c.d_model, x->f32tmp,
-                                 x->qkv_dim, rs.M_dev, rs.M_max, GEMM_STORE, x->gws, s));
+                                 x->qkv_dim, rs.M_dev, rs.M_max, GEMM_STORE, x->gws, s, rs.M_est));
     LAUNCH(ROPE_STORE, launch_rope_store(x->f32tmp, rs.rows, rs.M_dev, rs.M_max, c.n_q_heads, x->rope_cos,
                                          x->rope_sin, x->st, kv_view(x, l), x->qkv, x->cnt, s));
   }
@@ -358,7 +361,7 @@ void out_mlp_piece(focus_ctx* x, int l, int tl, float* xr, const RowSpace& rs) {
   cudaStream_t s = x->stream;
   tap(x, tl, TAP_ATTN, x->attn, (size_t)rs.M_max * x->q_dim * 2);
   LAUNCH(GEMM_O, launch_gemm(x->attn, x->q_dim, x->max_rows, x->Wo[l], c.d_model, x->q_dim, xr, c.d_model,
-                             rs.M_dev, rs.M_max, GEMM_ADD, x->gws, s));
+                             rs.M_dev, rs.M_max, GEMM_ADD, x->gws, s, rs.M_est));
   tap(x, tl, TAP_X_MID, xr, (size_t)rs.M_max * c.d_model * 4);
   LAUNCH(RMSNORM, launch_rmsnorm(xr, nullptr, rs.M_dev, rs.M_max, c.d_model, c.rms_eps, x->h, s));
   tap(x, tl, TAP_H2, x->h, (size_t)rs.M_max * c.d_model * 2);
@@ -368,16 +371,16 @@ void out_mlp_piece(focus_ctx* x, int l, int tl, float* xr, const RowSpace& rs) {
   bool fused = false;
   LAUNCH(GEMM_GU, fused = gemm_backend() == 1 &&
                           launch_gemm_tc(x->h, c.d_model, x->max_rows, x->Wgu[l], 2 * c.d_ff, c.d_model, nullptr, 0,
-                                         rs.M_dev, rs.M_max, GEMM_SWIGLU, x->gws, s, &e));
+                                         rs.M_dev, rs.M_max, GEMM_SWIGLU, x->gws, s, &e, rs.M_est));
   if (!fused) {
     --x->launches;
     LAUNCH(GEMM_GU, launch_gemm(x->h, c.d_model, x->max_rows, x->Wgu[l], 2 * c.d_ff, c.d_model, x->f32tmp,
-                                2 * c.d_ff, rs.M_dev, rs.M_max, GEMM_STORE, x->gws, s));
+                                2 * c.d_ff, rs.M_dev, rs.M_max, GEMM_STORE, x->gws, s, rs.M_est));
     LAUNCH(SILU, launch_silu_mul(x->f32tmp, rs.M_dev, rs.M_max, c.d_ff, x->act, s));
   }
   tap(x, tl, TAP_ACT, x->act, (size_t)rs.M_max * c.d_ff * 2);
   LAUNCH(GEMM_DOWN, launch_gemm(x->act, c.d_ff, x->max_rows, x->Wd[l], c.d_model, c.d_ff, xr, c.d_model, rs.M_dev,
-                                rs.M_max, GEMM_ADD, x->gws, s));
+                                rs.M_max, GEMM_ADD, x->gws, s, rs.M_est));
   tap(x, tl, TAP_X_OUT, xr, (size_t)rs.M_max * c.d_model * 4);
 }
 
@@ -459,6 +462,8 @@ focus_status focus_init(const focus_config* cfg, void* dev_arena, size_t arena_b
   // pinned staging ring
   x->up.cap = Upload::kSlots * 65536;
   if (cudaMallocHost(&x->up.host, x->up.cap) != cudaSuccess) { delete x; return FOCUS_ERR_CUDA; }
+  if (cudaMallocHost(&x->cnt_host, sizeof(Counters)) != cudaSuccess) { cudaFreeHost(x->up.host); delete x; return FOCUS_ERR_CUDA; }
+  std::memset(x->cnt_host, 0, sizeof(Counters));
   for (int i = 0; i < Upload::kSlots; ++i) {
     cudaEventCreateWithFlags(&x->up.ev[i], cudaEventDisableTiming);
     cudaEventRecord(x->up.ev[i], s);
@@ -539,6 +544,7 @@ focus_status focus_destroy(focus_ctx* x) {
   for (int i = 0; i < Upload::kSlots; ++i) cudaEventDestroy(x->up.ev[i]);
   for (cudaEvent_t e : x->prof_events) cudaEventDestroy(e);
   cudaFreeHost(x->up.host);
+  cudaFreeHost(x->cnt_host);
   delete x;
   return FOCUS_OK;
 }
@@ -584,7 +590,7 @@ focus_status focus_kv_append(focus_ctx* x, int32_t req_id, const int32_t* prompt
     if ((rc = upload(x, x->tokP, prompt + c0, (size_t)n * 4)) != FOCUS_OK) return rc;
     if ((rc = upload(x, x->rowP, rows.data(), (size_t)n * sizeof(RowInfo))) != FOCUS_OK) return rc;
     LAUNCH(EMBED, launch_embed(x->tokP, nullptr, n, x->E, c.d_model, x->x, s));
-    RowSpace rs{nullptr, n, x->rowP};
+    RowSpace rs{nullptr, n, x->rowP, n};
     for (int l = 0; l < c.n_layers; ++l) {
       qkv_piece(x, l, -1000, x->x, rs);
       AttnArgs a = attn_args(x, l, x->qkv, x->qkv_dim, 0, nullptr, 2);
@@ -649,8 +655,11 @@ focus_status focus_step_block(focus_ctx* x, const int32_t* ids, int32_t n_req) {
   const int* MS = &x->cnt->M_S;
   const int* ML = &x->cnt->M_L;
   LAUNCH(EMBED, launch_embed(x->tokP, MP, maxP, x->E, c.d_model, x->x, s));
-  RowSpace rsP{MP, maxP, x->rowP};
-  RowSpace rsS{MS, maxP, x->rowS};
+  // last step's live sizes (async pinned copy) as tile-shape estimates; the first step uses the maxima
+  Counters est = *x->cnt_host;
+  if (est.M_P <= 0 || est.M_P > maxP) { est.M_P = maxP; est.M_S = maxP; est.M_L = maxP; }
+  RowSpace rsP{MP, maxP, x->rowP, est.M_P};
+  RowSpace rsS{MS, maxP, x->rowS, est.M_S};
   // A2 layer 0 fully on P (+ fused importance I0)
   qkv_piece(x, 0, 0, x->x, rsP);
   {
@@ -710,8 +719,9 @@ focus_status focus_step_block(focus_ctx* x, const int32_t* ids, int32_t n_req) {
   // A8 final norm + LM head on S cap M, vocab reduction
   LAUNCH(RMSNORM, launch_rmsnorm(x->x2, x->srcL, ML, maxP, c.d_model, c.rms_eps, x->h, s));
   LAUNCH(GEMM_LM, launch_gemm(x->h, c.d_model, x->max_rows, x->Wlm, c.vocab, c.d_model, x->logits, c.vocab, ML, maxP,
-                              GEMM_STORE, x->gws, s));
+                              GEMM_STORE, x->gws, s, est.M_L));
   LAUNCH(VOCAB, launch_vocab_reduce(x->logits, ML, maxP, c.vocab, x->mask_id, x->nch_vocab, x->vpart, s));
+  cudaMemcpyAsync(x->cnt_host, x->cnt, sizeof(Counters), cudaMemcpyDeviceToHost, s);   // next step's estimates
   return cuda_status(cudaGetLastError());
 }
 

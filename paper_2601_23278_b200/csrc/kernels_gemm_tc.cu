@@ -24,50 +24,110 @@ namespace focus {
 
 namespace tc {
 
-constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
+constexpr int BM = 128, BK = 64;
 constexpr int A_BYTES = BM * BK * 2;               // 16 KB
-constexpr int B_BYTES = BN * BK * 2;               // 32 KB
-constexpr int STAGE_BYTES = A_BYTES + B_BYTES;     // 48 KB
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+// per tile width BN (128 or 256): W tile bytes, pipeline depth (192 KB of stages), shared memory
+template <int BN>
+struct GT {
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = (192 * 1024) / STAGE_BYTES;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+};
 constexpr int NUM_THREADS = 256;
 constexpr int TMEM_COLS = 512;
-constexpr int MAX_SPLIT = 4;
 
+
+// Hybrid data-parallel + stream-K schedule.  Tiles are ordered m-fastest.  The first dp_tiles tiles
+// (whole waves of `grid` tiles) run data-parallel round-robin (tile = b + wave*grid: CTAs running
+// together cover the m-tiles of the same weight tiles, which then stream from HBM once); the k-blocks
+// of the remaining tiles are cut into `grid` equal contiguous ranges (stream-K).  A tile whose
+// k-blocks span several CTAs is computed in pieces (one per CTA, in k order); each piece writes an
+// fp32 partial to its CTA's slot (slot 0: its first stream-K segment, slot 1: its last) and the
+// last-arriving piece reduces the partials in piece order (deterministic) and runs the epilogue.
+// Every CTA derives the same schedule from the live M.
 struct Sched {
-  int m_tiles, n_tiles, split, kb_total, units;
+  int m_tiles, n_tiles, kb, tiles, dp_tiles, sk_tiles, dp_mine;
+  long long W, w_lo, w_hi;                          // stream-K work and this CTA's range
 };
-
-// Same decision in every CTA: minimise waves x k-blocks per unit (+1 k-block of fix-up per extra split).
-__device__ __forceinline__ Sched make_sched(int M, int N, int K, int grid, int ws_tiles_cap) {
+__device__ __forceinline__ long long range_start(long long W, int b, int grid) { return (long long)b * W / grid; }
+// CTA whose stream-K range contains work position x
+__device__ __forceinline__ int owner(long long W, long long x, int grid) {
+  return (int)(((x + 1) * grid + W - 1) / W) - 1;
+}
+template <int BN>
+__device__ __forceinline__ Sched make_sched(int M, int N, int K, int policy) {
   Sched s;
   s.m_tiles = (M + BM - 1) / BM;
   s.n_tiles = (N + BN - 1) / BN;
-  s.kb_total = K / BK;
-  const int tiles = s.m_tiles * s.n_tiles;
-  int best = 1;
-  long long best_cost = -1;
-  for (int sp = 1; sp <= MAX_SPLIT; ++sp) {
-    if (sp > 1 && (s.kb_total / sp < 4 || tiles * sp > ws_tiles_cap)) break;
-    const long long waves = (tiles * sp + grid - 1) / grid;
-    const long long cost = waves * ((s.kb_total + sp - 1) / sp + (sp > 1 ? 2 : 0));
-    if (best_cost < 0 || cost < best_cost) { best_cost = cost; best = sp; }
-  }
-  s.split = best;
-  s.units = tiles * best;
+  s.kb = K / BK;
+  s.tiles = s.m_tiles * s.n_tiles;
+  const int grid = gridDim.x;
+  // policy 0: hybrid, 1: all stream-K, 2: all data-parallel
+  s.dp_tiles = policy == 1 ? 0 : (policy == 2 ? s.tiles : (s.tiles / grid) * grid);
+  s.sk_tiles = s.tiles - s.dp_tiles;
+  s.dp_mine = s.dp_tiles > (int)blockIdx.x ? (s.dp_tiles - 1 - (int)blockIdx.x) / grid + 1 : 0;
+  s.W = (long long)s.sk_tiles * s.kb;
+  s.w_lo = range_start(s.W, blockIdx.x, grid);
+  s.w_hi = range_start(s.W, blockIdx.x + 1, grid);
   return s;
 }
-
-__device__ __forceinline__ void unit_coords(const Sched& s, int u, int& mt, int& nt, int& sp) {
-  mt = u % s.m_tiles;
-  const int r = u / s.m_tiles;
-  sp = r % s.split;
-  nt = r / s.split;
+struct Seg {
+  int tile, mt, nt, kb0, kb1, piece, npieces, slot, mine;   // slot = CTA where the tile's SK work starts
+};
+// i-th segment of this CTA: data-parallel tiles first, then stream-K segments starting at work w
+__device__ __forceinline__ Seg dp_seg(const Sched& s, int i) {
+  Seg g;
+  g.tile = blockIdx.x + i * gridDim.x;
+  g.kb0 = 0;
+  g.kb1 = s.kb;
+  g.piece = 0;
+  g.npieces = 1;
+  g.slot = 0;
+  g.mine = 0;
+  g.mt = g.tile % s.m_tiles;
+  g.nt = g.tile / s.m_tiles;
+  return g;
 }
+__device__ __forceinline__ Seg sk_seg(const Sched& s, long long w) {
+  Seg g;
+  const int lt = (int)(w / s.kb);
+  g.tile = s.dp_tiles + lt;
+  g.kb0 = (int)(w % s.kb);
+  g.kb1 = (int)min((long long)s.kb, g.kb0 + (s.w_hi - w));
+  g.mt = g.tile % s.m_tiles;
+  g.nt = g.tile / s.m_tiles;
+  const long long t0 = (long long)lt * s.kb;
+  const int o0 = owner(s.W, t0, gridDim.x), o1 = owner(s.W, t0 + s.kb - 1, gridDim.x);
+  g.piece = blockIdx.x - o0;
+  g.npieces = o1 - o0 + 1;
+  g.slot = o0;
+  g.mine = (int)(s.w_lo / s.kb) == lt ? 0 : 1;
+  return g;
+}
+// iterate this CTA's segments: for (SegIter it(sc); it.valid(); it.next()) { const Seg& g = it.g; ... }
+struct SegIter {
+  const Sched& s;
+  int i;
+  long long w;
+  Seg g;
+  __device__ __forceinline__ explicit SegIter(const Sched& sc) : s(sc), i(0), w(sc.w_lo) { load(); }
+  __device__ __forceinline__ bool valid() const { return i < s.dp_mine || w < s.w_hi; }
+  __device__ __forceinline__ void load() {
+    if (i < s.dp_mine) g = dp_seg(s, i);
+    else if (w < s.w_hi) g = sk_seg(s, w);
+  }
+  __device__ __forceinline__ void next() {
+    if (i < s.dp_mine) ++i;
+    else w += g.kb1 - g.kb0;
+    load();
+  }
+};
 
 // ---------------------------------------------------------------- epilogue emitters
 // `chunk(c0, v)` yields 32 consecutive fp32 accumulator columns [c0, c0+32) of this thread's row of the
 // tile (TMEM or merged split partials); it must be called uniformly by the whole warp.
-template <int MODE, typename Chunk>
+template <int MODE, int BN, typename Chunk>
 __device__ __forceinline__ void epilogue_tile(Chunk&& chunk, int row, bool row_ok, int nt, int N, float* __restrict__ C,
                                               int ldc, const GemmEpi& epi) {
   if constexpr (MODE == GEMM_STORE || MODE == GEMM_ADD) {
@@ -180,11 +240,12 @@ __device__ __forceinline__ void epilogue_tile(Chunk&& chunk, int row, bool row_o
   }
 }
 
-template <int MODE>
+template <int MODE, int BN>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, float* __restrict__ C,
               int ldc, int N, int K, const int* __restrict__ M_dev, int M_max, float* __restrict__ ws,
-              int* __restrict__ sem, int ws_tiles_cap, const GemmEpi epi) {
+              int* __restrict__ sem, int policy, const GemmEpi epi) {
+  constexpr int STAGES = GT<BN>::STAGES, B_BYTES = GT<BN>::B_BYTES, STAGE_BYTES = GT<BN>::STAGE_BYTES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* sA = smem;                                   // STAGES x A_BYTES
@@ -199,7 +260,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int M = M_dev ? min(*M_dev, M_max) : M_max;
-  const Sched sc = make_sched(M, N, K, gridDim.x, ws_tiles_cap);
+  const Sched sc = make_sched<BN>(M, N, K, policy);
 
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < STAGES; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
@@ -223,15 +284,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int u = blockIdx.x; u < sc.units; u += gridDim.x) {
-        int mt, nt, sp;
-        unit_coords(sc, u, mt, nt, sp);
-        const int kb0 = sp * sc.kb_total / sc.split, kb1 = (sp + 1) * sc.kb_total / sc.split;
-        for (int kb = kb0; kb < kb1; ++kb) {
+      for (SegIter si(sc); si.valid(); si.next()) {
+        const Seg& g = si.g;
+        for (int kb = g.kb0; kb < g.kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_expect_tx(&full[stage], STAGE_BYTES);
-          tma_load_2d(sA + stage * A_BYTES, &mapA, &full[stage], kb * BK, mt * BM);
-          tma_load_2d(sB + stage * B_BYTES, &mapB, &full[stage], kb * BK, nt * BN);
+          tma_load_2d(sA + stage * A_BYTES, &mapA, &full[stage], kb * BK, g.mt * BM);
+          tma_load_2d(sB + stage * B_BYTES, &mapB, &full[stage], kb * BK, g.nt * BN);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -243,10 +302,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int u = blockIdx.x; u < sc.units; u += gridDim.x, ++it) {
-        int mt, nt, sp;
-        unit_coords(sc, u, mt, nt, sp);
-        const int kb0 = sp * sc.kb_total / sc.split, kb1 = (sp + 1) * sc.kb_total / sc.split;
+      for (SegIter si(sc); si.valid(); si.next(), ++it) {
+        const Seg& g = si.g;
+        const int kb0 = g.kb0, kb1 = g.kb1;
         const int acc = it & 1;
         mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
         tc_fence_after();
@@ -269,26 +327,26 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int q = warp - 4;
     const int et = threadIdx.x - 128;                   // 0..127
     int it = 0;
-    for (int u = blockIdx.x; u < sc.units; u += gridDim.x, ++it) {
-      int mt, nt, sp;
-      unit_coords(sc, u, mt, nt, sp);
+    for (SegIter si(sc); si.valid(); si.next(), ++it) {
+      const Seg& g = si.g;
+      const int nt = g.nt;
       const int acc = it & 1;
       mbar_wait(&tfull[acc], (it >> 1) & 1);
       tc_fence_after();
-      const int row = mt * BM + q * 32 + lane;
+      const int row = g.mt * BM + q * 32 + lane;
       const bool row_ok = row < M;
       const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
-      const int tile = nt * sc.m_tiles + mt;
-      if (sc.split == 1) {
+      if (g.npieces == 1) {
         // accumulator chunks straight from TMEM (warp-collective loads)
         auto chunk = [&](int c0, float* v) { tmem_ld32(taddr + c0, v); };
-        epilogue_tile<MODE>(chunk, row, row_ok, nt, N, C, ldc, epi);
+        epilogue_tile<MODE, BN>(chunk, row, row_ok, nt, N, C, ldc, epi);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[acc]);
       } else {
-        // split-K: write the partial, last-arriving split reduces all partials in split order
-        float* my = ws + ((size_t)tile * sc.split + sp) * (BM * BN) + (size_t)(q * 32 + lane) * BN;
+        // piece of a tile split across CTAs: write the partial, the last-arriving piece reduces all
+        // partials in piece (= k) order
+        float* my = ws + ((size_t)blockIdx.x * 2 + g.mine) * (BM * BN) + (size_t)(q * 32 + lane) * BN;
 #pragma unroll 1
         for (int c0 = 0; c0 < BN; c0 += 32) {
           float v[32];
@@ -302,27 +360,33 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (lane == 0) mbar_arrive(&tempty[acc]);
         __threadfence();
         asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (et == 0) *flag_sh = atomicAdd(&sem[tile], 1);
+        if (et == 0) *flag_sh = atomicAdd(&sem[g.slot], 1);
         asm volatile("bar.sync 1, 128;" ::: "memory");
-        const bool last = *flag_sh == sc.split - 1;
+        const bool last = *flag_sh == g.npieces - 1;
         asm volatile("bar.sync 1, 128;" ::: "memory");
         if (last) {
           __threadfence();
-          const float* base = ws + (size_t)tile * sc.split * (BM * BN) + (size_t)(q * 32 + lane) * BN;
+          // piece p was written by CTA slot+p: into its slot 1 if p == 0 and the tile is not that CTA's
+          // first segment, else into its slot 0
+          const int w0 = (int)(range_start(sc.W, g.slot, gridDim.x) / sc.kb) == g.tile - sc.dp_tiles ? 0 : 1;
+          const size_t row_off = (size_t)(q * 32 + lane) * BN;
+          auto piece_ptr = [&](int p) {
+            return ws + ((size_t)(g.slot + p) * 2 + (p == 0 ? w0 : 0)) * (BM * BN) + row_off;
+          };
           auto chunk = [&](int c0, float* v) {
 #pragma unroll
             for (int i = 0; i < 32; i += 4) {
-              float4 s4 = __ldcg(reinterpret_cast<const float4*>(base + c0 + i));
-              for (int p = 1; p < sc.split; ++p) {
-                const float4 t = __ldcg(reinterpret_cast<const float4*>(base + (size_t)p * (BM * BN) + c0 + i));
+              float4 s4 = __ldcg(reinterpret_cast<const float4*>(piece_ptr(0) + c0 + i));
+              for (int p = 1; p < g.npieces; ++p) {
+                const float4 t = __ldcg(reinterpret_cast<const float4*>(piece_ptr(p) + c0 + i));
                 s4.x += t.x; s4.y += t.y; s4.z += t.z; s4.w += t.w;
               }
               v[i] = s4.x; v[i + 1] = s4.y; v[i + 2] = s4.z; v[i + 3] = s4.w;
             }
           };
-          epilogue_tile<MODE>(chunk, row, row_ok, nt, N, C, ldc, epi);
+          epilogue_tile<MODE, BN>(chunk, row, row_ok, nt, N, C, ldc, epi);
           asm volatile("bar.sync 1, 128;" ::: "memory");
-          if (et == 0) sem[tile] = 0;
+          if (et == 0) sem[g.slot] = 0;
         }
       }
     }
@@ -377,41 +441,65 @@ int gemm_backend() {
 
 void gemm_set_backend(int b) { g_backend = b; }
 
-bool launch_gemm_tc(const bf16* A, int lda, int a_rows, const bf16* W, int N, int K, float* C, int ldc, const int* M_dev,
-                    int M_max, GemmMode mode, const GemmWs& ws, cudaStream_t s, const GemmEpi* epi) {
+template <int BN>
+static bool launch_bn(const bf16* A, int lda, int a_rows, const bf16* W, int N, int K, float* C, int ldc,
+                      const int* M_dev, int M_max, GemmMode mode, const GemmWs& ws, cudaStream_t s, const GemmEpi* epi) {
   using namespace tc;
-  if (M_max <= 0) return true;
-  if (K % BK || lda % 8 || a_rows < 1) return false;
   if ((mode == GEMM_SWIGLU || mode == GEMM_QKV_ROPE) && (!epi || N % BN)) return false;
-  if (mode == GEMM_QKV_ROPE && epi->kv.head_dim != 128) return false;
+  if (mode == GEMM_SWIGLU && BN != 2 * kGuGroup) return false;
+  if (mode == GEMM_QKV_ROPE && (epi->kv.head_dim != 128 || BN % 128)) return false;
   CUtensorMap ma, mb;
   if (!get_map(A, a_rows, K, lda, BM, &ma) || !get_map(W, N, K, K, BN, &mb)) return false;
+  constexpr int SMEM = GT<BN>::SMEM_BYTES;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_gemm_tc<GEMM_STORE>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    cudaFuncSetAttribute(k_gemm_tc<GEMM_ADD>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    cudaFuncSetAttribute(k_gemm_tc<GEMM_SWIGLU>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    cudaFuncSetAttribute(k_gemm_tc<GEMM_QKV_ROPE>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    cudaFuncSetAttribute(k_gemm_tc<GEMM_STORE, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    cudaFuncSetAttribute(k_gemm_tc<GEMM_ADD, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    if constexpr (BN == 2 * kGuGroup)
+      cudaFuncSetAttribute(k_gemm_tc<GEMM_SWIGLU, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    cudaFuncSetAttribute(k_gemm_tc<GEMM_QKV_ROPE, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
     attr = true;
   }
-  const int max_units = ((M_max + BM - 1) / BM) * ((N + BN - 1) / BN) * MAX_SPLIT;
-  const int grid = std::max(1, std::min(num_sms(), max_units));
-  const int cap = (int)std::min<size_t>(ws.sem_count, ws.bytes / (sizeof(float) * BM * BN));
+  // grid: one CTA per SM, never more CTAs than k-blocks of work at the smallest live M (one m-tile),
+  // and at most as many as the partial workspace (two slots per CTA) and semaphores allow
+  const long long w_min = (long long)((N + BN - 1) / BN) * (K / BK);
+  int grid = (int)std::min<long long>(num_sms(), std::max<long long>(1, w_min));
+  grid = std::max(1, std::min<int>(grid, (int)std::min<size_t>(ws.sem_count, ws.bytes / (sizeof(float) * BM * BN * 2))));
+  static int policy = -1;
+  if (policy < 0) {   // default: data-parallel tiles (measured fastest at the decode shapes)
+    const char* e = getenv("FOCUS_GEMM_SCHED");
+    policy = (e && e[0] == 's') ? 1 : (e && e[0] == 'h') ? 0 : 2;
+  }
   const GemmEpi e = epi ? *epi : GemmEpi{};
   switch (mode) {
     case GEMM_ADD:
-      k_gemm_tc<GEMM_ADD><<<grid, NUM_THREADS, SMEM_BYTES, s>>>(ma, mb, C, ldc, N, K, M_dev, M_max, ws.ptr, ws.sem, cap, e);
+      k_gemm_tc<GEMM_ADD, BN><<<grid, NUM_THREADS, SMEM, s>>>(ma, mb, C, ldc, N, K, M_dev, M_max, ws.ptr, ws.sem, policy, e);
       break;
     case GEMM_SWIGLU:
-      k_gemm_tc<GEMM_SWIGLU><<<grid, NUM_THREADS, SMEM_BYTES, s>>>(ma, mb, C, ldc, N, K, M_dev, M_max, ws.ptr, ws.sem, cap, e);
+      if constexpr (BN == 2 * kGuGroup)
+        k_gemm_tc<GEMM_SWIGLU, BN><<<grid, NUM_THREADS, SMEM, s>>>(ma, mb, C, ldc, N, K, M_dev, M_max, ws.ptr, ws.sem, policy, e);
       break;
     case GEMM_QKV_ROPE:
-      k_gemm_tc<GEMM_QKV_ROPE><<<grid, NUM_THREADS, SMEM_BYTES, s>>>(ma, mb, C, ldc, N, K, M_dev, M_max, ws.ptr, ws.sem, cap, e);
+      k_gemm_tc<GEMM_QKV_ROPE, BN><<<grid, NUM_THREADS, SMEM, s>>>(ma, mb, C, ldc, N, K, M_dev, M_max, ws.ptr, ws.sem, policy, e);
       break;
     default:
-      k_gemm_tc<GEMM_STORE><<<grid, NUM_THREADS, SMEM_BYTES, s>>>(ma, mb, C, ldc, N, K, M_dev, M_max, ws.ptr, ws.sem, cap, e);
+      k_gemm_tc<GEMM_STORE, BN><<<grid, NUM_THREADS, SMEM, s>>>(ma, mb, C, ldc, N, K, M_dev, M_max, ws.ptr, ws.sem, policy, e);
   }
   return true;
+}
+
+// m_est: expected live row count (host estimate, e.g. last step's counter) used only to pick the tile
+// width: 128-wide tiles when 256-wide tiles would leave more than ~half of the SMs idle.
+bool launch_gemm_tc(const bf16* A, int lda, int a_rows, const bf16* W, int N, int K, float* C, int ldc, const int* M_dev,
+                    int M_max, GemmMode mode, const GemmWs& ws, cudaStream_t s, const GemmEpi* epi, int m_est) {
+  using namespace tc;
+  if (M_max <= 0) return true;
+  if (K % BK || lda % 8 || a_rows < 1) return false;
+  const int m = m_est > 0 ? std::min(m_est, M_max) : M_max;
+  const long long tiles256 = (long long)((m + BM - 1) / BM) * ((N + 255) / 256);
+  const bool narrow = mode != GEMM_SWIGLU && 2 * tiles256 <= (num_sms() * 11) / 10 && getenv("FOCUS_GEMM_BN256") == nullptr;
+  if (narrow) return launch_bn<128>(A, lda, a_rows, W, N, K, C, ldc, M_dev, M_max, mode, ws, s, epi);
+  return launch_bn<256>(A, lda, a_rows, W, N, K, C, ldc, M_dev, M_max, mode, ws, s, epi);
 }
 
 }  // namespace focus

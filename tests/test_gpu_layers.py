@@ -30,6 +30,11 @@ MINI_G2 = ModelConfig(n_layers=3, d_model=512, n_q_heads=8, n_kv_heads=4, head_d
                       rope_theta=1e6)
 
 
+# GEMM stage tolerance: fp32 accumulation on the tensor core over K <= 12288 (DESIGN.md §7 "numerics":
+# the MMA's internal accumulation order is not the fp64 reference order; ~sqrt(K) * 2^-23 relative)
+GEMM_TOL = 5e-5
+
+
 def _bf16_close(got, want, tag, frac=0.95, tol=4e-3):
     assert rel_l2(got, want) < tol, (tag, rel_l2(got, want))
     assert np.mean(got == want) > frac, (tag, np.mean(got == want))
@@ -121,14 +126,14 @@ def test_layer_stages(model, B, nreq, prompt, taps, page):
             x_res = x_in
         x_mid = ctx.export_f32("TAP_X_MID", (Ma, d)).astype(np.float64)
         inc = att @ w["o"].T
-        assert rel_l2(x_mid - x_res, inc) < 1e-5, ("o-proj", l, rel_l2(x_mid - x_res, inc))
+        assert rel_l2(x_mid - x_res, inc) < GEMM_TOL, ("o-proj", l, rel_l2(x_mid - x_res, inc))
         h2 = ctx.export_bf16("TAP_H2", (Ma, d))
         _bf16_close(h2, bf16_round(rms_norm(x_mid, 1.0, model.rms_eps)), ("rmsnorm2", l), frac=0.99)
         act = ctx.export_bf16("TAP_ACT", (Ma, model.d_ff))
         _bf16_close(act, bf16_round(silu(f32(h2 @ w["gate"].T)) * f32(h2 @ w["up"].T)), ("swiglu", l))
         x_out = ctx.export_f32("TAP_X_OUT", (Ma, d)).astype(np.float64)
         inc = act @ w["down"].T
-        assert rel_l2(x_out - x_mid, inc) < 1e-5, ("down", l, rel_l2(x_out - x_mid, inc))
+        assert rel_l2(x_out - x_mid, inc) < GEMM_TOL, ("down", l, rel_l2(x_out - x_mid, inc))
         # LM head on S cap M rows (sampled vocab columns) after the last layer
         if l == model.n_layers - 1 and ML:
             hl = ctx.export_bf16("HL", (ML, d))
@@ -137,7 +142,7 @@ def test_layer_stages(model, B, nreq, prompt, taps, page):
             logits = ctx.export_f32("LOGITS", (ML, model.vocab))
             for lo in (0, model.vocab - 2048):
                 wl = weight_matrix(TID_LMHEAD, model.vocab, d, d, run.weight_seed, lo, lo + 2048).astype(np.float64)
-                assert rel_l2(logits[:, lo:lo + 2048], hl @ wl.T) < 1e-5, ("lm-head", lo)
+                assert rel_l2(logits[:, lo:lo + 2048], hl @ wl.T) < GEMM_TOL, ("lm-head", lo)
         ctx.commit_results(live)
     ctx.focus_set_tap(-1)
     ctx.focus_sync()
