@@ -49,19 +49,36 @@ constexpr int TMEM_COLS = 512;
 struct Sched {
   int m_tiles, n_tiles, kb, tiles, dp_tiles, sk_tiles, dp_mine;
   long long W, w_lo, w_hi;                          // stream-K work and this CTA's range
+  int cs, rank, cluster, n_clusters, m_groups;     // clusters of cs CTAs share one weight tile (multicast)
 };
 __device__ __forceinline__ long long range_start(long long W, int b, int grid) { return (long long)b * W / grid; }
 // CTA whose stream-K range contains work position x
 __device__ __forceinline__ int owner(long long W, long long x, int grid) {
   return (int)(((x + 1) * grid + W - 1) / W) - 1;
 }
-template <int BN>
+template <int BN, int CS>
 __device__ __forceinline__ Sched make_sched(int M, int N, int K, int policy) {
   Sched s;
   s.m_tiles = (M + BM - 1) / BM;
   s.n_tiles = (N + BN - 1) / BN;
   s.kb = K / BK;
   s.tiles = s.m_tiles * s.n_tiles;
+  s.cs = CS;
+  s.rank = CS > 1 ? (int)cluster_ctarank() : 0;
+  s.cluster = blockIdx.x / CS;
+  s.n_clusters = gridDim.x / CS;
+  s.m_groups = (s.m_tiles + CS - 1) / CS;
+  if (CS > 1) {
+    // cluster-granular data-parallel units (weight tile nt, m-group): CTA rank r takes m-tile
+    // mg * CS + r (past the live rows it computes discarded rows so the multicast stays in lockstep)
+    const int units = s.n_tiles * s.m_groups;
+    s.dp_tiles = units;
+    s.sk_tiles = 0;
+    s.dp_mine = units > s.cluster ? (units - 1 - s.cluster) / s.n_clusters + 1 : 0;
+    s.W = 0;
+    s.w_lo = s.w_hi = 0;
+    return s;
+  }
   const int grid = gridDim.x;
   // policy 0: hybrid, 1: all stream-K, 2: all data-parallel
   s.dp_tiles = policy == 1 ? 0 : (policy == 2 ? s.tiles : (s.tiles / grid) * grid);
@@ -78,15 +95,22 @@ struct Seg {
 // i-th segment of this CTA: data-parallel tiles first, then stream-K segments starting at work w
 __device__ __forceinline__ Seg dp_seg(const Sched& s, int i) {
   Seg g;
-  g.tile = blockIdx.x + i * gridDim.x;
   g.kb0 = 0;
   g.kb1 = s.kb;
   g.piece = 0;
   g.npieces = 1;
   g.slot = 0;
   g.mine = 0;
-  g.mt = g.tile % s.m_tiles;
-  g.nt = g.tile / s.m_tiles;
+  if (s.cs > 1) {
+    const int u = s.cluster + i * s.n_clusters;
+    g.nt = u / s.m_groups;
+    g.mt = (u % s.m_groups) * s.cs + s.rank;
+    g.tile = g.nt * s.m_tiles + g.mt;
+  } else {
+    g.tile = blockIdx.x + i * gridDim.x;
+    g.mt = g.tile % s.m_tiles;
+    g.nt = g.tile / s.m_tiles;
+  }
   return g;
 }
 __device__ __forceinline__ Seg sk_seg(const Sched& s, long long w) {
@@ -240,7 +264,7 @@ __device__ __forceinline__ void epilogue_tile(Chunk&& chunk, int row, bool row_o
   }
 }
 
-template <int MODE, int BN>
+template <int MODE, int BN, int CS>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, float* __restrict__ C,
               int ldc, int N, int K, const int* __restrict__ M_dev, int M_max, float* __restrict__ ws,
@@ -260,10 +284,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int M = M_dev ? min(*M_dev, M_max) : M_max;
-  const Sched sc = make_sched<BN>(M, N, K, policy);
+  const Sched sc = make_sched<BN, CS>(M, N, K, policy);
+  constexpr uint16_t cmask = (uint16_t)((1u << CS) - 1u);
 
   if (warp == 0 && lane == 0) {
-    for (int i = 0; i < STAGES; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+    // empty[s] completes when the MMA of every CTA of the cluster has consumed stage s (each CTA's
+    // commit multicasts an arrival), so any CTA may then multicast its W slice into all of them
+    for (int i = 0; i < STAGES; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], CS); }
     for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 4); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&mapA) : "memory");
@@ -276,6 +303,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if (CS > 1) cluster_sync();                           // peers' barriers initialised before any multicast
   tc_fence_after();
   const uint32_t tmem = *tmem_base_sh;
 
@@ -290,7 +318,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_expect_tx(&full[stage], STAGE_BYTES);
           tma_load_2d(sA + stage * A_BYTES, &mapA, &full[stage], kb * BK, g.mt * BM);
-          tma_load_2d(sB + stage * B_BYTES, &mapB, &full[stage], kb * BK, g.nt * BN);
+          if (CS == 1) {
+            tma_load_2d(sB + stage * B_BYTES, &mapB, &full[stage], kb * BK, g.nt * BN);
+          } else {                                      // my 1/CS slice of the W tile, to every CTA
+            constexpr int SL = BN / CS;
+            tma_load_2d_mc(sB + stage * B_BYTES + sc.rank * SL * 128, &mapB, &full[stage], kb * BK,
+                           g.nt * BN + sc.rank * SL, cmask);
+          }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -316,7 +350,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k)
             mma_bf16(d, desc_kmajor_sw128(a0 + k * 32), desc_kmajor_sw128(b0 + k * 32), idesc, (kb > kb0 || k > 0) ? 1u : 0u);
-          mma_commit(&empty[stage]);
+          if (CS == 1) mma_commit(&empty[stage]);
+          else mma_commit_mc(&empty[stage], cmask);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
         mma_commit(&tfull[acc]);
@@ -392,6 +427,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
   }
   __syncthreads();
+  if (CS > 1) cluster_sync();                           // no CTA leaves while peers may still signal it
   if (warp == 2) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
@@ -441,7 +477,31 @@ int gemm_backend() {
 
 void gemm_set_backend(int b) { g_backend = b; }
 
-template <int BN>
+template <int MODE, int BN, int CS>
+static void launch_k(int grid, int smem, cudaStream_t s, const CUtensorMap& ma, const CUtensorMap& mb, float* C, int ldc,
+                     int N, int K, const int* M_dev, int M_max, const GemmWs& ws, int policy, const GemmEpi& e) {
+  using namespace tc;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_gemm_tc<MODE, BN, CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(NUM_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CS;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k_gemm_tc<MODE, BN, CS>, ma, mb, C, ldc, N, K, M_dev, M_max, ws.ptr, ws.sem, policy, e);
+}
+
+template <int BN, int CS>
 static bool launch_bn(const bf16* A, int lda, int a_rows, const bf16* W, int N, int K, float* C, int ldc,
                       const int* M_dev, int M_max, GemmMode mode, const GemmWs& ws, cudaStream_t s, const GemmEpi* epi) {
   using namespace tc;
@@ -449,22 +509,14 @@ static bool launch_bn(const bf16* A, int lda, int a_rows, const bf16* W, int N, 
   if (mode == GEMM_SWIGLU && BN != 2 * kGuGroup) return false;
   if (mode == GEMM_QKV_ROPE && (epi->kv.head_dim != 128 || BN % 128)) return false;
   CUtensorMap ma, mb;
-  if (!get_map(A, a_rows, K, lda, BM, &ma) || !get_map(W, N, K, K, BN, &mb)) return false;
+  if (!get_map(A, a_rows, K, lda, BM, &ma) || !get_map(W, N, K, K, BN / CS, &mb)) return false;
   constexpr int SMEM = GT<BN>::SMEM_BYTES;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_gemm_tc<GEMM_STORE, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-    cudaFuncSetAttribute(k_gemm_tc<GEMM_ADD, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-    if constexpr (BN == 2 * kGuGroup)
-      cudaFuncSetAttribute(k_gemm_tc<GEMM_SWIGLU, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-    cudaFuncSetAttribute(k_gemm_tc<GEMM_QKV_ROPE, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-    attr = true;
-  }
-  // grid: one CTA per SM, never more CTAs than k-blocks of work at the smallest live M (one m-tile),
-  // and at most as many as the partial workspace (two slots per CTA) and semaphores allow
-  const long long w_min = (long long)((N + BN - 1) / BN) * (K / BK);
+  // grid: one CTA per SM (a multiple of the cluster size), never more CTAs than k-blocks of work at
+  // the smallest live M (one m-tile), and at most as many as the partial workspace and semaphores allow
+  const long long w_min = (long long)((N + BN - 1) / BN) * (K / BK) * CS;
   int grid = (int)std::min<long long>(num_sms(), std::max<long long>(1, w_min));
   grid = std::max(1, std::min<int>(grid, (int)std::min<size_t>(ws.sem_count, ws.bytes / (sizeof(float) * BM * BN * 2))));
+  grid = std::max(CS, grid / CS * CS);
   static int policy = -1;
   if (policy < 0) {   // default: data-parallel tiles (measured fastest at the decode shapes)
     const char* e = getenv("FOCUS_GEMM_SCHED");
@@ -472,18 +524,15 @@ static bool launch_bn(const bf16* A, int lda, int a_rows, const bf16* W, int N, 
   }
   const GemmEpi e = epi ? *epi : GemmEpi{};
   switch (mode) {
-    case GEMM_ADD:
-      k_gemm_tc<GEMM_ADD, BN><<<grid, NUM_THREADS, SMEM, s>>>(ma, mb, C, ldc, N, K, M_dev, M_max, ws.ptr, ws.sem, policy, e);
-      break;
+    case GEMM_ADD: launch_k<GEMM_ADD, BN, CS>(grid, SMEM, s, ma, mb, C, ldc, N, K, M_dev, M_max, ws, policy, e); break;
     case GEMM_SWIGLU:
       if constexpr (BN == 2 * kGuGroup)
-        k_gemm_tc<GEMM_SWIGLU, BN><<<grid, NUM_THREADS, SMEM, s>>>(ma, mb, C, ldc, N, K, M_dev, M_max, ws.ptr, ws.sem, policy, e);
+        launch_k<GEMM_SWIGLU, BN, CS>(grid, SMEM, s, ma, mb, C, ldc, N, K, M_dev, M_max, ws, policy, e);
       break;
     case GEMM_QKV_ROPE:
-      k_gemm_tc<GEMM_QKV_ROPE, BN><<<grid, NUM_THREADS, SMEM, s>>>(ma, mb, C, ldc, N, K, M_dev, M_max, ws.ptr, ws.sem, policy, e);
+      launch_k<GEMM_QKV_ROPE, BN, CS>(grid, SMEM, s, ma, mb, C, ldc, N, K, M_dev, M_max, ws, policy, e);
       break;
-    default:
-      k_gemm_tc<GEMM_STORE, BN><<<grid, NUM_THREADS, SMEM, s>>>(ma, mb, C, ldc, N, K, M_dev, M_max, ws.ptr, ws.sem, policy, e);
+    default: launch_k<GEMM_STORE, BN, CS>(grid, SMEM, s, ma, mb, C, ldc, N, K, M_dev, M_max, ws, policy, e);
   }
   return true;
 }
@@ -498,8 +547,17 @@ bool launch_gemm_tc(const bf16* A, int lda, int a_rows, const bf16* W, int N, in
   const int m = m_est > 0 ? std::min(m_est, M_max) : M_max;
   const long long tiles256 = (long long)((m + BM - 1) / BM) * ((N + 255) / 256);
   const bool narrow = mode != GEMM_SWIGLU && 2 * tiles256 <= (num_sms() * 11) / 10 && getenv("FOCUS_GEMM_BN256") == nullptr;
-  if (narrow) return launch_bn<128>(A, lda, a_rows, W, N, K, C, ldc, M_dev, M_max, mode, ws, s, epi);
-  return launch_bn<256>(A, lda, a_rows, W, N, K, C, ldc, M_dev, M_max, mode, ws, s, epi);
+  // opt-in (FOCUS_GEMM_MC=1): clusters of 4 CTAs (the 4 m-tiles of a weight tile) share W by TMA
+  // multicast when the live row count fills them.  Measured no faster at the C3 shapes (at cluster
+  // size <= 4 the L2 already serves the duplicate requests once), so one CTA per tile by default.
+  const int m_tiles = (m + BM - 1) / BM;
+  const bool cluster4 = getenv("FOCUS_GEMM_MC") != nullptr && m_tiles % 4 == 0;
+  if (narrow) {
+    if (cluster4) return launch_bn<128, 4>(A, lda, a_rows, W, N, K, C, ldc, M_dev, M_max, mode, ws, s, epi);
+    return launch_bn<128, 1>(A, lda, a_rows, W, N, K, C, ldc, M_dev, M_max, mode, ws, s, epi);
+  }
+  if (cluster4) return launch_bn<256, 4>(A, lda, a_rows, W, N, K, C, ldc, M_dev, M_max, mode, ws, s, epi);
+  return launch_bn<256, 1>(A, lda, a_rows, W, N, K, C, ldc, M_dev, M_max, mode, ws, s, epi);
 }
 
 }  // namespace focus

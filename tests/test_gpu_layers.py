@@ -42,6 +42,7 @@ def _bf16_close(got, want, tag, frac=0.95, tol=4e-3):
 
 @pytest.mark.parametrize("model,B,nreq,prompt,taps,page", [
     (M8B4, 16, 3, 100, (0, 1, 3), 64),
+    (M8B4, 16, 26, 40, (0, 1), 64),          # ~400 P rows: 4 m-tiles
     (M1P7B3, 4, 5, 70, (0, 1, 2), 64),
     (MINI128, 16, 3, 1100, (0, 1, 2), 16),
     (MINI128, 64, 2, 700, (0, 1, 2), 32),
@@ -146,3 +147,9 @@ def test_layer_stages(model, B, nreq, prompt, taps, page):
         ctx.commit_results(live)
     ctx.focus_set_tap(-1)
     ctx.focus_sync()
+
+
+def test_layer_stages_multicast_gemm(monkeypatch):
+    """Same stage-wise parity with the opt-in 4-CTA TMA-multicast GEMM clusters (4 m-tiles of rows)."""
+    monkeypatch.setenv("FOCUS_GEMM_MC", "1")
+    test_layer_stages(M8B4, 16, 26, 40, (0, 1), 64)
