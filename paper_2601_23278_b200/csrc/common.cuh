@@ -133,7 +133,12 @@ struct AttnArgs {
   float* part;                  // split partials [pair][max_nsplit][128 * head_dim + 2 * 128]
   float* imp_scratch;           // per-CTA block-score scratch [grid][128][64] (importance epilogue)
   unsigned long long* trace;    // debug: clock64 events [grid][8][kTraceEv] or nullptr
-  int* sem;                     // per-pair arrival counters (zero between launches)
+  int* sem;                     // (unused)
+  int* pair_nsplit;             // per (request, chunk, kv head): key splits of the last launch
+  int stream_k;                 // 1: stream-K over key tiles (balanced CTAs; attention without importance)
+  int may_split;                // 0: no key split is possible (host-known bound) -> no combine launch
+  void* plan_units;             // unit table [grid][UCAP] precomputed by k_attn_plan, or nullptr
+  int* plan_n;                  // [grid] units per CTA (nullptr: the kernel builds its table itself)
 };
 void launch_attention(const AttnArgs& a, cudaStream_t s);
 bool attn_tc_supported(int head_dim, int page_size, int group);
@@ -143,6 +148,8 @@ bool attn_tc_make_maps(const bf16* Kpool, const bf16* Vpool, size_t rows, int he
                        CUtensorMap* mk, CUtensorMap* mv);
 void launch_attention_tc(const CUtensorMap& mk, const CUtensorMap& mv, const CUtensorMap& mq, const AttnArgs& a,
                          cudaStream_t s);
+bool launch_attention_plan(const AttnArgs& a, cudaStream_t s);
+int attn_tc_plan_capacity();
 
 struct SelectArgs {
   const int* req_list; int n_req;

@@ -66,6 +66,8 @@ struct focus_ctx {
   float* attn_part = nullptr;
   float* attn_scratch = nullptr;
   unsigned long long* attn_trace = nullptr;
+  void* plan_units[4] = {};       // per-step attention unit tables: layer 0, layer-1 importance,
+  int* plan_n[4] = {};            // layer-1 suffix, layers >= 2
   int trace_layer = -1;
   int* attn_sem = nullptr;
   // weights
@@ -204,6 +206,10 @@ size_t carve(focus_ctx* x, char* base) {
     x->attn_part = (float*)take(pairs * x->max_nsplit * ((size_t)128 * c.head_dim + 256) * 4);
     x->attn_sem = (int*)take(pairs * 4);
     x->attn_scratch = (float*)take((size_t)1024 * 128 * kMaxB * 4);   // >= grid (one CTA per SM)
+    for (int k = 0; k < 4; ++k) {
+      x->plan_units[k] = take((size_t)1024 * attn_tc_plan_capacity() * 80);
+      x->plan_n[k] = (int*)take(1024 * 4);
+    }
     const char* tl = getenv("FOCUS_ATTN_TRACE_LAYER");
     x->trace_layer = tl ? atoi(tl) : -1;
     if (x->trace_layer >= 0) x->attn_trace = (unsigned long long*)take((size_t)1024 * 8 * kTraceEv * 8);
@@ -239,7 +245,7 @@ void derive(focus_ctx* x) {
   x->n_chunks = (x->B + x->attn_rpc - 1) / x->attn_rpc;
   x->split_tiles = 16;                         // 128-key tiles per split (the kernel may enlarge it)
   if (const char* e = getenv("FOCUS_ATTN_SPLIT_TILES")) x->split_tiles = std::max(2, atoi(e));
-  x->max_nsplit = ((c.max_seq_len + 127) / 128 + x->split_tiles - 1) / x->split_tiles + 1;
+  x->max_nsplit = std::max(16, ((c.max_seq_len + 127) / 128 + x->split_tiles - 1) / x->split_tiles + 1);
   x->nch_vocab = std::max(1, std::min(16, c.vocab / 8192));
   x->mask_id = c.vocab - 1;
   x->max_gen = c.max_seq_len;
@@ -407,13 +413,31 @@ AttnArgs attn_args(focus_ctx* x, int l, const bf16* q, int ldq, int n_req, const
   a.max_nsplit = x->max_nsplit;
   a.part = x->attn_part;
   a.sem = x->attn_sem;
+  a.pair_nsplit = x->attn_sem;      // reused as the per-pair split-count array
+  a.stream_k = getenv("FOCUS_ATTN_SK") ? 1 : 0;      // opt-in (measured slower at C3 with the combine)
+  // a key split can only happen with stream-K or when a context exceeds split_tiles 128-key tiles
+  a.may_split = a.stream_k || x->cfg.max_seq_len > 128 * x->split_tiles;
   a.imp_scratch = x->attn_scratch;
   a.trace = (l == x->trace_layer && x->cfg.debug_taps >= 0) ? x->attn_trace : nullptr;
   return a;
 }
 
+// Precompute the unit table of an attention launch shape into plan slot k; on success the args point
+// the kernel at it (otherwise the kernel builds its own table).
+bool plan_attention(focus_ctx* x, AttnArgs& a, int k) {
+  a.plan_units = x->plan_units[k];
+  a.plan_n = x->plan_n[k];
+  if (getenv("FOCUS_ATTN_NOPLAN") || !launch_attention_plan(a, x->stream)) {
+    a.plan_units = nullptr;
+    a.plan_n = nullptr;
+    return false;
+  }
+  return true;
+}
+
 void run_attention(focus_ctx* x, const AttnArgs& a) {
   if (a.trace) cudaMemsetAsync(a.trace, 0, (size_t)num_sms() * 8 * kTraceEv * 8, x->stream);
+  if (x->attn_tc && !a.imp_only && a.ext_mode != 2 && a.may_split) ++x->launches;   // + split combine
   if (x->attn_tc) launch_attention_tc(x->mapK, x->mapV, a.q == x->qS ? x->mapQ_qs : x->mapQ_qkv, a, x->stream);
   else launch_attention(a, x->stream);
 }
@@ -661,22 +685,21 @@ focus_status focus_step_block(focus_ctx* x, const int32_t* ids, int32_t n_req) {
   RowSpace rsP{MP, maxP, x->rowP, est.M_P};
   RowSpace rsS{MS, maxP, x->rowS, est.M_S};
   // A2 layer 0 fully on P (+ fused importance I0)
+  // attention unit tables of the P-row launches (layer 0, layer-1 importance), once per step
+  AttnArgs a0 = attn_args(x, 0, x->qkv, x->qkv_dim, n_req, x->offP, 0);
+  a0.imp = x->I0p;
+  AttnArgs a1 = attn_args(x, 1, x->qkv, x->qkv_dim, n_req, x->offP, 0);
+  a1.imp = x->I1p;
+  a1.imp_only = 1;
+  a1.out = nullptr;
+  if (x->attn_tc && plan_attention(x, a0, 0)) ++x->launches;
+  if (x->attn_tc && plan_attention(x, a1, 1)) ++x->launches;
   qkv_piece(x, 0, 0, x->x, rsP);
-  {
-    AttnArgs a = attn_args(x, 0, x->qkv, x->qkv_dim, n_req, x->offP, 0);
-    a.imp = x->I0p;
-    LAUNCH(ATTN, run_attention(x, a));
-  }
+  LAUNCH(ATTN, run_attention(x, a0));
   out_mlp_piece(x, 0, 0, x->x, rsP);
   // A3 layer-1 projections on P, K1/V1 stored before eviction, importance-only I1
   qkv_piece(x, 1, 1, x->x, rsP);
-  {
-    AttnArgs a = attn_args(x, 1, x->qkv, x->qkv_dim, n_req, x->offP, 0);
-    a.imp = x->I1p;
-    a.imp_only = 1;
-    a.out = nullptr;
-    LAUNCH(IMPORTANCE, run_attention(x, a));
-  }
+  LAUNCH(IMPORTANCE, run_attention(x, a1));
   // A4 selection + compaction plan, A5 gather
   {
     SelectArgs sa{};
@@ -703,16 +726,22 @@ focus_status focus_step_block(focus_ctx* x, const int32_t* ids, int32_t n_req) {
   }
   LAUNCH(GATHER, launch_gather_rows(x->x, x->qkv, x->qkv_dim, x->q_dim, x->srcP, MS, maxP, c.d_model, x->x2, x->qS, s));
   tap(x, 1, TAP_QS, x->qS, (size_t)maxP * x->q_dim * 2);
+  // attention unit tables of the S-row launches (layer-1 suffix, layers >= 2), once per step
+  AttnArgs a2 = attn_args(x, 1, x->qS, x->q_dim, n_req, x->offS, 0);
+  AttnArgs a3 = attn_args(x, 2, x->qkv, x->qkv_dim, n_req, x->offS, 1);
+  if (x->attn_tc && plan_attention(x, a2, 2)) ++x->launches;
+  if (x->attn_tc && c.n_layers > 2 && plan_attention(x, a3, 3)) ++x->launches;
   // A6 layer-1 suffix on S: keys = context + whole block
-  {
-    AttnArgs a = attn_args(x, 1, x->qS, x->q_dim, n_req, x->offS, 0);
-    LAUNCH(ATTN, run_attention(x, a));
-  }
+  LAUNCH(ATTN, run_attention(x, a2));
   out_mlp_piece(x, 1, 1, x->x2, rsS);
-  // A7 layers 2.. on S: keys = context + block [0, R']
+  // A7 layers 2.. on S: keys = context + block [0, R'] (same unit table for every layer)
   for (int l = 2; l < c.n_layers; ++l) {
     qkv_piece(x, l, l, x->x2, rsS);
-    AttnArgs a = attn_args(x, l, x->qkv, x->qkv_dim, n_req, x->offS, 1);
+    AttnArgs a = a3;
+    const AttnArgs al = attn_args(x, l, x->qkv, x->qkv_dim, n_req, x->offS, 1);
+    a.kv = al.kv;
+    a.layer = l;
+    a.trace = al.trace;
     LAUNCH(ATTN, run_attention(x, a));
     out_mlp_piece(x, l, l, x->x2, rsS);
   }

@@ -412,53 +412,17 @@ __device__ __noinline__ void importance_epilogue(const AttnArgs& a, const Unit& 
   named_bar(1, 128);                               // red[] reuse
 }
 
-template <bool IMP_ONLY>
-__global__ void __launch_bounds__(NTHREADS, 1)
-    k_attn_tc(const __grid_constant__ CUtensorMap mapK, const __grid_constant__ CUtensorMap mapV,
-              const __grid_constant__ CUtensorMap mapQ, AttnArgs a) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  uint8_t* sQ = smem + OFF_Q;
-  uint8_t* sK = smem + OFF_K;
-  uint8_t* sV = smem + OFF_V;
-  uint8_t* sP = smem + OFF_P;
-  uint64_t* bars = (uint64_t*)(smem + OFF_BAR);
-  uint64_t* kfull = bars;                  // [SK]
-  uint64_t* kempty = kfull + SK;           // [SK]
-  uint64_t* vfull = kempty + SK;           // [SV]
-  uint64_t* vempty = vfull + SV;           // [SV]
-  uint64_t* qfull = vempty + SV;           // [2]
-  uint64_t* qempty = qfull + 2;            // [2]
-  uint64_t* sfull = qempty + 2;            // [2]
-  uint64_t* sfree = sfull + 2;             // [2]  (4 softmax warps)
-  uint64_t* pfull = sfree + 2;             // [2]  (4 softmax warps)
-  uint64_t* pvdone = pfull + 2;            // [2]
-  uint64_t* ofull = pvdone + 2;            // [2]
-  uint64_t* ofree = ofull + 2;             // [2]  (4 epilogue warps)
-  uint64_t* statfull = ofree + 2;          // [2]  (4 softmax warps)
-  uint32_t* tmem_sh = (uint32_t*)(bars + N_BARS);
-  int* flag_sh = (int*)(tmem_sh + 1);
-  SoftSmem ss;
-  ss.m = (float*)(smem + OFF_M);
-  ss.alpha = (float*)(smem + OFF_ALPHA);
-  ss.thr = (float*)(smem + OFF_THR);
-  ss.nm = (float*)(smem + OFF_NM);
-  ss.stat = (float*)(smem + OFF_STAT);
-  ss.red = (float*)(smem + OFF_RED);
-  ss.flags = (int*)(smem + OFF_FLAG);
-  ss.sP = sP;
-  ss.sfull = sfull; ss.sfree = sfree; ss.pfull = pfull; ss.pvdone = pvdone; ss.ofree = ofree; ss.statfull = statfull;
-  float* merge = (float*)(smem + OFF_MERGE);
-  uint16_t* ones = (uint16_t*)(smem + OFF_ONES);
-  Unit* utab = (Unit*)(smem + OFF_UTAB);
-  int* pre = (int*)sP;                     // setup only (aliases the P^T buffers)
-  int* nsp = pre + 1028;
-
+// Unit table of CTA `cta` of `ncta` (the attention grid): per-request unit counts, exclusive prefix,
+// then the CTA's unit descriptors (whole (request, chunk, kv head) pairs, optionally key-split, or
+// stream-K pieces).  Called by all 384 threads of a block; `scratch` is >= 17 KB of shared memory.
+// Returns the number of units (same value in every thread).
+__device__ int build_units(const AttnArgs& a, int cta, int ncta, int* scratch, Unit* utab) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int H = a.kv.n_kv_heads;
   const int G = a.n_q_heads / H;
   const int rpc = NQM / G;
-
+  int* pre = scratch;
+  int* nsp = pre + 1028;
   // ---- unit table: per-request unit counts, exclusive prefix, then this CTA's unit descriptors
   const int n_ent = a.ext_mode == 2 ? 1 : a.n_req;
   int tps = max(2, a.split_tiles);
@@ -490,13 +454,183 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
     __syncthreads();
     total = pre[n_ent];
-    if (total <= UCAP * (int)gridDim.x || a.ext_mode == 2 || a.imp_only || tps >= (1 << 20)) break;
+    if (total <= UCAP * (int)ncta || a.ext_mode == 2 || a.imp_only || tps >= (1 << 20)) break;
     tps *= 2;                                      // too many units for the descriptor table
     __syncthreads();
   }
-  const int n_my = total > (int)blockIdx.x ? min(UCAP, (total - 1 - (int)blockIdx.x) / (int)gridDim.x + 1) : 0;
-  for (int k = threadIdx.x; k < n_my; k += NTHREADS)
-    utab[k] = decode_unit(a, blockIdx.x + k * gridDim.x, pre, nsp, n_ent, G, rpc);
+  int n_my = total > cta ? min(UCAP, (total - 1 - cta) / ncta + 1) : 0;
+  __shared__ int sk_on;
+  if (a.stream_k && a.ext_mode != 2 && a.imp == nullptr && !a.imp_only) {
+    // ---- stream-K over key tiles: every CTA takes T / grid_eff consecutive tiles of the flattened
+    // (request, chunk, kv head, tile) sequence; a pair cut at a CTA boundary becomes split pieces
+    // (merged by k_attn_combine in piece order)
+    __syncthreads();
+    int* pre2 = nsp + 1028;                        // [n_ent + 1] tile prefix   (P^T buffers, setup only)
+    int* ntr = pre2 + 1028;                        // [n_ent] tiles per pair
+    int* piece = ntr + 1028;                       // [UCAP][4] (request, pair_local, tile offset, tiles)
+    __shared__ int nt_minmax[2], n_pieces;
+    if (threadIdx.x == 0) { nt_minmax[0] = 1 << 30; nt_minmax[1] = 0; }
+    __syncthreads();
+    for (int i = threadIdx.x; i < n_ent; i += NTHREADS) {
+      const int rows = a.row_off[i + 1] - a.row_off[i];
+      int tiles = 0, nt = 0;
+      if (rows > 0) {
+        int kbeg, kend, s0;
+        key_range(a, i, kbeg, kend, s0);
+        nt = (kend + KT - 1) / KT - kbeg / KT;
+        tiles = ((rows + rpc - 1) / rpc) * H * nt;
+        atomicMin(&nt_minmax[0], nt);
+        atomicMax(&nt_minmax[1], nt);
+      }
+      ntr[i] = nt;
+      pre2[i + 1] = tiles;
+    }
+    __syncthreads();
+    if (warp == 0) {
+      const int per = (n_ent + 31) / 32;
+      const int b0 = min(n_ent, lane * per), b1 = min(n_ent, b0 + per);
+      int loc = 0;
+      for (int i = b0; i < b1; ++i) loc += pre2[i + 1];
+      int inc = loc;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += v;
+      }
+      int run = inc - loc;
+      for (int i = b0; i < b1; ++i) { const int c = pre2[i + 1]; pre2[i] = run; run += c; }
+      if (lane == 31) pre2[n_ent] = inc;
+    }
+    __syncthreads();
+    const long long T = pre2[n_ent];
+    const int ntmax = nt_minmax[1], ntmin = max(1, nt_minmax[0]);
+    // enough CTAs that a pair is cut into at most MAXS pieces; few enough pieces per CTA for utab
+    long long gel = T * (MAXS - 2) / max(1, ntmax);
+    if (gel < 1) gel = 1;
+    if (gel > (long long)ncta) gel = ncta;
+    if (gel > T) gel = T;
+    const int ge = (int)gel;
+    const bool fits = T > 0 && (T + ge - 1) / ge / ntmin + 2 <= UCAP;
+    if (threadIdx.x == 0) sk_on = fits ? 1 : 0;
+    if (fits && threadIdx.x == 0) {
+      int np = 0;
+      if ((int)cta < ge) {
+        const long long lo = (long long)cta * T / ge, hi = (long long)(cta + 1) * T / ge;
+        int i = 0, l = 0, h = n_ent - 1;             // request whose tiles contain lo
+        while (l < h) { const int mid = (l + h + 1) >> 1; if (pre2[mid] <= lo) l = mid; else h = mid - 1; }
+        i = l;
+        long long pos = lo;
+        while (pos < hi && np < UCAP) {
+          while (pos >= pre2[i + 1]) ++i;
+          const int nt = ntr[i];
+          const long long off = pos - pre2[i];
+          const int pl = (int)(off / nt), to = (int)(off % nt);
+          const int take = (int)min((long long)(nt - to), hi - pos);
+          piece[np * 4 + 0] = i; piece[np * 4 + 1] = pl; piece[np * 4 + 2] = to; piece[np * 4 + 3] = take;
+          ++np;
+          pos += take;
+        }
+      }
+      n_pieces = np;
+    }
+    __syncthreads();
+    if (sk_on) {
+      n_my = n_pieces;
+      for (int k = threadIdx.x; k < n_my; k += NTHREADS) {
+        const int i = piece[k * 4 + 0], pl = piece[k * 4 + 1], to = piece[k * 4 + 2], take = piece[k * 4 + 3];
+        const int nt = ntr[i];
+        Unit x;
+        x.i = i;
+        x.chunk = pl / H;
+        x.kvh = pl % H;
+        x.slot = a.req_list[i];
+        const focus_req_state& st = a.st[x.slot];
+        const int rb = a.row_off[i], re = a.row_off[i + 1];
+        x.r0 = rb + x.chunk * rpc;
+        x.nr = min(rpc, re - x.r0);
+        x.nq = x.nr * G;
+        key_range(a, i, x.kbeg, x.kend, x.s0);
+        x.t_lo = x.kbeg / KT + to;
+        x.t_hi = x.t_lo + take;
+        const long long ps = pre2[i] + (long long)pl * nt, pe = ps + nt - 1;
+        const int o0 = (int)(((ps + 1) * ge + T - 1) / T) - 1, o1 = (int)(((pe + 1) * ge + T - 1) / T) - 1;
+        x.sp = cta - o0;
+        x.nsplit = o1 - o0 + 1;
+        x.pos_base = 0;
+        x.P = st.P;
+        x.want_imp = 0;
+        x.pair = (i * a.n_chunks + x.chunk) * H + x.kvh;
+        x.pad = 0;
+        utab[k] = x;
+      }
+    }
+    __syncthreads();
+  } else if (threadIdx.x == 0) {
+    sk_on = 0;
+  }
+  __syncthreads();
+  if (!sk_on)
+    for (int k = threadIdx.x; k < n_my; k += NTHREADS)
+      utab[k] = decode_unit(a, cta + k * ncta, pre, nsp, n_ent, G, rpc);
+  __syncthreads();
+  return n_my;
+}
+
+template <bool IMP_ONLY>
+__global__ void __launch_bounds__(NTHREADS, 1)
+    k_attn_tc(const __grid_constant__ CUtensorMap mapK, const __grid_constant__ CUtensorMap mapV,
+              const __grid_constant__ CUtensorMap mapQ, AttnArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sQ = smem + OFF_Q;
+  uint8_t* sK = smem + OFF_K;
+  uint8_t* sV = smem + OFF_V;
+  uint8_t* sP = smem + OFF_P;
+  uint64_t* bars = (uint64_t*)(smem + OFF_BAR);
+  uint64_t* kfull = bars;                  // [SK]
+  uint64_t* kempty = kfull + SK;           // [SK]
+  uint64_t* vfull = kempty + SK;           // [SV]
+  uint64_t* vempty = vfull + SV;           // [SV]
+  uint64_t* qfull = vempty + SV;           // [2]
+  uint64_t* qempty = qfull + 2;            // [2]
+  uint64_t* sfull = qempty + 2;            // [2]
+  uint64_t* sfree = sfull + 2;             // [2]  (4 softmax warps)
+  uint64_t* pfull = sfree + 2;             // [2]  (4 softmax warps)
+  uint64_t* pvdone = pfull + 2;            // [2]
+  uint64_t* ofull = pvdone + 2;            // [2]
+  uint64_t* ofree = ofull + 2;             // [2]  (4 epilogue warps)
+  uint64_t* statfull = ofree + 2;          // [2]  (4 softmax warps)
+  uint32_t* tmem_sh = (uint32_t*)(bars + N_BARS);
+  SoftSmem ss;
+  ss.m = (float*)(smem + OFF_M);
+  ss.alpha = (float*)(smem + OFF_ALPHA);
+  ss.thr = (float*)(smem + OFF_THR);
+  ss.nm = (float*)(smem + OFF_NM);
+  ss.stat = (float*)(smem + OFF_STAT);
+  ss.red = (float*)(smem + OFF_RED);
+  ss.flags = (int*)(smem + OFF_FLAG);
+  ss.sP = sP;
+  ss.sfull = sfull; ss.sfree = sfree; ss.pfull = pfull; ss.pvdone = pvdone; ss.ofree = ofree; ss.statfull = statfull;
+  uint16_t* ones = (uint16_t*)(smem + OFF_ONES);
+  Unit* utab = (Unit*)(smem + OFF_UTAB);
+  int* pre = (int*)sP;                     // setup only (aliases the P^T buffers)
+  int* nsp = pre + 1028;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int H = a.kv.n_kv_heads;
+  const int G = a.n_q_heads / H;
+  const int rpc = NQM / G;
+
+  __shared__ int n_my_sh;
+  int n_my;
+  if (a.plan_n) {                                  // precomputed once per step by k_attn_plan
+    if (threadIdx.x == 0) n_my_sh = a.plan_n[blockIdx.x];
+    __syncthreads();
+    n_my = n_my_sh;
+    for (int k = threadIdx.x; k < n_my; k += NTHREADS)
+      utab[k] = static_cast<const Unit*>(a.plan_units)[(size_t)blockIdx.x * UCAP + k];
+  } else {
+    n_my = build_units(a, blockIdx.x, gridDim.x, pre, utab);
+  }
   if (threadIdx.x < 64) ones[threadIdx.x] = 0x3F80;   // bf16 1.0
   if (threadIdx.x == 0) {
     for (int i = 0; i < SK; ++i) { mbar_init(&kfull[i], 1); mbar_init(&kempty[i], 1); }
@@ -708,6 +842,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       mbar_wait(&statfull[ob], (it >> 1) & 1);
       tr.ev(1);
       tc_fence_after();
+      if (d == 0 && xr.sp == 0 && a.pair_nsplit) a.pair_nsplit[xr.pair] = xr.nsplit;
       if (xr.nsplit == 1) {
         // O / l straight to the bf16 output rows, 16 query rows at a time
 #pragma unroll 1
@@ -731,7 +866,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         if (lane == 0) mbar_arrive(&ofree[ob]);
         tr.ev(2);
       } else {
-        // split partial -> workspace; the last-arriving split merges all partials in split order
+        // split partial (unnormalised O^T rows, running max, row sum) -> workspace; k_attn_combine
+        // merges the splits in split order after the kernel
         const size_t slot_floats = (size_t)NQM * DH + 2 * NQM;
         float* base = a.part + (size_t)xr.pair * a.max_nsplit * slot_floats;
         float* po = base + (size_t)xr.sp * slot_floats;
@@ -753,39 +889,6 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&ofree[ob]);
-        __threadfence();
-        named_bar(2, 128);
-        if (d == 0) *flag_sh = atomicAdd(&a.sem[xr.pair], 1);
-        named_bar(2, 128);
-        const bool last = *flag_sh == xr.nsplit - 1;
-        if (last) {
-          __threadfence();
-          // per-row split scales f_s = 2^(m_s - m) / sum_s' l_s' 2^(m_s' - m), in split order
-          if (d < nq) {
-            float m = -CUDART_INF_F;
-            for (int s2 = 0; s2 < xr.nsplit; ++s2)
-              m = fmaxf(m, __ldcg(reinterpret_cast<const float2*>(base + (size_t)s2 * slot_floats + NQM * DH) + d).x);
-            float lsum = 0.f;
-            for (int s2 = 0; s2 < xr.nsplit; ++s2) {
-              const float2 ml = __ldcg(reinterpret_cast<const float2*>(base + (size_t)s2 * slot_floats + NQM * DH) + d);
-              const float f = ml.x == -CUDART_INF_F ? 0.f : ex2(ml.x - m);
-              merge[s2 * NQM + d] = f;
-              lsum += ml.y * f;
-            }
-            merge[MAXS * NQM + d] = 1.0f / lsum;
-          }
-          named_bar(2, 128);
-#pragma unroll 4
-          for (int n = 0; n < nq; ++n) {
-            float acc = 0.f;
-            for (int s2 = 0; s2 < xr.nsplit; ++s2)
-              acc += __ldcg(base + (size_t)s2 * slot_floats + n * DH + d) * merge[s2 * NQM + n];
-            const int row = xr.r0 + n / G, head = xr.kvh * G + n % G;
-            a.out[(size_t)row * a.ldo + head * DH + d] = __float2bfloat16_rn(acc * merge[MAXS * NQM + n]);
-          }
-          if (d == 0) a.sem[xr.pair] = 0;
-        }
-        named_bar(2, 128);                         // merge[] / flag reuse
       }
     }
   }
@@ -793,6 +896,69 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   if (warp == 3) {
     tc_fence_after();
     tmem_free<TMEM_COLS>(tmem);
+  }
+}
+
+// Unit table of one attention launch shape (CTA b of the attention grid = block b here), computed
+// once per step instead of in the prologue of every attention launch (34 launches share the plan of
+// layers >= 2).
+__global__ void __launch_bounds__(NTHREADS) k_attn_plan(AttnArgs a) {
+  __shared__ __align__(16) int scratch[4400];
+  __shared__ Unit ut[UCAP];
+  const int n = build_units(a, blockIdx.x, gridDim.x, scratch, ut);
+  Unit* out = static_cast<Unit*>(a.plan_units);
+  for (int k = threadIdx.x; k < n; k += NTHREADS) out[(size_t)blockIdx.x * UCAP + k] = ut[k];
+  if (threadIdx.x == 0) a.plan_n[blockIdx.x] = n;
+}
+
+// Split merge (flash-decoding style, deterministic split order): one CTA per (request, chunk, kv head)
+// pair that was split.  O = sum_s 2^(m_s - m) O_s / sum_s 2^(m_s - m) l_s.
+__global__ void __launch_bounds__(256) k_attn_combine(AttnArgs a) {
+  const int pair = blockIdx.x;
+  const int H = a.kv.n_kv_heads, G = a.n_q_heads / H, rpc = NQM / G;
+  const int i = pair / (a.n_chunks * H), chunk = (pair / H) % a.n_chunks, kvh = pair % H;
+  if (i >= a.n_req) return;
+  const int rb = a.row_off[i], re = a.row_off[i + 1];
+  const int r0 = rb + chunk * rpc, nr = min(rpc, re - r0);
+  if (nr <= 0) return;
+  const int ns = a.pair_nsplit[pair];
+  if (ns <= 1) return;
+  const int nq = nr * G;
+  __shared__ float fs[MAXS][NQM];
+  __shared__ float inv_l[NQM];
+  const size_t slot_floats = (size_t)NQM * DH + 2 * NQM;
+  const float* __restrict__ base = a.part + (size_t)pair * a.max_nsplit * slot_floats;
+  bf16* __restrict__ out = a.out;
+  if (threadIdx.x < nq) {
+    const int n = threadIdx.x;
+    float m = -CUDART_INF_F;
+    for (int s2 = 0; s2 < ns; ++s2)
+      m = fmaxf(m, __ldcg(reinterpret_cast<const float2*>(base + (size_t)s2 * slot_floats + NQM * DH) + n).x);
+    float lsum = 0.f;
+    for (int s2 = 0; s2 < ns; ++s2) {
+      const float2 ml = __ldcg(reinterpret_cast<const float2*>(base + (size_t)s2 * slot_floats + NQM * DH) + n);
+      const float f = ml.x == -CUDART_INF_F ? 0.f : ex2(ml.x - m);
+      fs[s2][n] = f;
+      lsum += ml.y * f;
+    }
+    inv_l[n] = 1.0f / lsum;
+  }
+  __syncthreads();
+  // 4 consecutive d per thread (16-B loads), rows spread over the block; loads of all splits first
+  for (int idx = threadIdx.x; idx < nq * (DH / 4); idx += blockDim.x) {
+    const int n = idx / (DH / 4), d4 = (idx % (DH / 4)) * 4;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 4
+    for (int s2 = 0; s2 < ns; ++s2) {
+      const float4 v = __ldcg(reinterpret_cast<const float4*>(base + (size_t)s2 * slot_floats + n * DH + d4));
+      const float f = fs[s2][n];
+      acc.x += v.x * f; acc.y += v.y * f; acc.z += v.z * f; acc.w += v.w * f;
+    }
+    const float il = inv_l[n];
+    const int row = r0 + n / G, head = kvh * G + n % G;
+    __nv_bfloat162* o = reinterpret_cast<__nv_bfloat162*>(out + (size_t)row * a.ldo + head * DH + d4);
+    o[0] = __floats2bfloat162_rn(acc.x * il, acc.y * il);
+    o[1] = __floats2bfloat162_rn(acc.z * il, acc.w * il);
   }
 }
 
@@ -831,17 +997,37 @@ static void launch_tc(const CUtensorMap& mk, const CUtensorMap& mv, const CUtens
   attn::k_attn_tc<IMP><<<grid, attn::NTHREADS, attn::SMEM_BYTES, s>>>(mk, mv, mq, a);
 }
 
-void launch_attention_tc(const CUtensorMap& mk, const CUtensorMap& mv, const CUtensorMap& mq, const AttnArgs& a,
-                         cudaStream_t s) {
+static int attn_grid(const AttnArgs& a) {
   const int G = a.n_q_heads / a.kv.n_kv_heads;
   const int rpc = attn::NQM / G;
   int max_units;
   if (a.ext_mode == 2) max_units = ((a.prefill_rows + rpc - 1) / rpc) * a.kv.n_kv_heads;
   else max_units = a.n_req * a.n_chunks * a.kv.n_kv_heads * (a.imp_only ? 1 : a.max_nsplit);
-  if (max_units <= 0) return;
-  const int grid = std::max(1, std::min(num_sms(), max_units));
-  if (a.imp_only) launch_tc<true>(mk, mv, mq, a, grid, s);
-  else launch_tc<false>(mk, mv, mq, a, grid, s);
+  return max_units <= 0 ? 0 : std::max(1, std::min(num_sms(), max_units));
+}
+
+int attn_tc_plan_capacity() { return attn::UCAP; }
+
+// Plan the unit table of a decode attention launch shape into a.plan_units / a.plan_n; the launches
+// that use it must have the same request list, row offsets and split settings.
+bool launch_attention_plan(const AttnArgs& a, cudaStream_t s) {
+  const int g = attn_grid(a);
+  if (g <= 0 || !a.plan_units || !a.plan_n || a.ext_mode == 2) return false;
+  attn::k_attn_plan<<<g, attn::NTHREADS, 0, s>>>(a);
+  return true;
+}
+
+void launch_attention_tc(const CUtensorMap& mk, const CUtensorMap& mv, const CUtensorMap& mq, const AttnArgs& a,
+                         cudaStream_t s) {
+  const int grid = attn_grid(a);
+  if (grid <= 0) return;
+  if (a.imp_only) {
+    launch_tc<true>(mk, mv, mq, a, grid, s);
+  } else {
+    launch_tc<false>(mk, mv, mq, a, grid, s);
+    if (a.ext_mode != 2 && a.pair_nsplit && a.may_split)   // merge the split pairs (no-op blocks otherwise)
+      attn::k_attn_combine<<<a.n_req * a.n_chunks * a.kv.n_kv_heads, 256, 0, s>>>(a);
+  }
 }
 
 }  // namespace focus

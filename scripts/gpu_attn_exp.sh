@@ -1,10 +1,11 @@
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || { tail -30 gpurun_out/build.log; exit 1; }
-timeout 300 python -m pytest tests/test_gpu_layers.py -x -q 2>&1 | tail -3
-for ST in 16 4; do
-  FOCUS_ATTN_SPLIT_TILES=$ST timeout 200 python scripts/attn_trace.py 10 > /dev/null 2>&1; echo "trace rc $?"
-  cp gpurun_out/attn_trace.npz gpurun_out/attn_trace_st$ST.npz
-  FOCUS_ATTN_SPLIT_TILES=$ST timeout 300 python bench.py --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/bench_st$ST.json 2> gpurun_out/bench.err; echo "bench rc $?"
+timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc $?"; tail -2 gpurun_out/pytest_gpu.log
+for V in plan sk noplan; do
+  unset FOCUS_ATTN_SK FOCUS_ATTN_NOPLAN
+  if [ $V = sk ]; then export FOCUS_ATTN_SK=1; fi
+  if [ $V = noplan ]; then export FOCUS_ATTN_NOPLAN=1; fi
+  timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_$V.json 2> gpurun_out/bench.err; echo "bench rc $?"
   python -c "
-import json; d=json.load(open('gpurun_out/bench_st$ST.json'))
-print('ST=$ST', d['value'], d['ms_per_step'], d['kernels']['attention'])"
+import json; d=json.load(open('gpurun_out/bench_$V.json'))
+print('$V', d['value'], d['ms_per_step'], d['kernels']['attention'])"
 done

@@ -153,3 +153,16 @@ def test_layer_stages_multicast_gemm(monkeypatch):
     """Same stage-wise parity with the opt-in 4-CTA TMA-multicast GEMM clusters (4 m-tiles of rows)."""
     monkeypatch.setenv("FOCUS_GEMM_MC", "1")
     test_layer_stages(M8B4, 16, 26, 40, (0, 1), 64)
+
+
+def test_layer_stages_stream_k_attention(monkeypatch):
+    """Stage-wise parity with the opt-in stream-K attention schedule (pairs cut at CTA boundaries,
+    merged by the combine kernel) on a long-context, multi-request case."""
+    monkeypatch.setenv("FOCUS_ATTN_SK", "1")
+    test_layer_stages(MINI128, 16, 3, 1100, (0, 1, 2), 16)
+
+
+def test_layer_stages_unplanned_attention(monkeypatch):
+    """Stage-wise parity with the attention unit table built in the kernel prologue (no plan kernel)."""
+    monkeypatch.setenv("FOCUS_ATTN_NOPLAN", "1")
+    test_layer_stages(MINI_G2, 8, 3, 2900, (0, 1, 2), 256)
