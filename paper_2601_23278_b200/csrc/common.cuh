@@ -137,6 +137,7 @@ struct AttnArgs {
   int* pair_nsplit;             // per (request, chunk, kv head): key splits of the last launch
   int stream_k;                 // 1: stream-K over key tiles (balanced CTAs; attention without importance)
   int may_split;                // 0: no key split is possible (host-known bound) -> no combine launch
+  int l2_prefetch;              // K/V tiles past the smem rings to prefetch into L2
   void* plan_units;             // unit table [grid][UCAP] precomputed by k_attn_plan, or nullptr
   int* plan_n;                  // [grid] units per CTA (nullptr: the kernel builds its table itself)
 };

@@ -671,11 +671,25 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       const size_t layer_rows = (size_t)a.kv_pages * H * ps;
       Tracer tr(a.trace, isK ? 0 : 1);
       uint32_t g = 0;
+      auto prefetch_tile = [&](const Unit& x, int t) {
+        for (int pc = 0; pc < KT / pr; ++pc) {
+          const int pos = t * KT + pc * pr;
+          const int pidx = min(pos / ps, a.kv.max_pages - 1);
+          const int page = a.kv.page_table[(size_t)x.slot * a.kv.max_pages + pidx];
+          const int row = (int)((size_t)a.layer * layer_rows + ((size_t)page * H + x.kvh) * ps + pos % ps);
+          tma_prefetch_2d(map, 0, row);
+          tma_prefetch_2d(map, 64, row);
+        }
+      };
+      const int pf = a.l2_prefetch;                // tiles past the ring to warm in L2
       for (int k = 0; k < n_my; ++k) {
         const Unit& x = utab[k];
         tr.ev(0);
+        for (int t = x.t_lo; t < min(x.t_hi, x.t_lo + NS + pf); ++t)
+          if (t >= x.t_lo + NS) prefetch_tile(x, t);
         for (int t = x.t_lo; t < x.t_hi; ++t, ++g) {
           const int slot = g % NS;
+          if (pf > 0 && t + NS + pf < x.t_hi) prefetch_tile(x, t + NS + pf);
           mbar_wait(&emptyb[slot], ((g / NS) & 1) ^ 1);
           tr.ev(1);
           mbar_expect_tx(&fullb[slot], KV_BYTES);

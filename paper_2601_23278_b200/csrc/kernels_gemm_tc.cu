@@ -284,7 +284,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int M = M_dev ? min(*M_dev, M_max) : M_max;
-  const Sched sc = make_sched<BN, CS>(M, N, K, policy);
+  const Sched sc = make_sched<BN, CS>(M, N, K, policy & 0xff);
+  const int pf = policy >> 8;                           // L2 prefetch distance in k-blocks
   constexpr uint16_t cmask = (uint16_t)((1u << CS) - 1u);
 
   if (warp == 0 && lane == 0) {
@@ -314,7 +315,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       uint32_t phase = 0;
       for (SegIter si(sc); si.valid(); si.next()) {
         const Seg& g = si.g;
+        // warm L2 with the first k-blocks of the segment beyond the smem ring
+        for (int kb = g.kb0 + STAGES; kb < min(g.kb1, g.kb0 + STAGES + pf); ++kb) {
+          tma_prefetch_2d(&mapA, kb * BK, g.mt * BM);
+          tma_prefetch_2d(&mapB, kb * BK, g.nt * BN + (CS > 1 ? sc.rank * (BN / CS) : 0));
+        }
         for (int kb = g.kb0; kb < g.kb1; ++kb) {
+          // L2 prefetch `pf` k-blocks past the ring, so the TMA loads below hit L2 instead of HBM
+          if (pf > 0 && kb + STAGES + pf < g.kb1) {
+            tma_prefetch_2d(&mapA, (kb + STAGES + pf) * BK, g.mt * BM);
+            tma_prefetch_2d(&mapB, (kb + STAGES + pf) * BK, g.nt * BN + (CS > 1 ? sc.rank * (BN / CS) : 0));
+          }
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_expect_tx(&full[stage], STAGE_BYTES);
           tma_load_2d(sA + stage * A_BYTES, &mapA, &full[stage], kb * BK, g.mt * BM);
@@ -517,11 +528,18 @@ static bool launch_bn(const bf16* A, int lda, int a_rows, const bf16* W, int N, 
   int grid = (int)std::min<long long>(num_sms(), std::max<long long>(1, w_min));
   grid = std::max(1, std::min<int>(grid, (int)std::min<size_t>(ws.sem_count, ws.bytes / (sizeof(float) * BM * BN * 2))));
   grid = std::max(CS, grid / CS * CS);
-  static int policy = -1;
-  if (policy < 0) {   // default: data-parallel tiles (measured fastest at the decode shapes)
+  static int policy0 = -1;
+  if (policy0 < 0) {   // default: data-parallel tiles (measured fastest at the decode shapes)
     const char* e = getenv("FOCUS_GEMM_SCHED");
-    policy = (e && e[0] == 's') ? 1 : (e && e[0] == 'h') ? 0 : 2;
+    policy0 = (e && e[0] == 's') ? 1 : (e && e[0] == 'h') ? 0 : 2;
   }
+  int policy = policy0;
+  static int pf = -1;
+  if (pf < 0) {
+    const char* e = getenv("FOCUS_GEMM_PF");
+    pf = e ? std::max(0, std::min(64, atoi(e))) : 0;   // measured: prefetch does not help
+  }
+  policy = (policy & 0xff) | (pf << 8);
   const GemmEpi e = epi ? *epi : GemmEpi{};
   switch (mode) {
     case GEMM_ADD: launch_k<GEMM_ADD, BN, CS>(grid, SMEM, s, ma, mb, C, ldc, N, K, M_dev, M_max, ws, policy, e); break;
