@@ -414,8 +414,8 @@ AttnArgs attn_args(focus_ctx* x, int l, const bf16* q, int ldq, int n_req, const
   a.part = x->attn_part;
   a.sem = x->attn_sem;
   a.pair_nsplit = x->attn_sem;      // reused as the per-pair split-count array
-  a.stream_k = getenv("FOCUS_ATTN_SK") ? 1 : 0;
-  a.l2_prefetch = getenv("FOCUS_ATTN_PF") ? std::max(0, atoi(getenv("FOCUS_ATTN_PF"))) : 0;      // opt-in (measured slower at C3 with the combine)
+  a.stream_k = getenv("FOCUS_ATTN_SK") ? 1 : 0;   // opt-in: measured slower at C3 (combine cost)
+  a.l2_prefetch = getenv("FOCUS_ATTN_PF") ? std::max(0, atoi(getenv("FOCUS_ATTN_PF"))) : 0;   // opt-in
   // a key split can only happen with stream-K or when a context exceeds split_tiles 128-key tiles
   a.may_split = a.stream_k || x->cfg.max_seq_len > 128 * x->split_tiles;
   a.imp_scratch = x->attn_scratch;
