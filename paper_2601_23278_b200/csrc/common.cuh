@@ -5,11 +5,36 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 #include "focus.h"
 
 typedef __nv_bfloat16 bf16;
 
 namespace focus {
+
+// ---------------------------------------------------------------- programmatic dependent launch
+// Every kernel of the step triggers its dependents at entry and waits for its predecessor (full
+// completion + memory flush) before touching data produced earlier in the stream; setup that only
+// reads launch parameters / weights (barrier init, TMEM alloc, tensor-map prefetch) runs before the
+// wait and overlaps the previous kernel's tail.  Without the launch attribute both are no-ops.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 constexpr int kMaxB = 64;          // per-request masks are uint64 (focus.h)
 constexpr int kGuGroup = 128;      // gate/up rows interleaved in groups of 128 (Wgu layout)

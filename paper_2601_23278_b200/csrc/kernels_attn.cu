@@ -17,6 +17,8 @@ namespace focus {
 
 template <int DH>
 __global__ void __launch_bounds__(128) k_attention(AttnArgs a) {
+  pdl_trigger();
+  pdl_wait();
   constexpr int QR = kAttnQRows, KT = kAttnKT;
   constexpr int DPL = DH >= 32 ? DH / 32 : 1;          // head dims per lane in the PV product
   extern __shared__ __align__(16) float smem[];
@@ -212,7 +214,7 @@ static void launch_attn_dh(const AttnArgs& a, cudaStream_t s) {
   const int rpc = QR / G;
   dim3 grid(a.ext_mode == 2 ? (a.prefill_rows + rpc - 1) / rpc : a.n_req * a.n_chunks, a.kv.n_kv_heads);
   if (grid.x == 0) return;
-  k_attention<DH><<<grid, 128, smem, s>>>(a);
+  launch_pdl(k_attention<DH>, grid, dim3(128), smem, s, a);
 }
 
 void launch_attention(const AttnArgs& a, cudaStream_t s) {

@@ -620,17 +620,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   const int G = a.n_q_heads / H;
   const int rpc = NQM / G;
 
-  __shared__ int n_my_sh;
-  int n_my;
-  if (a.plan_n) {                                  // precomputed once per step by k_attn_plan
-    if (threadIdx.x == 0) n_my_sh = a.plan_n[blockIdx.x];
-    __syncthreads();
-    n_my = n_my_sh;
-    for (int k = threadIdx.x; k < n_my; k += NTHREADS)
-      utab[k] = static_cast<const Unit*>(a.plan_units)[(size_t)blockIdx.x * UCAP + k];
-  } else {
-    n_my = build_units(a, blockIdx.x, gridDim.x, pre, utab);
-  }
+  pdl_trigger();
   if (threadIdx.x < 64) ones[threadIdx.x] = 0x3F80;   // bf16 1.0
   if (threadIdx.x == 0) {
     for (int i = 0; i < SK; ++i) { mbar_init(&kfull[i], 1); mbar_init(&kempty[i], 1); }
@@ -654,6 +644,19 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  pdl_wait();                                       // plan tables, q rows, KV pages come from earlier kernels
+  __shared__ int n_my_sh;
+  int n_my;
+  if (a.plan_n) {                                  // precomputed once per step by k_attn_plan
+    if (threadIdx.x == 0) n_my_sh = a.plan_n[blockIdx.x];
+    __syncthreads();
+    n_my = n_my_sh;
+    for (int k = threadIdx.x; k < n_my; k += NTHREADS)
+      utab[k] = static_cast<const Unit*>(a.plan_units)[(size_t)blockIdx.x * UCAP + k];
+  } else {
+    n_my = build_units(a, blockIdx.x, gridDim.x, pre, utab);
+  }
+  __syncthreads();
   if (threadIdx.x == 0 && a.trace) a.trace[((size_t)blockIdx.x * 8 + 7) * kTraceEv] = clock64();
   const uint32_t tmem = *tmem_sh;
 
@@ -917,6 +920,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 // once per step instead of in the prologue of every attention launch (34 launches share the plan of
 // layers >= 2).
 __global__ void __launch_bounds__(NTHREADS) k_attn_plan(AttnArgs a) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ __align__(16) int scratch[4400];
   __shared__ Unit ut[UCAP];
   const int n = build_units(a, blockIdx.x, gridDim.x, scratch, ut);
@@ -928,6 +933,8 @@ __global__ void __launch_bounds__(NTHREADS) k_attn_plan(AttnArgs a) {
 // Split merge (flash-decoding style, deterministic split order): one CTA per (request, chunk, kv head)
 // pair that was split.  O = sum_s 2^(m_s - m) O_s / sum_s 2^(m_s - m) l_s.
 __global__ void __launch_bounds__(256) k_attn_combine(AttnArgs a) {
+  pdl_trigger();
+  pdl_wait();
   const int pair = blockIdx.x;
   const int H = a.kv.n_kv_heads, G = a.n_q_heads / H, rpc = NQM / G;
   const int i = pair / (a.n_chunks * H), chunk = (pair / H) % a.n_chunks, kvh = pair % H;
@@ -1008,7 +1015,7 @@ static void launch_tc(const CUtensorMap& mk, const CUtensorMap& mv, const CUtens
     cudaFuncSetAttribute(attn::k_attn_tc<IMP>, cudaFuncAttributeMaxDynamicSharedMemorySize, attn::SMEM_BYTES);
     attr = true;
   }
-  attn::k_attn_tc<IMP><<<grid, attn::NTHREADS, attn::SMEM_BYTES, s>>>(mk, mv, mq, a);
+  launch_pdl(attn::k_attn_tc<IMP>, dim3(grid), dim3(attn::NTHREADS), attn::SMEM_BYTES, s, mk, mv, mq, a);
 }
 
 static int attn_grid(const AttnArgs& a) {
@@ -1027,7 +1034,7 @@ int attn_tc_plan_capacity() { return attn::UCAP; }
 bool launch_attention_plan(const AttnArgs& a, cudaStream_t s) {
   const int g = attn_grid(a);
   if (g <= 0 || !a.plan_units || !a.plan_n || a.ext_mode == 2) return false;
-  attn::k_attn_plan<<<g, attn::NTHREADS, 0, s>>>(a);
+  launch_pdl(attn::k_attn_plan, dim3(g), dim3(attn::NTHREADS), 0, s, a);
   return true;
 }
 
@@ -1040,7 +1047,7 @@ void launch_attention_tc(const CUtensorMap& mk, const CUtensorMap& mv, const CUt
   } else {
     launch_tc<false>(mk, mv, mq, a, grid, s);
     if (a.ext_mode != 2 && a.pair_nsplit && a.may_split)   // merge the split pairs (no-op blocks otherwise)
-      attn::k_attn_combine<<<a.n_req * a.n_chunks * a.kv.n_kv_heads, 256, 0, s>>>(a);
+      launch_pdl(attn::k_attn_combine, dim3(a.n_req * a.n_chunks * a.kv.n_kv_heads), dim3(256), 0, s, a);
   }
 }
 

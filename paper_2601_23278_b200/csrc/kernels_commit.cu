@@ -28,6 +28,8 @@ __device__ __forceinline__ VocabPartial vp_combine(VocabPartial a, VocabPartial 
 __global__ void __launch_bounds__(256) k_vocab_reduce(const float* __restrict__ logits, const int* __restrict__ M_dev,
                                                       int M_max, int V, int mask_id, int nch,
                                                       VocabPartial* __restrict__ part) {
+  pdl_trigger();
+  pdl_wait();
   const int r = blockIdx.x, c = blockIdx.y;
   if (r >= min(*M_dev, M_max)) return;
   const int per = ((V + nch - 1) / nch + 3) & ~3;
@@ -78,10 +80,12 @@ void launch_vocab_reduce(const float* logits, const int* M_dev, int M_max, int V
                          VocabPartial* part, cudaStream_t s) {
   if (M_max <= 0) return;
   dim3 grid(M_max, nch);
-  k_vocab_reduce<<<grid, 256, 0, s>>>(logits, M_dev, M_max, V, mask_id, nch, part);
+  launch_pdl(k_vocab_reduce, grid, dim3(256), 0, s, logits, M_dev, M_max, V, mask_id, nch, part);
 }
 
 __global__ void __launch_bounds__(1024) k_commit(CommitArgs a) {
+  pdl_trigger();
+  pdl_wait();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int B = a.B;
   const uint64_t full = full_mask(B);
@@ -193,7 +197,7 @@ __global__ void __launch_bounds__(1024) k_commit(CommitArgs a) {
 }
 
 void launch_commit(const CommitArgs& a, cudaStream_t s) {
-  k_commit<<<1, 1024, 0, s>>>(a);
+  launch_pdl(k_commit, dim3(1), dim3(1024), 0, s, a);
 }
 
 }  // namespace focus

@@ -9,6 +9,8 @@ template <int MODE>
 __global__ void __launch_bounds__(256) k_gemm_simt(const bf16* __restrict__ A, int lda, const bf16* __restrict__ W,
                                                    int N, int K, float* __restrict__ C, int ldc,
                                                    const int* __restrict__ M_dev, int M_max) {
+  pdl_trigger();
+  pdl_wait();
   const int M = M_dev ? min(*M_dev, M_max) : M_max;
   const int m0 = blockIdx.y * 128, n0 = blockIdx.x * 128;
   if (m0 >= M) return;
@@ -68,9 +70,9 @@ void launch_gemm_simt(const bf16* A, int lda, const bf16* W, int N, int K, float
   if (M_max <= 0) return;
   dim3 grid((N + 127) / 128, (M_max + 127) / 128);
   if (mode == GEMM_ADD)
-    k_gemm_simt<GEMM_ADD><<<grid, 256, 0, s>>>(A, lda, W, N, K, C, ldc, M_dev, M_max);
+    launch_pdl(k_gemm_simt<GEMM_ADD>, grid, dim3(256), 0, s, A, lda, W, N, K, C, ldc, M_dev, M_max);
   else
-    k_gemm_simt<GEMM_STORE><<<grid, 256, 0, s>>>(A, lda, W, N, K, C, ldc, M_dev, M_max);
+    launch_pdl(k_gemm_simt<GEMM_STORE>, grid, dim3(256), 0, s, A, lda, W, N, K, C, ldc, M_dev, M_max);
 }
 
 }  // namespace focus

@@ -283,8 +283,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   int* flag_sh = (int*)(tmem_base_sh + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int M = M_dev ? min(*M_dev, M_max) : M_max;
-  const Sched sc = make_sched<BN, CS>(M, N, K, policy & 0xff);
+  pdl_trigger();
   const int pf = policy >> 8;                           // L2 prefetch distance in k-blocks
   constexpr uint16_t cmask = (uint16_t)((1u << CS) - 1u);
 
@@ -307,6 +306,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (CS > 1) cluster_sync();                           // peers' barriers initialised before any multicast
   tc_fence_after();
   const uint32_t tmem = *tmem_base_sh;
+  pdl_wait();                                           // the A rows / live M come from earlier kernels
+  const int M = M_dev ? min(*M_dev, M_max) : M_max;
+  const Sched sc = make_sched<BN, CS>(M, N, K, policy & 0xff);
 
   if (warp == 0) {
     // ---------------- TMA producer
@@ -502,13 +504,15 @@ static void launch_k(int grid, int smem, cudaStream_t s, const CUtensorMap& ma, 
   cfg.blockDim = dim3(NUM_THREADS);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = CS;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
   cudaLaunchKernelEx(&cfg, k_gemm_tc<MODE, BN, CS>, ma, mb, C, ldc, N, K, M_dev, M_max, ws.ptr, ws.sem, policy, e);
 }
 

@@ -36,6 +36,8 @@ __global__ void __launch_bounds__(1024) k_step_setup(const int* __restrict__ req
                                                      focus_req_state* __restrict__ st, int B,
                                                      RowInfo* __restrict__ rowP, int* __restrict__ offP,
                                                      int* __restrict__ tokP, Counters* __restrict__ cnt) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ int scan[1024];
   __shared__ int carry;
   if (threadIdx.x == 0) carry = 0;
@@ -94,7 +96,7 @@ __global__ void __launch_bounds__(1024) k_step_setup(const int* __restrict__ req
 
 void launch_step_setup(const int* req_list, int n_req, focus_req_state* st, int B, RowInfo* rowP,
                        int* offP, int* tokP, Counters* cnt, cudaStream_t s) {
-  k_step_setup<<<1, 1024, 0, s>>>(req_list, n_req, st, B, rowP, offP, tokP, cnt);
+  launch_pdl(k_step_setup, dim3(1), dim3(1024), 0, s, req_list, n_req, st, B, rowP, offP, tokP, cnt);
 }
 
 __device__ __forceinline__ int live_rows(const int* M_dev, int M_max) {
@@ -105,6 +107,8 @@ __device__ __forceinline__ int live_rows(const int* M_dev, int M_max) {
 // x_r = E[tok_r] (fp32 residual stream).  One CTA per row, 16-byte loads.
 __global__ void k_embed(const int* __restrict__ tok, const int* __restrict__ M_dev, int M_max,
                         const bf16* __restrict__ E, int d, float* __restrict__ x) {
+  pdl_trigger();
+  pdl_wait();
   const int r = blockIdx.x;
   if (r >= live_rows(M_dev, M_max)) return;
   const bf16* src = E + (size_t)tok[r] * d;
@@ -124,7 +128,7 @@ __global__ void k_embed(const int* __restrict__ tok, const int* __restrict__ M_d
 
 void launch_embed(const int* tok, const int* M_dev, int M_max, const bf16* E, int d, float* x, cudaStream_t s) {
   if (M_max <= 0) return;
-  k_embed<<<M_max, 128, 0, s>>>(tok, M_dev, M_max, E, d, x);
+  launch_pdl(k_embed, dim3(M_max), dim3(128), 0, s, tok, M_dev, M_max, E, d, x);
 }
 
 // ------------------------------------------------------------------ RMSNorm
@@ -132,6 +136,8 @@ void launch_embed(const int* tok, const int* M_dev, int M_max, const bf16* E, in
 __global__ void k_rmsnorm(const float* __restrict__ x, const int* __restrict__ src_map,
                           const int* __restrict__ M_dev, int M_max, int d, float eps,
                           bf16* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
   const int r = blockIdx.x;
   if (r >= live_rows(M_dev, M_max)) return;
   const int src = src_map ? src_map[r] : r;
@@ -167,7 +173,7 @@ __global__ void k_rmsnorm(const float* __restrict__ x, const int* __restrict__ s
 void launch_rmsnorm(const float* x, const int* src_map, const int* M_dev, int M_max, int d, float eps,
                     bf16* out, cudaStream_t s) {
   if (M_max <= 0) return;
-  k_rmsnorm<<<M_max, 256, 0, s>>>(x, src_map, M_dev, M_max, d, eps, out);
+  launch_pdl(k_rmsnorm, dim3(M_max), dim3(256), 0, s, x, src_map, M_dev, M_max, d, eps, out);
 }
 
 // ------------------------------------------------------------------ RoPE + paged KV store
@@ -179,6 +185,8 @@ __global__ void k_rope_store(const float* __restrict__ qkv, const RowInfo* __res
                              const float* __restrict__ rcos, const float* __restrict__ rsin,
                              const focus_req_state* __restrict__ st, KVView kv, bf16* __restrict__ out,
                              Counters* cnt) {
+  pdl_trigger();
+  pdl_wait();
   const int r = blockIdx.x;
   if (r >= live_rows(M_dev, M_max)) return;
   const RowInfo ri = rows[r];
@@ -216,7 +224,7 @@ void launch_rope_store(const float* qkv_f32, const RowInfo* rows, const int* M_d
                        const float* rope_cos, const float* rope_sin, const focus_req_state* st, KVView kv,
                        bf16* qkv_out, Counters* cnt, cudaStream_t s) {
   if (M_max <= 0) return;
-  k_rope_store<<<M_max, 256, 0, s>>>(qkv_f32, rows, M_dev, M_max, n_q_heads, rope_cos, rope_sin, st, kv,
+  launch_pdl(k_rope_store, dim3(M_max), dim3(256), 0, s, qkv_f32, rows, M_dev, M_max, n_q_heads, rope_cos, rope_sin, st, kv,
                                      qkv_out, cnt);
 }
 
@@ -224,6 +232,8 @@ void launch_rope_store(const float* qkv_f32, const RowInfo* rows, const int* M_d
 // act[r][f] = bf16( silu(g) * u ), g/u read from the interleaved gate|up GEMM output.
 __global__ void k_silu_mul(const float* __restrict__ gu, const int* __restrict__ M_dev, int M_max, int d_ff,
                            bf16* __restrict__ act) {
+  pdl_trigger();
+  pdl_wait();
   const int r = blockIdx.x;
   if (r >= live_rows(M_dev, M_max)) return;
   const float* in = gu + (size_t)r * 2 * d_ff;
@@ -236,7 +246,7 @@ __global__ void k_silu_mul(const float* __restrict__ gu, const int* __restrict__
 
 void launch_silu_mul(const float* gu, const int* M_dev, int M_max, int d_ff, bf16* act, cudaStream_t s) {
   if (M_max <= 0) return;
-  k_silu_mul<<<M_max, 256, 0, s>>>(gu, M_dev, M_max, d_ff, act);
+  launch_pdl(k_silu_mul, dim3(M_max), dim3(256), 0, s, gu, M_dev, M_max, d_ff, act);
 }
 
 // ------------------------------------------------------------------ compaction gather
@@ -245,6 +255,8 @@ void launch_silu_mul(const float* gu, const int* M_dev, int M_max, int d_ff, bf1
 __global__ void k_gather_rows(const float* __restrict__ x, const bf16* __restrict__ qkv, int qkv_dim, int q_dim,
                               const int* __restrict__ src, const int* __restrict__ M_dev, int M_max, int d,
                               float* __restrict__ x_out, bf16* __restrict__ q_out) {
+  pdl_trigger();
+  pdl_wait();
   const int r = blockIdx.x;
   if (r >= live_rows(M_dev, M_max)) return;
   const int sr = src[r];
@@ -261,7 +273,7 @@ __global__ void k_gather_rows(const float* __restrict__ x, const bf16* __restric
 void launch_gather_rows(const float* x, const bf16* qkv, int qkv_dim, int q_dim, const int* src, const int* M_dev,
                         int M_max, int d, float* x_out, bf16* q_out, cudaStream_t s) {
   if (M_max <= 0) return;
-  k_gather_rows<<<M_max, 256, 0, s>>>(x, qkv, qkv_dim, q_dim, src, M_dev, M_max, d, x_out, q_out);
+  launch_pdl(k_gather_rows, dim3(M_max), dim3(256), 0, s, x, qkv, qkv_dim, q_dim, src, M_dev, M_max, d, x_out, q_out);
 }
 
 }  // namespace focus

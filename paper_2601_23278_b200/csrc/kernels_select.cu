@@ -12,6 +12,8 @@
 namespace focus {
 
 __global__ void __launch_bounds__(1024) k_select_plan(SelectArgs a) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ float dl[32][kMaxB];
   __shared__ int nS_sh[1024], nL_sh[1024];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -192,7 +194,7 @@ __global__ void __launch_bounds__(1024) k_select_plan(SelectArgs a) {
 }
 
 void launch_select_plan(const SelectArgs& a, cudaStream_t s) {
-  k_select_plan<<<1, 1024, 0, s>>>(a);
+  launch_pdl(k_select_plan, dim3(1), dim3(1024), 0, s, a);
 }
 
 }  // namespace focus

@@ -1,5 +1,6 @@
 // Host helpers of the tensor-core kernels: TMA descriptor encoding through the runtime's driver
 // entry point (no link-time dependency on libcuda) and the SM count of the current device.
+#include <cstdlib>
 #include <mutex>
 
 #include "tc_ptx.cuh"
@@ -53,6 +54,15 @@ bool make_tma_3d_bf16(const void* ptr, uint64_t d0, uint64_t d1, uint64_t d2, ui
   return enc(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), gdim, gstride, box, estr,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+bool pdl_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("FOCUS_PDL");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
 }
 
 int num_sms() {
