@@ -73,6 +73,22 @@ def all_gather_stats(stats: Sequence[int], device=None) -> list:
     return [o.tolist() for o in out]
 
 
+def gather_outputs(local: dict, device=None) -> dict:
+    """Gather {global request id: committed token ids} from every rank (all ranks receive the union).
+    Requests are independent, so the union is identical for any world size."""
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()):
+        return dict(local)
+    parts = [None] * dist.get_world_size()
+    dist.all_gather_object(parts, {int(k): list(map(int, v)) for k, v in local.items()})
+    out = {}
+    for p in parts:
+        for k, v in p.items():
+            assert k not in out, f"request {k} owned by two ranks"
+            out[k] = v
+    return out
+
+
 def barrier(device=None):
     import torch.distributed as dist
     if dist.is_available() and dist.is_initialized():
