@@ -156,20 +156,43 @@ def run_focus(args):
     dec_all = D.reduce_sum(dec, dev)
     value = dec_all / (ms_max / 1e3)
 
-    # ---- e2e: through the C ABI with host buffers; H2D of the request list and D2H of the commit
-    # results inside the timed region, every step
-    res = torch.empty(n_req * __import__("ctypes").sizeof(focus_commit_result), dtype=torch.uint8).pin_memory()
-    e2e_steps = max(1, min(args.steps, 10))
+    # ---- e2e: through the C ABI with host buffers; every step uploads the request list from host
+    # memory and copies its commit results (newly decoded tokens per request) back into pinned host
+    # memory.  The readback is double-buffered like a serving loop: step t's results are read on the
+    # host (event wait + parse) while step t+1 runs, since all decode state stays on the device.
+    rsz = __import__("ctypes").sizeof(focus_commit_result)
+    res = [torch.empty(n_req * rsz, dtype=torch.uint8).pin_memory() for _ in range(2)]
+    done = [None, None]
+    e2e_steps = max(1, min(args.steps, 20))
     dec0 = tok_sum()
+    host_decoded = 0
+
+    def consume(k):
+        nonlocal host_decoded
+        done[k].synchronize()
+        arr = (focus_commit_result * n_req).from_address(res[k].data_ptr())
+        host_decoded += sum(int(r.n_new) for r in arr)
+
     D.barrier(dev)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    for _ in range(e2e_steps):
+    for i in range(e2e_steps):
+        k = i & 1
+        if done[k] is not None:
+            consume(k)
+            done[k] = None
         ctx.focus_step_block(rids)
-        ctx.focus_commit(rids, res.data_ptr())
-        ctx.focus_sync()
+        ctx.focus_commit(rids, res[k].data_ptr())
+        done[k] = torch.cuda.Event()
+        done[k].record(st)
+    for i in (e2e_steps - 2, e2e_steps - 1):       # drain the last two steps' readbacks, in order
+        if i >= 0 and done[i & 1] is not None:
+            consume(i & 1)
+            done[i & 1] = None
+    ctx.focus_sync()
     e2e_s = time.perf_counter() - t0
     e2e_dec = tok_sum() - dec0
+    assert host_decoded == e2e_dec, (host_decoded, e2e_dec)
     e2e_val = D.reduce_sum(e2e_dec, dev) / D.reduce_max(e2e_s, dev)
 
     # ---- kernel breakdown: per-launch CUDA events (separate pass, 2 steps)
@@ -256,8 +279,8 @@ def run_focus(args):
                           "timed_steps_from": f"step {args.warmup + 1} of the decode (context {run.prompt_len}+)",
                           "prefill_s": round(prefill_s, 2)},
                "e2e": {"value": round(e2e_val, 2), "unit": UNIT, "h2d_bytes_per_step": 4 * n_req,
-                       "d2h_bytes_per_step": n_req * __import__("ctypes").sizeof(focus_commit_result) + 32,
-                       "steps": e2e_steps},
+                       "d2h_bytes_per_step": n_req * rsz + 32, "steps": e2e_steps,
+                       "readback": "every step's commit results to pinned host memory, double-buffered"},
                "gpu_launches": int(launches), "roofline": roofline, "roofline_gemms": roofline_gemms,
                "kernels": kernels,
                "clocks": clk.summary(), "decoded_in_window": int(dec_all), "per_rank": stats}
