@@ -4,13 +4,16 @@
 //   GEMM_QKV_ROPE          q|k|v = bf16(RoPE(acc)) + paged KV store of k and v (head_dim 128)
 // A = activations (bf16, K-major rows), W = weights (bf16, [N][K] row-major = K-major).
 //
-// Persistent, warp-specialised (one CTA per SM, 256 threads):
+// Default path: k_gemm_pair (below), CTA pairs on 256-row tiles with tcgen05.mma.cta_group::2.
+// k_gemm_tc is the one-CTA-per-tile variant (FOCUS_GEMM_PAIR=0, and the stream-K / multicast
+// experiments).  Persistent, warp-specialised (one CTA per SM, 256 threads):
 //   warp 0      TMA producer: A tile 128 x 64 and W tile 256 x 64 per stage (128B swizzle), 4 stages
 //   warp 1      MMA issuer: one elected thread issues tcgen05.mma.cta_group::1.kind::f16
 //               (M=128, N=256, K=16) x 4 per stage into a TMEM accumulator; tcgen05.commit releases
 //               the smem stage and, after the last k-block, signals the epilogue
 //   warp 2      TMEM allocator (512 columns = two 128 x 256 fp32 accumulators, double-buffered)
-//   warps 4..7  epilogue: tcgen05.ld 32x32b -> registers -> the mode's emitter (thread = output row)
+//   warps 4..7  epilogue: tcgen05.ld 32x32b -> registers -> the mode's emitter (thread = output row),
+//               stores staged through shared memory so they leave as whole 128-B lines
 // Work units = (m tile, n tile, k split) with m fastest (CTAs sharing a weight tile run together and
 // hit L2).  M is read from device memory (ragged row counts of the FOCUS step) and the split-K factor
 // is chosen on device from the live tile count; split-K partials are reduced by the last-arriving
@@ -26,13 +29,14 @@ namespace tc {
 
 constexpr int BM = 128, BK = 64;
 constexpr int A_BYTES = BM * BK * 2;               // 16 KB
+constexpr int EPI_SMEM = 4 * 32 * 128;             // epilogue staging: 4 warps x 32 rows x 128 B
 // per tile width BN (128 or 256): W tile bytes, pipeline depth (192 KB of stages), shared memory
 template <int BN>
 struct GT {
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES = (192 * 1024) / STAGE_BYTES;
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_SMEM + 1024 /*align*/ + 256 /*barriers*/;
 };
 constexpr int NUM_THREADS = 256;
 constexpr int TMEM_COLS = 512;
@@ -149,82 +153,121 @@ struct SegIter {
 };
 
 // ---------------------------------------------------------------- epilogue emitters
+// The accumulator arrives thread = row (tcgen05.ld 32x32b).  Stores go through a per-warp 32 x 128 B
+// shared staging buffer (16-B chunks XOR-swizzled by row & 7: conflict-free both ways) and leave it
+// row-contiguous: 8 lanes per row, 4 rows per instruction, so every warp store writes whole 128-B lines
+// instead of 32 rows x 16 B.
+constexpr int EPI_BUF = 32 * 128;                       // bytes per epilogue warp
+__device__ __forceinline__ uint32_t epi_slot(uint32_t buf, int r, int j) { return buf + r * 128 + ((j ^ (r & 7)) << 4); }
+__device__ __forceinline__ uint4 f4_bits(const float* v) {
+  return make_uint4(__float_as_uint(v[0]), __float_as_uint(v[1]), __float_as_uint(v[2]), __float_as_uint(v[3]));
+}
+__device__ __forceinline__ uint32_t pack_bf2(float a, float b) {
+  const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+
 // `chunk(c0, v)` yields 32 consecutive fp32 accumulator columns [c0, c0+32) of this thread's row of the
-// tile (TMEM or merged split partials); it must be called uniformly by the whole warp.
+// tile (TMEM or merged split partials); it must be called uniformly by the whole warp.  row0 = the
+// warp's first tile row (this thread's row = row0 + lane), rows >= M are not written.
 template <int MODE, int BN, typename Chunk>
-__device__ __forceinline__ void epilogue_tile(Chunk&& chunk, int row, bool row_ok, int nt, int N, float* __restrict__ C,
-                                              int ldc, const GemmEpi& epi) {
+__device__ __forceinline__ void epilogue_tile(Chunk&& chunk, int row0, int M, int nt, int N, float* __restrict__ C,
+                                              int ldc, const GemmEpi& epi, uint32_t buf) {
+  const int lane = threadIdx.x & 31;
+  const int rr = lane >> 3, jj = lane & 7;              // read-back: row 4i + rr, 16-B chunk jj
   if constexpr (MODE == GEMM_STORE || MODE == GEMM_ADD) {
     const bool vec_ok = (ldc % 4) == 0 && (((uintptr_t)C) & 15) == 0;
 #pragma unroll 1
     for (int c0 = 0; c0 < BN; c0 += 32) {
       float v[32];
       chunk(c0, v);
-      const int n0 = nt * BN + c0;
-      if (row_ok && n0 < N) {
-        float* dst = C + (size_t)row * ldc + n0;
-        if (n0 + 32 <= N && vec_ok) {
 #pragma unroll
-          for (int i = 0; i < 32; i += 4) {
-            float4 o = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-            if (MODE == GEMM_ADD) {
-              const float4 p = *reinterpret_cast<const float4*>(dst + i);
-              o.x += p.x; o.y += p.y; o.z += p.z; o.w += p.w;
-            }
-            *reinterpret_cast<float4*>(dst + i) = o;
-          }
-        } else {
-          for (int i = 0; i < 32 && n0 + i < N; ++i) dst[i] = MODE == GEMM_ADD ? dst[i] + v[i] : v[i];
+      for (int j = 0; j < 8; ++j) sts128(epi_slot(buf, lane, j), f4_bits(v + 4 * j));
+      __syncwarp();
+      const int col = nt * BN + c0 + 4 * jj;
+      const bool col_vec = col + 4 <= N && vec_ok;
+      float4 prev[8];
+      if (MODE == GEMM_ADD) {   // all residual loads in flight before the first store
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int row = row0 + 4 * i + rr;
+          prev[i] = (row < M && col_vec) ? __ldcs(reinterpret_cast<const float4*>(C + (size_t)row * ldc + col))
+                                         : make_float4(0.f, 0.f, 0.f, 0.f);
         }
       }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int r = 4 * i + rr, row = row0 + r;
+        const uint4 x = lds128(epi_slot(buf, r, jj));
+        if (row < M && col < N) {
+          float* dst = C + (size_t)row * ldc + col;
+          float4 o = make_float4(__uint_as_float(x.x), __uint_as_float(x.y), __uint_as_float(x.z), __uint_as_float(x.w));
+          if (col_vec) {
+            if (MODE == GEMM_ADD) { o.x += prev[i].x; o.y += prev[i].y; o.z += prev[i].z; o.w += prev[i].w; }
+            *reinterpret_cast<float4*>(dst) = o;
+          } else {
+            const float e[4] = {o.x, o.y, o.z, o.w};
+            for (int t = 0; t < 4 && col + t < N; ++t) dst[t] = MODE == GEMM_ADD ? dst[t] + e[t] : e[t];
+          }
+        }
+      }
+      __syncwarp();
     }
   } else if constexpr (MODE == GEMM_SWIGLU) {
     // tile nt = gate rows [128 nt, 128 nt + 128) | up rows (W_gu interleaved by kGuGroup = BN / 2):
-    // act[row][128 nt + c] = bf16(silu(gate_c) * up_c)
+    // act[row][128 nt + c] = bf16(silu(gate_c) * up_c); two 32-column groups (64 bf16 = 128 B) per staging
     static_assert(BN == 2 * kGuGroup, "gate/up interleave must match the tile");
 #pragma unroll 1
-    for (int c0 = 0; c0 < kGuGroup; c0 += 32) {
-      float gv[32], uv[32];
-      chunk(c0, gv);
-      chunk(c0 + kGuGroup, uv);
-      if (row_ok) {
-        bf16* dst = epi.out + (size_t)row * epi.ldo + nt * kGuGroup + c0;
+    for (int c0 = 0; c0 < kGuGroup; c0 += 64) {
 #pragma unroll
-        for (int i = 0; i < 32; i += 8) {
-          uint4 pk;
-          uint32_t* w = reinterpret_cast<uint32_t*>(&pk);
+      for (int h = 0; h < 2; ++h) {
+        float gv[32], uv[32];
+        chunk(c0 + 32 * h, gv);
+        chunk(c0 + 32 * h + kGuGroup, uv);
 #pragma unroll
-          for (int e = 0; e < 8; e += 2) {
-            const float a0 = gv[i + e] / (1.0f + expf(-gv[i + e])) * uv[i + e];
-            const float a1 = gv[i + e + 1] / (1.0f + expf(-gv[i + e + 1])) * uv[i + e + 1];
-            const __nv_bfloat162 b = __floats2bfloat162_rn(a0, a1);
-            w[e / 2] = *reinterpret_cast<const uint32_t*>(&b);
+        for (int j = 0; j < 4; ++j) {
+          uint32_t w[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int i = 8 * j + 2 * e;
+            const float a0 = gv[i] / (1.0f + expf(-gv[i])) * uv[i];
+            const float a1 = gv[i + 1] / (1.0f + expf(-gv[i + 1])) * uv[i + 1];
+            w[e] = pack_bf2(a0, a1);
           }
-          *reinterpret_cast<uint4*>(dst + i) = pk;
+          sts128(epi_slot(buf, lane, 4 * h + j), make_uint4(w[0], w[1], w[2], w[3]));
         }
       }
+      __syncwarp();
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int r = 4 * i + rr, row = row0 + r;
+        const uint4 x = lds128(epi_slot(buf, r, jj));
+        if (row < M) *reinterpret_cast<uint4*>(epi.out + (size_t)row * epi.ldo + nt * kGuGroup + c0 + 8 * jj) = x;
+      }
+      __syncwarp();
     }
   } else {
-    // GEMM_QKV_ROPE (head_dim 128): the tile holds 2 heads of the fused q|k|v output.  q and k heads
+    // GEMM_QKV_ROPE (head_dim 128): the tile holds BN/128 heads of the fused q|k|v output.  q and k heads
     // are rotated (rotate-half pairs (c, c+64), angle pos * theta^(-2c/dh) from the fp64-built table),
     // rounded to bf16 and written to the qkv rows; k and v heads are also stored at the row's paged
     // KV slot (the "sparse KV fill").  Writing a committed block slot raises the invariant flag.
+    const int row = row0 + lane;
     RowInfo ri{0, -1, 0, 0};
-    if (row_ok) ri = epi.rows[row];
-    if (row_ok && ri.j >= 0 && ((epi.st[ri.slot].committed >> ri.j) & 1ull)) atomicExch(&epi.cnt->invariant, 1);
+    if (row < M) ri = epi.rows[row];
+    if (row < M && ri.j >= 0 && ((epi.st[ri.slot].committed >> ri.j) & 1ull)) atomicExch(&epi.cnt->invariant, 1);
     const int hkv = epi.kv.n_kv_heads;
 #pragma unroll 1
     for (int hh = 0; hh < BN / 128; ++hh) {
       const int head = nt * (BN / 128) + hh;              // 0..Hq-1 q, then k, then v
       const bool is_v = head >= epi.n_q_heads + hkv;
       const bool is_k = !is_v && head >= epi.n_q_heads;
+      const int kvh = head - epi.n_q_heads - (is_v ? hkv : 0);
 #pragma unroll 1
       for (int c0 = 0; c0 < 64; c0 += 32) {
         float lo[32], hi[32];
         chunk(hh * 128 + c0, lo);
         chunk(hh * 128 + c0 + 64, hi);
-        if (!row_ok) continue;
-        if (!is_v) {
+        if (!is_v && row < M) {
           const float* cr = epi.rcos + (size_t)ri.pos * 64 + c0;
           const float* sr = epi.rsin + (size_t)ri.pos * 64 + c0;
 #pragma unroll
@@ -236,29 +279,30 @@ __device__ __forceinline__ void epilogue_tile(Chunk&& chunk, int row, bool row_o
             hi[i] = y2;
           }
         }
-        uint4 plo[4], phi[4];
+        // staged row: chunks 0..3 = bf16 cols [c0, c0+32), chunks 4..7 = cols [c0+64, c0+96)
 #pragma unroll
-        for (int i = 0; i < 32; i += 2) {
-          const __nv_bfloat162 bl = __floats2bfloat162_rn(lo[i], lo[i + 1]);
-          const __nv_bfloat162 bh = __floats2bfloat162_rn(hi[i], hi[i + 1]);
-          reinterpret_cast<uint32_t*>(plo)[i / 2] = *reinterpret_cast<const uint32_t*>(&bl);
-          reinterpret_cast<uint32_t*>(phi)[i / 2] = *reinterpret_cast<const uint32_t*>(&bh);
+        for (int j = 0; j < 4; ++j) {
+          sts128(epi_slot(buf, lane, j),
+                 make_uint4(pack_bf2(lo[8 * j], lo[8 * j + 1]), pack_bf2(lo[8 * j + 2], lo[8 * j + 3]),
+                            pack_bf2(lo[8 * j + 4], lo[8 * j + 5]), pack_bf2(lo[8 * j + 6], lo[8 * j + 7])));
+          sts128(epi_slot(buf, lane, 4 + j),
+                 make_uint4(pack_bf2(hi[8 * j], hi[8 * j + 1]), pack_bf2(hi[8 * j + 2], hi[8 * j + 3]),
+                            pack_bf2(hi[8 * j + 4], hi[8 * j + 5]), pack_bf2(hi[8 * j + 6], hi[8 * j + 7])));
         }
-        bf16* dst = epi.out + (size_t)row * epi.ldo + head * 128 + c0;
+        __syncwarp();
+        const int col = c0 + (jj < 4 ? 8 * jj : 64 + 8 * (jj - 4));
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          reinterpret_cast<uint4*>(dst)[i] = plo[i];
-          reinterpret_cast<uint4*>(dst + 64)[i] = phi[i];
-        }
-        if (is_k || is_v) {
-          const int kvh = head - epi.n_q_heads - (is_v ? hkv : 0);
-          bf16* pool = (is_v ? epi.kv.V : epi.kv.K) + kv_offset(epi.kv, ri.slot, ri.pos, kvh) + c0;
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            reinterpret_cast<uint4*>(pool)[i] = plo[i];
-            reinterpret_cast<uint4*>(pool + 64)[i] = phi[i];
+        for (int i = 0; i < 8; ++i) {
+          const int r = 4 * i + rr, rw = row0 + r;
+          const uint4 x = lds128(epi_slot(buf, r, jj));
+          const int slot = __shfl_sync(0xffffffffu, ri.slot, r), pos = __shfl_sync(0xffffffffu, ri.pos, r);
+          if (rw < M) {
+            *reinterpret_cast<uint4*>(epi.out + (size_t)rw * epi.ldo + head * 128 + col) = x;
+            if (is_k || is_v)
+              *reinterpret_cast<uint4*>((is_v ? epi.kv.V : epi.kv.K) + kv_offset(epi.kv, slot, pos, kvh) + col) = x;
           }
         }
+        __syncwarp();
       }
     }
   }
@@ -274,7 +318,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* sA = smem;                                   // STAGES x A_BYTES
   uint8_t* sB = smem + STAGES * A_BYTES;                // STAGES x B_BYTES
-  uint64_t* bars = (uint64_t*)(smem + STAGES * STAGE_BYTES);
+  const uint32_t epi_buf = smem_u32(smem + STAGES * STAGE_BYTES) + (uint32_t)(((threadIdx.x >> 5) & 3) * 32 * 128);
+  uint64_t* bars = (uint64_t*)(smem + STAGES * STAGE_BYTES + EPI_SMEM);
   uint64_t* full = bars;                                // [STAGES]
   uint64_t* empty = bars + STAGES;                      // [STAGES]
   uint64_t* tfull = bars + 2 * STAGES;                  // [2]
@@ -387,7 +432,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       if (g.npieces == 1) {
         // accumulator chunks straight from TMEM (warp-collective loads)
         auto chunk = [&](int c0, float* v) { tmem_ld32(taddr + c0, v); };
-        epilogue_tile<MODE, BN>(chunk, row, row_ok, nt, N, C, ldc, epi);
+        epilogue_tile<MODE, BN>(chunk, row - lane, M, nt, N, C, ldc, epi, epi_buf);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -432,7 +477,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               v[i] = s4.x; v[i + 1] = s4.y; v[i + 2] = s4.z; v[i + 3] = s4.w;
             }
           };
-          epilogue_tile<MODE, BN>(chunk, row, row_ok, nt, N, C, ldc, epi);
+          epilogue_tile<MODE, BN>(chunk, row - lane, M, nt, N, C, ldc, epi, epi_buf);
           asm volatile("bar.sync 1, 128;" ::: "memory");
           if (et == 0) sem[g.slot] = 0;
         }
@@ -447,30 +492,192 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   }
 }
 
+// ---------------------------------------------------------------- CTA-pair variant (cta_group::2)
+// A (2,1,1) cluster computes a 256 x BN tile: CTA r stages A rows [256 mp + 128 r, +128) and W rows
+// [BN nt + BN/2 r, +BN/2) in its own shared memory (both loads complete on the leader's `full`
+// barrier), the leader's MMA thread issues tcgen05.mma.cta_group::2 (M=256, N=BN, K=16) which reads
+// both CTAs' operands, and each CTA's TMEM receives its own 128 rows x BN columns.  Per CTA and
+// k-block this moves (128 + BN/2) x 64 operand elements instead of (128 + BN) x 64 for the same MMA
+// work, i.e. a quarter less L2->SM traffic at BN = 256 and a deeper pipeline (6 stages instead of 4).
+// KA k-atoms (64 columns each) per pipeline stage: each operand of a stage is ONE 3-D TMA box
+// {64, rows, KA} (measured: a CTA's TMA throughput is set by boxes per stage more than by bytes per box,
+// so fewer, larger boxes per stage feed the tensor core faster).
+template <int BN, int KA>
+struct GP {
+  static constexpr int A_STAGE = BM * BK * 2 * KA;
+  static constexpr int B_ATOM = (BN / 2) * BK * 2;
+  static constexpr int B_STAGE = B_ATOM * KA;
+  static constexpr int STAGE_BYTES = A_STAGE + B_STAGE;
+  static constexpr int STAGES = (192 * 1024) / STAGE_BYTES;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_SMEM + 1024 + 256;
+};
+
+__device__ __forceinline__ void tma_load_3d_pair(void* dst, const CUtensorMap* map, uint32_t bar_cluster, int x, int y,
+                                                 int z) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], "
+      "[%2];" ::"r"(smem_u32(dst)),
+      "l"((uint64_t)map), "r"(bar_cluster), "r"(x), "r"(y), "r"(z)
+      : "memory");
+}
+
+// development trace (scripts/gemm_bench.cu): per CTA, 3 roles x 256 clock64 stamps (producer after each
+// empty wait, MMA after each full wait, epilogue after each tfull wait / at the end); null = off
+__device__ long long* g_gemm_trace = nullptr;
+constexpr int kGemmTraceEv = 256;
+
+template <int MODE, int BN, int KA>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    k_gemm_pair(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, float* __restrict__ C,
+                int ldc, int N, int K, const int* __restrict__ M_dev, int M_max, const GemmEpi epi) {
+  using G = GP<BN, KA>;
+  constexpr int STAGES = G::STAGES, STAGE_BYTES = G::STAGE_BYTES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * G::A_STAGE;
+  const uint32_t epi_buf = smem_u32(smem + STAGES * STAGE_BYTES) + (uint32_t)(((threadIdx.x >> 5) & 3) * 32 * 128);
+  uint64_t* bars = (uint64_t*)(smem + STAGES * STAGE_BYTES + EPI_SMEM);
+  uint64_t* full = bars;                                // [STAGES]  (leader's are the live ones)
+  uint64_t* empty = bars + STAGES;                      // [STAGES]  (both CTAs, by the leader's commit)
+  uint64_t* tfull = bars + 2 * STAGES;                  // [2]       (both CTAs, by the leader's commit)
+  uint64_t* tempty = bars + 2 * STAGES + 2;             // [2]       (leader's: 8 epilogue warps of the pair)
+  uint32_t* tmem_base_sh = (uint32_t*)(bars + 2 * STAGES + 4);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  pdl_trigger();
+  const uint32_t rank = cluster_ctarank();
+  if (warp == 0 && lane == 0) {
+    for (int i = 0; i < STAGES; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 8); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    prefetch_map(&mapA);
+    prefetch_map(&mapB);
+  }
+  if (warp == 2) {   // the same warp of both CTAs allocates the pair's TMEM (same destination offset)
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_base_sh)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_base_sh;
+  pdl_wait();
+  const int M = M_dev ? min(*M_dev, M_max) : M_max;
+  const int m_pairs = (M + 2 * BM - 1) / (2 * BM);
+  const int units = m_pairs * ((N + BN - 1) / BN);
+  const int pair = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
+  const int ks_n = K / (BK * KA);                      // pipeline stages per tile
+  long long* trace = g_gemm_trace ? g_gemm_trace + (size_t)blockIdx.x * 3 * kGemmTraceEv : nullptr;
+  int tn = 0;
+  auto stamp = [&](int role) {
+    if (trace && tn < kGemmTraceEv - 1) trace[role * kGemmTraceEv + 1 + tn++] = clock64();
+  };
+  if (trace && threadIdx.x == 0) trace[0] = clock64();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint32_t full_l = mapa_shared(smem_u32(full), 0);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = pair; u < units; u += n_pairs) {
+        const int mp = u % m_pairs, nt = u / m_pairs;
+        for (int ks = 0; ks < ks_n; ++ks) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          stamp(0);
+          if (rank == 0) mbar_expect_tx(&full[stage], 2 * STAGE_BYTES);
+          const uint32_t fb = full_l + stage * 8;
+          tma_load_3d_pair(sA + stage * G::A_STAGE, &mapA, fb, 0, mp * 2 * BM + (int)rank * BM, ks * KA);
+          tma_load_3d_pair(sB + stage * G::B_STAGE, &mapB, fb, 0, nt * BN + (int)rank * (BN / 2), ks * KA);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (rank == 0 && lane == 0) {
+      constexpr uint32_t idesc = idesc_bf16(2 * BM, BN, false, false);
+      int stage = 0, it = 0;
+      uint32_t phase = 0;
+      for (int u = pair; u < units; u += n_pairs, ++it) {
+        const int acc = it & 1;
+        mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + (uint32_t)(acc * BN);
+        for (int ks = 0; ks < ks_n; ++ks) {
+          mbar_wait(&full[stage], phase);
+          stamp(1);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sA + stage * G::A_STAGE), b0 = smem_u32(sB + stage * G::B_STAGE);
+#pragma unroll
+          for (int ka = 0; ka < KA; ++ka)
+#pragma unroll
+            for (int k = 0; k < BK / 16; ++k)
+              mma_bf16_pair(d, desc_kmajor_sw128(a0 + ka * A_BYTES + k * 32), desc_kmajor_sw128(b0 + ka * G::B_ATOM + k * 32),
+                            idesc, (ks > 0 || ka > 0 || k > 0) ? 1u : 0u);
+          mma_commit_pair(&empty[stage]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        mma_commit_pair(&tfull[acc]);
+      }
+    }
+  } else if (warp >= 4) {
+    const int q = warp - 4;
+    const uint32_t tempty_l = mapa_shared(smem_u32(tempty), 0);
+    int it = 0;
+    for (int u = pair; u < units; u += n_pairs, ++it) {
+      const int mp = u % m_pairs, nt = u / m_pairs;
+      const int acc = it & 1;
+      mbar_wait(&tfull[acc], (it >> 1) & 1);
+      if (threadIdx.x == 128) stamp(2);
+      tc_fence_after();
+      const int row = mp * 2 * BM + (int)rank * BM + q * 32 + lane;
+      const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
+      auto chunk = [&](int c0, float* v) { tmem_ld32(taddr + c0, v); };
+      epilogue_tile<MODE, BN>(chunk, row - lane, M, nt, N, C, ldc, epi, epi_buf);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(tempty_l + acc * 8);
+      if (threadIdx.x == 128) stamp(2);
+    }
+  }
+  __syncthreads();
+  cluster_sync();                                       // no CTA leaves while its peer may still signal it
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+  }
+}
+
 // ---------------------------------------------------------------------------- host side
 struct MapKey {
   const void* p;
-  int rows, cols, ld, box_rows;
+  int rows, cols, ld, box_rows, ka;
   bool operator==(const MapKey& o) const {
-    return p == o.p && rows == o.rows && cols == o.cols && ld == o.ld && box_rows == o.box_rows;
+    return p == o.p && rows == o.rows && cols == o.cols && ld == o.ld && box_rows == o.box_rows && ka == o.ka;
   }
 };
 struct MapKeyHash {
   size_t operator()(const MapKey& k) const {
     return std::hash<const void*>()(k.p) ^ ((size_t)k.rows * 1000003u) ^ ((size_t)k.cols * 7919u) ^
-           ((size_t)k.ld << 20) ^ (size_t)k.box_rows;
+           ((size_t)k.ld << 20) ^ (size_t)k.box_rows ^ ((size_t)k.ka << 40);
   }
 };
 
-bool get_map(const void* ptr, int rows, int cols, int ld, int box_rows, CUtensorMap* out) {
+// ka = 0: 2-D map [rows][cols], box box_rows x 64.  ka >= 1: 3-D view {64, rows, cols / 64} of the same
+// matrix (k-atom stride 128 B), box {64, box_rows, ka} = ka consecutive SW128 K-major tiles.
+bool get_map(const void* ptr, int rows, int cols, int ld, int box_rows, CUtensorMap* out, int ka = 0) {
   static std::mutex mu;
   static std::unordered_map<MapKey, CUtensorMap, MapKeyHash> cache;
   std::lock_guard<std::mutex> g(mu);
-  const MapKey k{ptr, rows, cols, ld, box_rows};
+  const MapKey k{ptr, rows, cols, ld, box_rows, ka};
   auto it = cache.find(k);
   if (it != cache.end()) { *out = it->second; return true; }
   CUtensorMap m;
-  if (!make_tma_2d_bf16(ptr, rows, cols, ld, BK, box_rows, &m)) return false;
+  const bool ok = ka == 0 ? make_tma_2d_bf16(ptr, rows, cols, ld, BK, box_rows, &m)
+                          : make_tma_3d_bf16(ptr, BK, rows, cols / BK, (uint64_t)ld * 2, BK * 2, BK, box_rows, ka, &m);
+  if (!ok) return false;
   cache.emplace(k, m);
   *out = m;
   return true;
@@ -489,6 +696,9 @@ int gemm_backend() {
 }
 
 void gemm_set_backend(int b) { g_backend = b; }
+
+// development hook: route the pair kernel's clock64 trace to `buf` (3 * 256 int64 per CTA) or off (null)
+void gemm_set_trace(long long* buf) { cudaMemcpyToSymbol(tc::g_gemm_trace, &buf, sizeof(buf)); }
 
 template <int MODE, int BN, int CS>
 static void launch_k(int grid, int smem, cudaStream_t s, const CUtensorMap& ma, const CUtensorMap& mb, float* C, int ldc,
@@ -559,6 +769,58 @@ static bool launch_bn(const bf16* A, int lda, int a_rows, const bf16* W, int N, 
   return true;
 }
 
+template <int MODE, int BN, int KA>
+static void launch_pair_k(int grid, cudaStream_t s, const CUtensorMap& ma, const CUtensorMap& mb, float* C, int ldc,
+                          int N, int K, const int* M_dev, int M_max, const GemmEpi& e) {
+  using namespace tc;
+  constexpr int SMEM = GP<BN, KA>::SMEM_BYTES;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_gemm_pair<MODE, BN, KA>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(NUM_THREADS);
+  cfg.dynamicSmemBytes = SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  cudaLaunchKernelEx(&cfg, k_gemm_pair<MODE, BN, KA>, ma, mb, C, ldc, N, K, M_dev, M_max, e);
+}
+
+template <int BN, int KA>
+static bool launch_pair(const bf16* A, int lda, int a_rows, const bf16* W, int N, int K, float* C, int ldc,
+                        const int* M_dev, int M_max, GemmMode mode, cudaStream_t s, const GemmEpi* epi, int m) {
+  using namespace tc;
+  if ((mode == GEMM_SWIGLU || mode == GEMM_QKV_ROPE) && (!epi || N % BN)) return false;
+  if (mode == GEMM_SWIGLU && BN != 2 * kGuGroup) return false;
+  if (mode == GEMM_QKV_ROPE && (epi->kv.head_dim != 128 || BN % 128)) return false;
+  CUtensorMap ma, mb;
+  if (K % (BK * KA)) return false;
+  if (!get_map(A, a_rows, K, lda, BM, &ma, KA) || !get_map(W, N, K, K, BN / 2, &mb, KA)) return false;
+  // one pair per unit of the expected row count, at most one CTA per SM
+  const long long units = (long long)((m + 2 * BM - 1) / (2 * BM)) * ((N + BN - 1) / BN);
+  const int grid = (int)std::max<long long>(2, std::min<long long>(num_sms() / 2, units) * 2);
+  const GemmEpi e = epi ? *epi : GemmEpi{};
+  switch (mode) {
+    case GEMM_ADD: launch_pair_k<GEMM_ADD, BN, KA>(grid, s, ma, mb, C, ldc, N, K, M_dev, M_max, e); break;
+    case GEMM_SWIGLU:
+      if constexpr (BN == 2 * kGuGroup) launch_pair_k<GEMM_SWIGLU, BN, KA>(grid, s, ma, mb, C, ldc, N, K, M_dev, M_max, e);
+      break;
+    case GEMM_QKV_ROPE: launch_pair_k<GEMM_QKV_ROPE, BN, KA>(grid, s, ma, mb, C, ldc, N, K, M_dev, M_max, e); break;
+    default: launch_pair_k<GEMM_STORE, BN, KA>(grid, s, ma, mb, C, ldc, N, K, M_dev, M_max, e);
+  }
+  return true;
+}
+
 // m_est: expected live row count (host estimate, e.g. last step's counter) used only to pick the tile
 // width: 128-wide tiles when 256-wide tiles would leave more than ~half of the SMs idle.
 bool launch_gemm_tc(const bf16* A, int lda, int a_rows, const bf16* W, int N, int K, float* C, int ldc, const int* M_dev,
@@ -572,6 +834,26 @@ bool launch_gemm_tc(const bf16* A, int lda, int a_rows, const bf16* W, int N, in
   // opt-in (FOCUS_GEMM_MC=1): clusters of 4 CTAs (the 4 m-tiles of a weight tile) share W by TMA
   // multicast when the live row count fills them.  Measured no faster at the C3 shapes (at cluster
   // size <= 4 the L2 already serves the duplicate requests once), so one CTA per tile by default.
+  static int pair_mode = -1;
+  if (pair_mode < 0) {
+    const char* e = getenv("FOCUS_GEMM_PAIR");   // CTA-pair tiles by default; FOCUS_GEMM_PAIR=0: one CTA per tile
+    pair_mode = (e && e[0] == '0') ? 0 : 1;
+  }
+  if (pair_mode) {
+    const long long units256 = (long long)((m + 2 * BM - 1) / (2 * BM)) * ((N + 255) / 256);
+    const bool narrow2 = mode != GEMM_SWIGLU && 4 * units256 <= (num_sms() * 11) / 10 && getenv("FOCUS_GEMM_BN256") == nullptr;
+    static int ka = -1;
+    if (ka < 0) {
+      const char* e = getenv("FOCUS_GEMM_KA");
+      ka = (e && e[0] == '1') ? 1 : 2;
+    }
+    if (ka == 2 && K % (2 * BK) == 0) {
+      if (narrow2) return launch_pair<128, 2>(A, lda, a_rows, W, N, K, C, ldc, M_dev, M_max, mode, s, epi, m);
+      return launch_pair<256, 2>(A, lda, a_rows, W, N, K, C, ldc, M_dev, M_max, mode, s, epi, m);
+    }
+    if (narrow2) return launch_pair<128, 1>(A, lda, a_rows, W, N, K, C, ldc, M_dev, M_max, mode, s, epi, m);
+    return launch_pair<256, 1>(A, lda, a_rows, W, N, K, C, ldc, M_dev, M_max, mode, s, epi, m);
+  }
   const int m_tiles = (m + BM - 1) / BM;
   const bool cluster4 = getenv("FOCUS_GEMM_MC") != nullptr && m_tiles % 4 == 0;
   if (narrow) {

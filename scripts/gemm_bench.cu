@@ -1,0 +1,130 @@
+// Standalone timing harness for the tcgen05 GEMM of libfocus.so (development tool, not the product
+// path): times focus::launch_gemm_tc at the C3 decode shapes with CUDA events, for the default
+// tile-shape choice and the env-switch variants.  Build + run on the GPU box:
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O2 -std=c++17 -I include scripts/gemm_bench.cu \
+//        -o /tmp/gemm_bench -Lpaper_2601_23278_b200 -lfocus -Xlinker -rpath=$PWD/paper_2601_23278_b200
+#include <cstdio>
+#include <cstdlib>
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "../paper_2601_23278_b200/csrc/common.cuh"
+
+namespace focus {
+bool launch_gemm_tc(const bf16* A, int lda, int a_rows, const bf16* W, int N, int K, float* C, int ldc,
+                    const int* M_dev, int M_max, GemmMode mode, const GemmWs& ws, cudaStream_t s, const GemmEpi* epi,
+                    int m_est);
+void gemm_set_trace(long long* buf);
+}
+
+using namespace focus;
+
+__global__ void fill(bf16* p, size_t n, uint32_t seed) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    uint32_t h = (uint32_t)(i * 2654435761u) ^ seed;
+    h ^= h >> 13;
+    p[i] = __float2bfloat16((float)((int)(h & 1023) - 512) / 4096.f);
+  }
+}
+
+// naive fp32 reference C[m][n] = sum_k A[m][k] W[n][k] for a sampled set of rows
+__global__ void ref_rows(const bf16* A, const bf16* W, float* R, int N, int K, int row_step) {
+  const int r = blockIdx.y * row_step;
+  for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < N; n += gridDim.x * blockDim.x) {
+    float acc = 0.f;
+    for (int k = 0; k < K; ++k) acc += __bfloat162float(A[(size_t)r * K + k]) * __bfloat162float(W[(size_t)n * K + k]);
+    R[(size_t)blockIdx.y * N + n] = acc;
+  }
+}
+
+int main(int argc, char** argv) {
+  const int M = argc > 1 ? atoi(argv[1]) : 428;
+  struct Shape { const char* name; int N, K; GemmMode mode; };
+  const Shape shapes[] = {{"qkv(store)", 6144, 4096, GEMM_STORE}, {"o(add)", 4096, 4096, GEMM_ADD},
+                          {"gu(store)", 24576, 4096, GEMM_STORE}, {"down(add)", 4096, 12288, GEMM_ADD},
+                          {"lm(store)", 151936, 4096, GEMM_STORE}};
+  const int max_rows = 1024;
+  bf16 *A, *W;
+  float* C;
+  int* Mdev;
+  cudaMalloc(&A, (size_t)max_rows * 12288 * 2);
+  cudaMalloc(&W, (size_t)151936 * 4096 * 2);
+  cudaMalloc(&C, (size_t)max_rows * 151936 * 4);
+  cudaMalloc(&Mdev, 4);
+  cudaMemcpy(Mdev, &M, 4, cudaMemcpyHostToDevice);
+  fill<<<1024, 256>>>(A, (size_t)max_rows * 12288, 1);
+  fill<<<4096, 256>>>(W, (size_t)151936 * 4096, 2);
+  GemmWs ws;
+  ws.bytes = (size_t)64 << 20;
+  cudaMalloc(&ws.ptr, ws.bytes);
+  ws.sem_count = 4096;
+  cudaMalloc(&ws.sem, ws.sem_count * 4);
+  cudaMemset(ws.sem, 0, ws.sem_count * 4);
+  cudaStream_t s;
+  cudaStreamCreate(&s);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  // L2 flush buffer (> 126 MB) between repetitions
+  void* flush;
+  cudaMalloc(&flush, (size_t)256 << 20);
+  printf("M=%d  (%s)\n", M, getenv("GEMM_TAG") ? getenv("GEMM_TAG") : "default");
+  long long* tr = nullptr;
+  if (getenv("GEMM_TRACE")) {   // dump the pair kernel's per-role stage stamps of the last rep of each shape
+    cudaMalloc(&tr, (size_t)148 * 3 * 256 * 8);
+    gemm_set_trace(tr);
+  }
+  for (const Shape& sh : shapes) {
+    const int lda = sh.K;
+    float best = 1e30f, tot = 0.f;
+    const int reps = 6;
+    for (int r = 0; r < reps + 1; ++r) {
+      if (!getenv("GEMM_NOFLUSH")) cudaMemsetAsync(flush, r, (size_t)256 << 20, s);
+      cudaEventRecord(e0, s);
+      if (!launch_gemm_tc(A, lda, max_rows, W, sh.N, sh.K, C, sh.N, Mdev, max_rows, sh.mode, ws, s, nullptr, M)) {
+        printf("%s: launch refused\n", sh.name);
+        break;
+      }
+      cudaEventRecord(e1, s);
+      cudaEventSynchronize(e1);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      if (r > 0) { best = ms < best ? ms : best; tot += ms; }
+    }
+    if (sh.mode == GEMM_STORE && sh.N <= 24576) {   // spot-check sampled rows against the naive kernel
+      const int step = 37, nr = (M + step - 1) / step;
+      float* R;
+      cudaMalloc(&R, (size_t)nr * sh.N * 4);
+      ref_rows<<<dim3(16, nr), 256, 0, s>>>(A, W, R, sh.N, sh.K, step);
+      std::vector<float> hr((size_t)nr * sh.N), hc(sh.N);
+      cudaMemcpyAsync(hr.data(), R, hr.size() * 4, cudaMemcpyDeviceToHost, s);
+      double maxe = 0, maxr = 0;
+      for (int i = 0; i < nr; ++i) {
+        cudaMemcpyAsync(hc.data(), C + (size_t)i * step * sh.N, sh.N * 4, cudaMemcpyDeviceToHost, s);
+        cudaStreamSynchronize(s);
+        for (int n = 0; n < sh.N; ++n) {
+          maxe = std::max(maxe, (double)fabsf(hc[n] - hr[(size_t)i * sh.N + n]));
+          maxr = std::max(maxr, (double)fabsf(hr[(size_t)i * sh.N + n]));
+        }
+      }
+      printf("  check %s: max|err| %.3e (max|ref| %.3e) %s\n", sh.name, maxe, maxr, maxe <= 1e-3 * maxr + 1e-4 ? "OK" : "MISMATCH");
+      cudaFree(R);
+    }
+    if (tr) {
+      std::vector<long long> h((size_t)148 * 3 * 256);
+      cudaMemcpy(h.data(), tr, h.size() * 8, cudaMemcpyDeviceToHost);
+      char fn[128];
+      snprintf(fn, sizeof fn, "gpurun_out/gemm_trace_M%d_%s.bin", M, sh.name);
+      FILE* f = fopen(fn, "wb");
+      if (f) { fwrite(h.data(), 8, h.size(), f); fclose(f); }
+      cudaMemset(tr, 0, h.size() * 8);
+    }
+    const double fl = 2.0 * M * sh.N * sh.K;
+    printf("%-12s N=%6d K=%5d  best %8.1f us  avg %8.1f us  %7.1f TFLOP/s  weights %6.0f GB/s\n", sh.name, sh.N, sh.K,
+           best * 1e3, tot / reps * 1e3, fl / (best * 1e-3) / 1e12, 2.0 * sh.N * sh.K / (best * 1e-3) / 1e9);
+  }
+  cudaError_t err = cudaDeviceSynchronize();
+  printf("status: %s\n", cudaGetErrorString(err));
+  return err == cudaSuccess ? 0 : 1;
+}
