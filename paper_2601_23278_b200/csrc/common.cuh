@@ -158,10 +158,9 @@ struct AttnArgs {
   float* part;                  // split partials [pair][max_nsplit][128 * head_dim + 2 * 128]
   float* imp_scratch;           // per-CTA block-score scratch [grid][128][64] (importance epilogue)
   unsigned long long* trace;    // debug: clock64 events [grid][8][kTraceEv] or nullptr
-  int* sem;                     // (unused)
-  int* pair_nsplit;             // per (request, chunk, kv head): key splits of the last launch
+  int* sem;                     // per (request, chunk, kv head): arrival count of split pieces (zeroed)
   int stream_k;                 // 1: stream-K over key tiles (balanced CTAs; attention without importance)
-  int may_split;                // 0: no key split is possible (host-known bound) -> no combine launch
+  int tail_split;               // 1: units of the last partial round are key-split across the idle CTAs
   int l2_prefetch;              // K/V tiles past the smem rings to prefetch into L2
   void* plan_units;             // unit table [grid][UCAP] precomputed by k_attn_plan, or nullptr
   int* plan_n;                  // [grid] units per CTA (nullptr: the kernel builds its table itself)

@@ -413,11 +413,9 @@ AttnArgs attn_args(focus_ctx* x, int l, const bf16* q, int ldq, int n_req, const
   a.max_nsplit = x->max_nsplit;
   a.part = x->attn_part;
   a.sem = x->attn_sem;
-  a.pair_nsplit = x->attn_sem;      // reused as the per-pair split-count array
-  a.stream_k = getenv("FOCUS_ATTN_SK") ? 1 : 0;   // opt-in: measured slower at C3 (combine cost)
+  a.stream_k = getenv("FOCUS_ATTN_SK") ? 1 : 0;   // opt-in stream-K (measured slower than the tail split)
+  a.tail_split = getenv("FOCUS_ATTN_TAIL") ? 1 : 0;   // opt-in: measured no faster at C3
   a.l2_prefetch = getenv("FOCUS_ATTN_PF") ? std::max(0, atoi(getenv("FOCUS_ATTN_PF"))) : 0;   // opt-in
-  // a key split can only happen with stream-K or when a context exceeds split_tiles 128-key tiles
-  a.may_split = a.stream_k || x->cfg.max_seq_len > 128 * x->split_tiles;
   a.imp_scratch = x->attn_scratch;
   a.trace = (l == x->trace_layer && x->cfg.debug_taps >= 0) ? x->attn_trace : nullptr;
   return a;
@@ -438,7 +436,6 @@ bool plan_attention(focus_ctx* x, AttnArgs& a, int k) {
 
 void run_attention(focus_ctx* x, const AttnArgs& a) {
   if (a.trace) cudaMemsetAsync(a.trace, 0, (size_t)num_sms() * 8 * kTraceEv * 8, x->stream);
-  if (x->attn_tc && !a.imp_only && a.ext_mode != 2 && a.may_split) ++x->launches;   // + split combine
   if (x->attn_tc) launch_attention_tc(x->mapK, x->mapV, a.q == x->qS ? x->mapQ_qs : x->mapQ_qkv, a, x->stream);
   else launch_attention(a, x->stream);
 }

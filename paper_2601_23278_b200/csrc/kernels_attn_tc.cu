@@ -463,7 +463,7 @@ __device__ int build_units(const AttnArgs& a, int cta, int ncta, int* scratch, U
   if (a.stream_k && a.ext_mode != 2 && a.imp == nullptr && !a.imp_only) {
     // ---- stream-K over key tiles: every CTA takes T / grid_eff consecutive tiles of the flattened
     // (request, chunk, kv head, tile) sequence; a pair cut at a CTA boundary becomes split pieces
-    // (merged by k_attn_combine in piece order)
+    // (merged in piece order by the pair's last-arriving piece)
     __syncthreads();
     int* pre2 = nsp + 1028;                        // [n_ent + 1] tile prefix   (P^T buffers, setup only)
     int* ntr = pre2 + 1028;                        // [n_ent] tiles per pair
@@ -568,9 +568,45 @@ __device__ int build_units(const AttnArgs& a, int cta, int ncta, int* scratch, U
     sk_on = 0;
   }
   __syncthreads();
-  if (!sk_on)
-    for (int k = threadIdx.x; k < n_my; k += NTHREADS)
-      utab[k] = decode_unit(a, cta + k * ncta, pre, nsp, n_ent, G, rpc);
+  if (!sk_on) {
+    // Tail split: whole units round-robin for the R = total / ncta full rounds; the U' = total % ncta
+    // units of the last, partial round are each cut into s = ncta / U' key ranges (one piece per CTA)
+    // so no CTA ends a whole unit behind the others.  Only for unsplit units of plain attention.
+    const int R = total / ncta, Ut = total - R * ncta;
+    const int s = (a.tail_split && Ut > 0 && a.ext_mode != 2 && a.imp == nullptr && !a.imp_only) ? min(MAXS, ncta / Ut) : 1;
+    if (s >= 2 && R < UCAP) {
+      // the piece runs FIRST: its pair's merge (by the last-arriving piece's epilogue warps) then
+      // overlaps the CTA's whole units instead of trailing the kernel
+      __shared__ int extra;
+      if (threadIdx.x == 0) {
+        extra = 0;
+        if (cta < Ut * s) {
+          Unit x = decode_unit(a, R * ncta + cta / s, pre, nsp, n_ent, G, rpc);
+          const int t0 = x.kbeg / KT, nt = (x.kend + KT - 1) / KT - t0;
+          const int ns = min(s, nt), sp = cta % s;
+          if (x.nsplit == 1 && sp < ns) {
+            x.sp = sp;
+            x.nsplit = ns;
+            x.t_lo = t0 + (sp * nt) / ns;
+            x.t_hi = t0 + ((sp + 1) * nt) / ns;
+            x.want_imp = 0;
+            utab[0] = x;
+            extra = 1;
+          } else if (x.nsplit > 1 && sp == 0) {        // already key-split unit: keep it whole here
+            utab[0] = x;
+            extra = 1;
+          }
+        }
+      }
+      __syncthreads();
+      for (int k = threadIdx.x; k < R; k += NTHREADS)
+        utab[extra + k] = decode_unit(a, cta + k * ncta, pre, nsp, n_ent, G, rpc);
+      n_my = R + extra;
+    } else {
+      for (int k = threadIdx.x; k < n_my; k += NTHREADS)
+        utab[k] = decode_unit(a, cta + k * ncta, pre, nsp, n_ent, G, rpc);
+    }
+  }
   __syncthreads();
   return n_my;
 }
@@ -646,6 +682,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   tc_fence_after();
   pdl_wait();                                       // plan tables, q rows, KV pages come from earlier kernels
   __shared__ int n_my_sh;
+  __shared__ int merge_flag;
   int n_my;
   if (a.plan_n) {                                  // precomputed once per step by k_attn_plan
     if (threadIdx.x == 0) n_my_sh = a.plan_n[blockIdx.x];
@@ -859,7 +896,6 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       mbar_wait(&statfull[ob], (it >> 1) & 1);
       tr.ev(1);
       tc_fence_after();
-      if (d == 0 && xr.sp == 0 && a.pair_nsplit) a.pair_nsplit[xr.pair] = xr.nsplit;
       if (xr.nsplit == 1) {
         // O / l straight to the bf16 output rows, 16 query rows at a time
 #pragma unroll 1
@@ -883,8 +919,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         if (lane == 0) mbar_arrive(&ofree[ob]);
         tr.ev(2);
       } else {
-        // split partial (unnormalised O^T rows, running max, row sum) -> workspace; k_attn_combine
-        // merges the splits in split order after the kernel
+        // split piece: partial (unnormalised O^T rows, running max, row sum) -> workspace; the
+        // last-arriving piece of the pair merges all partials in split order (flash-decoding style):
+        // O = sum_s 2^(m_s - m) O_s / sum_s 2^(m_s - m) l_s.  Every piece reads the partials back from
+        // global memory, so the arithmetic does not depend on which piece arrives last.
         const size_t slot_floats = (size_t)NQM * DH + 2 * NQM;
         float* base = a.part + (size_t)xr.pair * a.max_nsplit * slot_floats;
         float* po = base + (size_t)xr.sp * slot_floats;
@@ -906,6 +944,61 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&ofree[ob]);
+        __threadfence();
+        named_bar(2, 128);
+        if (d == 0) merge_flag = atomicAdd(&a.sem[xr.pair], 1);
+        named_bar(2, 128);
+        if (merge_flag == xr.nsplit - 1) {               // last piece: merge
+          __threadfence();
+          const int ns = xr.nsplit;
+          float* fsc = reinterpret_cast<float*>(smem + OFF_MERGE);   // [MAXS][NQM] scales, [MAXS][..] 1/l
+          if (d < nq) {
+            float2 ml[MAXS];
+#pragma unroll
+            for (int s2 = 0; s2 < MAXS; ++s2)          // all statistics loads in flight at once
+              if (s2 < ns) ml[s2] = __ldcg(reinterpret_cast<const float2*>(base + (size_t)s2 * slot_floats + NQM * DH) + d);
+            float m = -CUDART_INF_F;
+#pragma unroll
+            for (int s2 = 0; s2 < MAXS; ++s2)
+              if (s2 < ns) m = fmaxf(m, ml[s2].x);
+            float lsum = 0.f;
+#pragma unroll
+            for (int s2 = 0; s2 < MAXS; ++s2)
+              if (s2 < ns) {
+                const float f = ml[s2].x == -CUDART_INF_F ? 0.f : ex2(ml[s2].x - m);
+                fsc[s2 * NQM + d] = f;
+                lsum += ml[s2].y * f;
+              }
+            fsc[MAXS * NQM + d] = 1.0f / lsum;
+          }
+          named_bar(2, 128);
+#pragma unroll 1
+          for (int n0 = 0; n0 < nq; n0 += 16) {
+            float acc[16];
+#pragma unroll
+            for (int e = 0; e < 16; ++e) acc[e] = 0.f;
+#pragma unroll 2
+            for (int s2 = 0; s2 < ns; ++s2) {
+              const float* ps = base + (size_t)s2 * slot_floats + d;
+              float v[16];
+#pragma unroll
+              for (int e = 0; e < 16; ++e) v[e] = n0 + e < nq ? __ldcg(ps + (n0 + e) * DH) : 0.f;
+#pragma unroll
+              for (int e = 0; e < 16; ++e) acc[e] += v[e] * fsc[s2 * NQM + n0 + e];
+            }
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+              const int n = n0 + e;
+              if (n < nq) {
+                const int row = xr.r0 + n / G, head = xr.kvh * G + n % G;
+                a.out[(size_t)row * a.ldo + head * DH + d] = __float2bfloat16_rn(acc[e] * fsc[MAXS * NQM + n]);
+              }
+            }
+          }
+          if (d == 0) a.sem[xr.pair] = 0;                 // re-arm for the next launch
+          named_bar(2, 128);                             // fsc reuse by the next merge
+        }
+        tr.ev(2);
       }
     }
   }
@@ -928,59 +1021,6 @@ __global__ void __launch_bounds__(NTHREADS) k_attn_plan(AttnArgs a) {
   Unit* out = static_cast<Unit*>(a.plan_units);
   for (int k = threadIdx.x; k < n; k += NTHREADS) out[(size_t)blockIdx.x * UCAP + k] = ut[k];
   if (threadIdx.x == 0) a.plan_n[blockIdx.x] = n;
-}
-
-// Split merge (flash-decoding style, deterministic split order): one CTA per (request, chunk, kv head)
-// pair that was split.  O = sum_s 2^(m_s - m) O_s / sum_s 2^(m_s - m) l_s.
-__global__ void __launch_bounds__(256) k_attn_combine(AttnArgs a) {
-  pdl_trigger();
-  pdl_wait();
-  const int pair = blockIdx.x;
-  const int H = a.kv.n_kv_heads, G = a.n_q_heads / H, rpc = NQM / G;
-  const int i = pair / (a.n_chunks * H), chunk = (pair / H) % a.n_chunks, kvh = pair % H;
-  if (i >= a.n_req) return;
-  const int rb = a.row_off[i], re = a.row_off[i + 1];
-  const int r0 = rb + chunk * rpc, nr = min(rpc, re - r0);
-  if (nr <= 0) return;
-  const int ns = a.pair_nsplit[pair];
-  if (ns <= 1) return;
-  const int nq = nr * G;
-  __shared__ float fs[MAXS][NQM];
-  __shared__ float inv_l[NQM];
-  const size_t slot_floats = (size_t)NQM * DH + 2 * NQM;
-  const float* __restrict__ base = a.part + (size_t)pair * a.max_nsplit * slot_floats;
-  bf16* __restrict__ out = a.out;
-  if (threadIdx.x < nq) {
-    const int n = threadIdx.x;
-    float m = -CUDART_INF_F;
-    for (int s2 = 0; s2 < ns; ++s2)
-      m = fmaxf(m, __ldcg(reinterpret_cast<const float2*>(base + (size_t)s2 * slot_floats + NQM * DH) + n).x);
-    float lsum = 0.f;
-    for (int s2 = 0; s2 < ns; ++s2) {
-      const float2 ml = __ldcg(reinterpret_cast<const float2*>(base + (size_t)s2 * slot_floats + NQM * DH) + n);
-      const float f = ml.x == -CUDART_INF_F ? 0.f : ex2(ml.x - m);
-      fs[s2][n] = f;
-      lsum += ml.y * f;
-    }
-    inv_l[n] = 1.0f / lsum;
-  }
-  __syncthreads();
-  // 4 consecutive d per thread (16-B loads), rows spread over the block; loads of all splits first
-  for (int idx = threadIdx.x; idx < nq * (DH / 4); idx += blockDim.x) {
-    const int n = idx / (DH / 4), d4 = (idx % (DH / 4)) * 4;
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll 4
-    for (int s2 = 0; s2 < ns; ++s2) {
-      const float4 v = __ldcg(reinterpret_cast<const float4*>(base + (size_t)s2 * slot_floats + n * DH + d4));
-      const float f = fs[s2][n];
-      acc.x += v.x * f; acc.y += v.y * f; acc.z += v.z * f; acc.w += v.w * f;
-    }
-    const float il = inv_l[n];
-    const int row = r0 + n / G, head = kvh * G + n % G;
-    __nv_bfloat162* o = reinterpret_cast<__nv_bfloat162*>(out + (size_t)row * a.ldo + head * DH + d4);
-    o[0] = __floats2bfloat162_rn(acc.x * il, acc.y * il);
-    o[1] = __floats2bfloat162_rn(acc.z * il, acc.w * il);
-  }
 }
 
 }  // namespace attn
@@ -1046,8 +1086,6 @@ void launch_attention_tc(const CUtensorMap& mk, const CUtensorMap& mv, const CUt
     launch_tc<true>(mk, mv, mq, a, grid, s);
   } else {
     launch_tc<false>(mk, mv, mq, a, grid, s);
-    if (a.ext_mode != 2 && a.pair_nsplit && a.may_split)   // merge the split pairs (no-op blocks otherwise)
-      launch_pdl(attn::k_attn_combine, dim3(a.n_req * a.n_chunks * a.kv.n_kv_heads), dim3(256), 0, s, a);
   }
 }
 

@@ -186,27 +186,22 @@ __device__ __forceinline__ void epilogue_tile(Chunk&& chunk, int row0, int M, in
       __syncwarp();
       const int col = nt * BN + c0 + 4 * jj;
       const bool col_vec = col + 4 <= N && vec_ok;
-      float4 prev[8];
-      if (MODE == GEMM_ADD) {   // all residual loads in flight before the first store
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int row = row0 + 4 * i + rr;
-          prev[i] = (row < M && col_vec) ? __ldcs(reinterpret_cast<const float4*>(C + (size_t)row * ldc + col))
-                                         : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-      }
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const int r = 4 * i + rr, row = row0 + r;
         const uint4 x = lds128(epi_slot(buf, r, jj));
         if (row < M && col < N) {
           float* dst = C + (size_t)row * ldc + col;
-          float4 o = make_float4(__uint_as_float(x.x), __uint_as_float(x.y), __uint_as_float(x.z), __uint_as_float(x.w));
+          const float e[4] = {__uint_as_float(x.x), __uint_as_float(x.y), __uint_as_float(x.z), __uint_as_float(x.w)};
           if (col_vec) {
-            if (MODE == GEMM_ADD) { o.x += prev[i].x; o.y += prev[i].y; o.z += prev[i].z; o.w += prev[i].w; }
-            *reinterpret_cast<float4*>(dst) = o;
+            if (MODE == GEMM_ADD)   // residual += acc as a vector reduction at L2 (one contributor per
+                                    // element, so the result is exactly fl(x + acc)); no load round trip
+              asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "f"(e[0]), "f"(e[1]), "f"(e[2]),
+                           "f"(e[3])
+                           : "memory");
+            else
+              *reinterpret_cast<float4*>(dst) = make_float4(e[0], e[1], e[2], e[3]);
           } else {
-            const float e[4] = {o.x, o.y, o.z, o.w};
             for (int t = 0; t < 4 && col + t < N; ++t) dst[t] = MODE == GEMM_ADD ? dst[t] + e[t] : e[t];
           }
         }
@@ -268,15 +263,20 @@ __device__ __forceinline__ void epilogue_tile(Chunk&& chunk, int row0, int M, in
         chunk(hh * 128 + c0, lo);
         chunk(hh * 128 + c0 + 64, hi);
         if (!is_v && row < M) {
-          const float* cr = epi.rcos + (size_t)ri.pos * 64 + c0;
-          const float* sr = epi.rsin + (size_t)ri.pos * 64 + c0;
+          const float4* cr = reinterpret_cast<const float4*>(epi.rcos + (size_t)ri.pos * 64 + c0);
+          const float4* sr = reinterpret_cast<const float4*>(epi.rsin + (size_t)ri.pos * 64 + c0);
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const float c = cr[i], sn = sr[i];
-            const float y1 = lo[i] * c - hi[i] * sn;
-            const float y2 = hi[i] * c + lo[i] * sn;
-            lo[i] = y1;
-            hi[i] = y2;
+          for (int i4 = 0; i4 < 8; ++i4) {
+            const float4 c4 = __ldg(cr + i4), s4 = __ldg(sr + i4);
+            const float cc[4] = {c4.x, c4.y, c4.z, c4.w}, ss[4] = {s4.x, s4.y, s4.z, s4.w};
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+              const int i = 4 * i4 + t;
+              const float y1 = lo[i] * cc[t] - hi[i] * ss[t];
+              const float y2 = hi[i] * cc[t] + lo[i] * ss[t];
+              lo[i] = y1;
+              hi[i] = y2;
+            }
           }
         }
         // staged row: chunks 0..3 = bf16 cols [c0, c0+32), chunks 4..7 = cols [c0+64, c0+96)
@@ -526,10 +526,19 @@ __device__ __forceinline__ void tma_load_3d_pair(void* dst, const CUtensorMap* m
 __device__ long long* g_gemm_trace = nullptr;
 constexpr int kGemmTraceEv = 256;
 
+__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* map, int x, int y, int z) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global [%0, {%1, %2, %3}];" ::"l"((uint64_t)map), "r"(x), "r"(y), "r"(z)
+               : "memory");
+}
+
+// m_hint: expected live rows (host estimate).  Before waiting on the producing kernel (PDL), the
+// producer prefetches into L2 the weight boxes of the first stages of the unit it expects to run
+// first; weights are never written by earlier kernels, and a wrong guess only costs a wasted prefetch.
 template <int MODE, int BN, int KA>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     k_gemm_pair(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, float* __restrict__ C,
-                int ldc, int N, int K, const int* __restrict__ M_dev, int M_max, const GemmEpi epi) {
+                int ldc, int N, int K, const int* __restrict__ M_dev, int M_max, const GemmEpi epi, int m_hint,
+                float* __restrict__ ws, int* __restrict__ sem, int sk) {
   using G = GP<BN, KA>;
   constexpr int STAGES = G::STAGES, STAGE_BYTES = G::STAGE_BYTES;
   extern __shared__ uint8_t smem_raw[];
@@ -559,6 +568,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                  "r"(TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
   }
+  if (warp == 0 && lane == 0 && m_hint > 0 && !sk) {
+    const int mph = (m_hint + 2 * BM - 1) / (2 * BM);
+    const int u = blockIdx.x >> 1;
+    if (u < mph * ((N + BN - 1) / BN)) {
+      const int nt = u / mph;
+      const int pf = min(K / (BK * KA), STAGES);
+      for (int ks = 0; ks < pf; ++ks) tma_prefetch_3d(&mapB, 0, nt * BN + (int)rank * (BN / 2), ks * KA);
+    }
+  }
   tc_fence_before();
   __syncthreads();
   cluster_sync();
@@ -577,14 +595,40 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   };
   if (trace && threadIdx.x == 0) trace[0] = clock64();
 
+  // Work of this pair: data-parallel (sk = 0: whole units pair, pair + n_pairs, ...) or stream-K
+  // (sk = 1: the flattened (unit, stage) sequence cut into n_pairs equal contiguous ranges).  A unit
+  // cut by a range boundary is computed in pieces; the piece holding its first stages (run last by
+  // its pair) finalises it: it adds the later pieces' fp32 partials (run first by the following
+  // pairs, written to their CTA's workspace slot) in pair order, then runs the epilogue.  Every pair
+  // writes at most one partial (its first segment), so slot = CTA.
+  const long long W = (long long)units * ks_n;
+  const long long w_lo = sk ? (long long)pair * W / n_pairs : 0, w_hi = sk ? (long long)(pair + 1) * W / n_pairs : 0;
+  auto owner = [&](long long x) { return (int)(((x + 1) * n_pairs + W - 1) / W) - 1; };
+  auto empty_range = [&](int qq) { return (long long)qq * W / n_pairs == (long long)(qq + 1) * W / n_pairs; };
+  struct PSeg { int u, k0, k1; };
+  // segment i of this pair (valid while the returned u < units)
+  auto seg_at = [&](int i, long long& w) -> PSeg {
+    PSeg g;
+    if (!sk) { g.u = pair + i * n_pairs; g.k0 = 0; g.k1 = ks_n; return g; }
+    if (w >= w_hi) { g.u = units; g.k0 = g.k1 = 0; return g; }
+    g.u = (int)(w / ks_n);
+    g.k0 = (int)(w % ks_n);
+    g.k1 = (int)min((long long)ks_n, g.k0 + (w_hi - w));
+    w += g.k1 - g.k0;
+    return g;
+  };
+
   if (warp == 0) {
     if (lane == 0) {
       const uint32_t full_l = mapa_shared(smem_u32(full), 0);
       int stage = 0;
       uint32_t phase = 0;
-      for (int u = pair; u < units; u += n_pairs) {
-        const int mp = u % m_pairs, nt = u / m_pairs;
-        for (int ks = 0; ks < ks_n; ++ks) {
+      long long w = w_lo;
+      for (int i = 0;; ++i) {
+        const PSeg g = seg_at(i, w);
+        if (g.u >= units) break;
+        const int mp = g.u % m_pairs, nt = g.u / m_pairs;
+        for (int ks = g.k0; ks < g.k1; ++ks) {
           mbar_wait(&empty[stage], phase ^ 1);
           stamp(0);
           if (rank == 0) mbar_expect_tx(&full[stage], 2 * STAGE_BYTES);
@@ -598,14 +642,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   } else if (warp == 1) {
     if (rank == 0 && lane == 0) {
       constexpr uint32_t idesc = idesc_bf16(2 * BM, BN, false, false);
-      int stage = 0, it = 0;
+      int stage = 0;
       uint32_t phase = 0;
-      for (int u = pair; u < units; u += n_pairs, ++it) {
+      long long w = w_lo;
+      for (int it = 0;; ++it) {
+        const PSeg g = seg_at(it, w);
+        if (g.u >= units) break;
         const int acc = it & 1;
         mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d = tmem + (uint32_t)(acc * BN);
-        for (int ks = 0; ks < ks_n; ++ks) {
+        for (int ks = g.k0; ks < g.k1; ++ks) {
           mbar_wait(&full[stage], phase);
           stamp(1);
           tc_fence_after();
@@ -615,7 +662,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
             for (int k = 0; k < BK / 16; ++k)
               mma_bf16_pair(d, desc_kmajor_sw128(a0 + ka * A_BYTES + k * 32), desc_kmajor_sw128(b0 + ka * G::B_ATOM + k * 32),
-                            idesc, (ks > 0 || ka > 0 || k > 0) ? 1u : 0u);
+                            idesc, (ks > g.k0 || ka > 0 || k > 0) ? 1u : 0u);
           mma_commit_pair(&empty[stage]);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
@@ -624,21 +671,70 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
   } else if (warp >= 4) {
     const int q = warp - 4;
+    const int rl = q * 32 + lane;                        // this thread's row within the CTA's 128
     const uint32_t tempty_l = mapa_shared(smem_u32(tempty), 0);
-    int it = 0;
-    for (int u = pair; u < units; u += n_pairs, ++it) {
-      const int mp = u % m_pairs, nt = u / m_pairs;
+    float* my_part = ws + (size_t)blockIdx.x * BM * BN;  // column-major [BN][128]: coalesced by row
+    long long w = w_lo;
+    for (int it = 0;; ++it) {
+      const PSeg g = seg_at(it, w);
+      if (g.u >= units) break;
+      const int mp = g.u % m_pairs, nt = g.u / m_pairs;
       const int acc = it & 1;
       mbar_wait(&tfull[acc], (it >> 1) & 1);
       if (threadIdx.x == 128) stamp(2);
       tc_fence_after();
-      const int row = mp * 2 * BM + (int)rank * BM + q * 32 + lane;
+      const int row = mp * 2 * BM + (int)rank * BM + rl;
       const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
-      auto chunk = [&](int c0, float* v) { tmem_ld32(taddr + c0, v); };
-      epilogue_tile<MODE, BN>(chunk, row - lane, M, nt, N, C, ldc, epi, epi_buf);
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(tempty_l + acc * 8);
+      if (g.k0 > 0) {
+        // later piece of a cut unit: fp32 partial -> this CTA's slot, then flag it for the finaliser
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+          float v[32];
+          tmem_ld32(taddr + c0, v);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) __stcg(my_part + (size_t)(c0 + i) * BM + rl, v[i]);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(tempty_l + acc * 8);
+        __threadfence();
+        named_bar(1, 128);
+        if (threadIdx.x == 128) asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(sem + blockIdx.x), "r"(1) : "memory");
+      } else {
+        // whole unit, or the first piece: add the partials of the pieces that follow (pairs
+        // pair+1 .. owner(last stage of the unit), same CTA rank), in pair order
+        const int q1 = g.k1 < ks_n ? owner((long long)(g.u + 1) * ks_n - 1) : pair;
+        if (q1 > pair) {
+          if (threadIdx.x == 128)
+            for (int qq = pair + 1; qq <= q1; ++qq) {
+              if (empty_range(qq)) continue;              // (W < n_pairs: some pairs own no stage)
+              int f = 0;
+              do {
+                asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(f) : "l"(sem + 2 * qq + (int)rank) : "memory");
+              } while (f == 0);
+            }
+          named_bar(1, 128);
+        }
+        auto chunk = [&](int c0, float* v) {
+          tmem_ld32(taddr + c0, v);
+          for (int qq = pair + 1; qq <= q1; ++qq) {
+            if (empty_range(qq)) continue;
+            const float* pp = ws + (size_t)(2 * qq + (int)rank) * BM * BN + (size_t)c0 * BM + rl;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] += __ldcg(pp + (size_t)i * BM);
+          }
+        };
+        epilogue_tile<MODE, BN>(chunk, row - lane, M, nt, N, C, ldc, epi, epi_buf);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(tempty_l + acc * 8);
+        if (q1 > pair) {
+          named_bar(1, 128);                             // every thread has read the partials
+          if (threadIdx.x == 128)
+            for (int qq = pair + 1; qq <= q1; ++qq)
+              if (!empty_range(qq)) sem[2 * qq + (int)rank] = 0;   // re-arm
+        }
+      }
       if (threadIdx.x == 128) stamp(2);
     }
   }
@@ -771,7 +867,8 @@ static bool launch_bn(const bf16* A, int lda, int a_rows, const bf16* W, int N, 
 
 template <int MODE, int BN, int KA>
 static void launch_pair_k(int grid, cudaStream_t s, const CUtensorMap& ma, const CUtensorMap& mb, float* C, int ldc,
-                          int N, int K, const int* M_dev, int M_max, const GemmEpi& e) {
+                          int N, int K, const int* M_dev, int M_max, const GemmEpi& e, int m_hint, const GemmWs& ws,
+                          int sk) {
   using namespace tc;
   constexpr int SMEM = GP<BN, KA>::SMEM_BYTES;
   static bool attr = false;
@@ -793,12 +890,13 @@ static void launch_pair_k(int grid, cudaStream_t s, const CUtensorMap& ma, const
   at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = pdl_enabled() ? 2 : 1;
-  cudaLaunchKernelEx(&cfg, k_gemm_pair<MODE, BN, KA>, ma, mb, C, ldc, N, K, M_dev, M_max, e);
+  cudaLaunchKernelEx(&cfg, k_gemm_pair<MODE, BN, KA>, ma, mb, C, ldc, N, K, M_dev, M_max, e, m_hint, ws.ptr, ws.sem, sk);
 }
 
 template <int BN, int KA>
 static bool launch_pair(const bf16* A, int lda, int a_rows, const bf16* W, int N, int K, float* C, int ldc,
-                        const int* M_dev, int M_max, GemmMode mode, cudaStream_t s, const GemmEpi* epi, int m) {
+                        const int* M_dev, int M_max, GemmMode mode, const GemmWs& ws, cudaStream_t s, const GemmEpi* epi,
+                        int m) {
   using namespace tc;
   if ((mode == GEMM_SWIGLU || mode == GEMM_QKV_ROPE) && (!epi || N % BN)) return false;
   if (mode == GEMM_SWIGLU && BN != 2 * kGuGroup) return false;
@@ -806,17 +904,32 @@ static bool launch_pair(const bf16* A, int lda, int a_rows, const bf16* W, int N
   CUtensorMap ma, mb;
   if (K % (BK * KA)) return false;
   if (!get_map(A, a_rows, K, lda, BM, &ma, KA) || !get_map(W, N, K, K, BN / 2, &mb, KA)) return false;
-  // one pair per unit of the expected row count, at most one CTA per SM
+  // one pair per unit of the expected row count, at most one CTA per SM.  Stream-K (every SM busy,
+  // units cut at pair boundaries) when the units do not fill whole waves of pairs
   const long long units = (long long)((m + 2 * BM - 1) / (2 * BM)) * ((N + BN - 1) / BN);
-  const int grid = (int)std::max<long long>(2, std::min<long long>(num_sms() / 2, units) * 2);
+  const int np = num_sms() / 2;
+  // opt-in (FOCUS_GEMM_PSK=1, read per call): measured slower at the C3 shapes -- the fp32 partial
+  // write + read of the cut units costs more than the idle SMs of the ragged last wave
+  const char* sk_e = getenv("FOCUS_GEMM_PSK");
+  int sk = (sk_e && sk_e[0] == '1') ? 1 : 0;
+  if (ws.ptr == nullptr || ws.sem == nullptr || ws.sem_count < (size_t)2 * np ||
+      ws.bytes < (size_t)2 * np * BM * BN * sizeof(float))
+    sk = 0;
+  const int grid = sk ? 2 * np : (int)std::max<long long>(2, std::min<long long>(np, units) * 2);
   const GemmEpi e = epi ? *epi : GemmEpi{};
+  static int pf_on = -1;
+  if (pf_on < 0) {
+    const char* ev = getenv("FOCUS_GEMM_WPF");      // opt-in weight L2 prefetch before the PDL wait
+    pf_on = (ev && ev[0] == '1') ? 1 : 0;   // measured: no gain in the step (default off)
+  }
+  const int pf_hint = pf_on ? m : 0;
   switch (mode) {
-    case GEMM_ADD: launch_pair_k<GEMM_ADD, BN, KA>(grid, s, ma, mb, C, ldc, N, K, M_dev, M_max, e); break;
+    case GEMM_ADD: launch_pair_k<GEMM_ADD, BN, KA>(grid, s, ma, mb, C, ldc, N, K, M_dev, M_max, e, pf_hint, ws, sk); break;
     case GEMM_SWIGLU:
-      if constexpr (BN == 2 * kGuGroup) launch_pair_k<GEMM_SWIGLU, BN, KA>(grid, s, ma, mb, C, ldc, N, K, M_dev, M_max, e);
+      if constexpr (BN == 2 * kGuGroup) launch_pair_k<GEMM_SWIGLU, BN, KA>(grid, s, ma, mb, C, ldc, N, K, M_dev, M_max, e, pf_hint, ws, sk);
       break;
-    case GEMM_QKV_ROPE: launch_pair_k<GEMM_QKV_ROPE, BN, KA>(grid, s, ma, mb, C, ldc, N, K, M_dev, M_max, e); break;
-    default: launch_pair_k<GEMM_STORE, BN, KA>(grid, s, ma, mb, C, ldc, N, K, M_dev, M_max, e);
+    case GEMM_QKV_ROPE: launch_pair_k<GEMM_QKV_ROPE, BN, KA>(grid, s, ma, mb, C, ldc, N, K, M_dev, M_max, e, pf_hint, ws, sk); break;
+    default: launch_pair_k<GEMM_STORE, BN, KA>(grid, s, ma, mb, C, ldc, N, K, M_dev, M_max, e, pf_hint, ws, sk);
   }
   return true;
 }
@@ -834,25 +947,25 @@ bool launch_gemm_tc(const bf16* A, int lda, int a_rows, const bf16* W, int N, in
   // opt-in (FOCUS_GEMM_MC=1): clusters of 4 CTAs (the 4 m-tiles of a weight tile) share W by TMA
   // multicast when the live row count fills them.  Measured no faster at the C3 shapes (at cluster
   // size <= 4 the L2 already serves the duplicate requests once), so one CTA per tile by default.
-  static int pair_mode = -1;
-  if (pair_mode < 0) {
-    const char* e = getenv("FOCUS_GEMM_PAIR");   // CTA-pair tiles by default; FOCUS_GEMM_PAIR=0: one CTA per tile
-    pair_mode = (e && e[0] == '0') ? 0 : 1;
-  }
+  const char* pm_e = getenv("FOCUS_GEMM_PAIR");   // CTA-pair tiles by default; FOCUS_GEMM_PAIR=0: one CTA per tile
+  const bool pair_mode = !(pm_e && pm_e[0] == '0');
   if (pair_mode) {
     const long long units256 = (long long)((m + 2 * BM - 1) / (2 * BM)) * ((N + 255) / 256);
     const bool narrow2 = mode != GEMM_SWIGLU && 4 * units256 <= (num_sms() * 11) / 10 && getenv("FOCUS_GEMM_BN256") == nullptr;
-    static int ka = -1;
-    if (ka < 0) {
+    // k-atoms per stage (measured at the C3 shapes): 2 for 128-wide tiles (4 stages of 48 KB), 1 for
+    // 256-wide tiles (6 stages of 32 KB); FOCUS_GEMM_KA=1|2 forces one
+    static int ka_env = -1;
+    if (ka_env < 0) {
       const char* e = getenv("FOCUS_GEMM_KA");
-      ka = (e && e[0] == '1') ? 1 : 2;
+      ka_env = (e && (e[0] == '1' || e[0] == '2')) ? e[0] - '0' : 0;
     }
+    const int ka = ka_env ? ka_env : (narrow2 ? 2 : 1);
     if (ka == 2 && K % (2 * BK) == 0) {
-      if (narrow2) return launch_pair<128, 2>(A, lda, a_rows, W, N, K, C, ldc, M_dev, M_max, mode, s, epi, m);
-      return launch_pair<256, 2>(A, lda, a_rows, W, N, K, C, ldc, M_dev, M_max, mode, s, epi, m);
+      if (narrow2) return launch_pair<128, 2>(A, lda, a_rows, W, N, K, C, ldc, M_dev, M_max, mode, ws, s, epi, m);
+      return launch_pair<256, 2>(A, lda, a_rows, W, N, K, C, ldc, M_dev, M_max, mode, ws, s, epi, m);
     }
-    if (narrow2) return launch_pair<128, 1>(A, lda, a_rows, W, N, K, C, ldc, M_dev, M_max, mode, s, epi, m);
-    return launch_pair<256, 1>(A, lda, a_rows, W, N, K, C, ldc, M_dev, M_max, mode, s, epi, m);
+    if (narrow2) return launch_pair<128, 1>(A, lda, a_rows, W, N, K, C, ldc, M_dev, M_max, mode, ws, s, epi, m);
+    return launch_pair<256, 1>(A, lda, a_rows, W, N, K, C, ldc, M_dev, M_max, mode, ws, s, epi, m);
   }
   const int m_tiles = (m + BM - 1) / BM;
   const bool cluster4 = getenv("FOCUS_GEMM_MC") != nullptr && m_tiles % 4 == 0;

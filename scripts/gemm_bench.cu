@@ -41,8 +41,9 @@ __global__ void ref_rows(const bf16* A, const bf16* W, float* R, int N, int K, i
 int main(int argc, char** argv) {
   const int M = argc > 1 ? atoi(argv[1]) : 428;
   struct Shape { const char* name; int N, K; GemmMode mode; };
-  const Shape shapes[] = {{"qkv(store)", 6144, 4096, GEMM_STORE}, {"o(add)", 4096, 4096, GEMM_ADD},
-                          {"gu(store)", 24576, 4096, GEMM_STORE}, {"down(add)", 4096, 12288, GEMM_ADD},
+  const Shape shapes[] = {{"qkv(store)", 6144, 4096, GEMM_STORE}, {"qkv(rope)", 6144, 4096, GEMM_QKV_ROPE},
+                          {"o(add)", 4096, 4096, GEMM_ADD},         {"gu(store)", 24576, 4096, GEMM_STORE},
+                          {"gu(swiglu)", 24576, 4096, GEMM_SWIGLU}, {"down(add)", 4096, 12288, GEMM_ADD},
                           {"lm(store)", 151936, 4096, GEMM_STORE}};
   const int max_rows = 1024;
   bf16 *A, *W;
@@ -63,6 +64,43 @@ int main(int argc, char** argv) {
   cudaMemset(ws.sem, 0, ws.sem_count * 4);
   cudaStream_t s;
   cudaStreamCreate(&s);
+  // fused-epilogue inputs shaped like the C3 step: 64 requests, rows r -> slot r % 64, block position
+  // (r / 64) % 16, context 1024; paged KV (page 16) with 8 kv heads of 128; RoPE tables for 2048 positions
+  const int n_slots = 64, page = 16, max_pages = 128, n_kvh = 8;
+  std::vector<RowInfo> hrows(max_rows);
+  for (int r = 0; r < max_rows; ++r) hrows[r] = RowInfo{r % n_slots, (r / n_slots) % 16, 1024 + (r / n_slots) % 16, r % n_slots};
+  std::vector<int> hpt((size_t)n_slots * max_pages);
+  for (size_t i = 0; i < hpt.size(); ++i) hpt[i] = (int)i;
+  RowInfo* drows;
+  int* dpt;
+  float *rc, *rs;
+  focus_req_state* dst;
+  Counters* dcnt;
+  bf16 *kp, *vp, *eout;
+  cudaMalloc(&drows, max_rows * sizeof(RowInfo));
+  cudaMemcpy(drows, hrows.data(), max_rows * sizeof(RowInfo), cudaMemcpyHostToDevice);
+  cudaMalloc(&dpt, hpt.size() * 4);
+  cudaMemcpy(dpt, hpt.data(), hpt.size() * 4, cudaMemcpyHostToDevice);
+  cudaMalloc(&rc, 2048 * 64 * 4);
+  cudaMalloc(&rs, 2048 * 64 * 4);
+  cudaMemset(rc, 0, 2048 * 64 * 4);
+  cudaMemset(rs, 0, 2048 * 64 * 4);
+  cudaMalloc(&dst, n_slots * sizeof(focus_req_state));
+  cudaMemset(dst, 0, n_slots * sizeof(focus_req_state));
+  cudaMalloc(&dcnt, sizeof(Counters));
+  cudaMemset(dcnt, 0, sizeof(Counters));
+  const size_t pool = (size_t)n_slots * max_pages * n_kvh * page * 128;
+  cudaMalloc(&kp, pool * 2);
+  cudaMalloc(&vp, pool * 2);
+  cudaMalloc(&eout, (size_t)max_rows * 12288 * 2);
+  GemmEpi epi{};
+  epi.rows = drows;
+  epi.rcos = rc;
+  epi.rsin = rs;
+  epi.st = dst;
+  epi.cnt = dcnt;
+  epi.kv = KVView{kp, vp, dpt, max_pages, page, n_kvh, 128};
+  epi.n_q_heads = 32;
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
@@ -82,7 +120,10 @@ int main(int argc, char** argv) {
     for (int r = 0; r < reps + 1; ++r) {
       if (!getenv("GEMM_NOFLUSH")) cudaMemsetAsync(flush, r, (size_t)256 << 20, s);
       cudaEventRecord(e0, s);
-      if (!launch_gemm_tc(A, lda, max_rows, W, sh.N, sh.K, C, sh.N, Mdev, max_rows, sh.mode, ws, s, nullptr, M)) {
+      epi.out = eout;
+      epi.ldo = sh.mode == GEMM_SWIGLU ? 12288 : 6144;
+      const bool fused = sh.mode == GEMM_SWIGLU || sh.mode == GEMM_QKV_ROPE;
+      if (!launch_gemm_tc(A, lda, max_rows, W, sh.N, sh.K, C, sh.N, Mdev, max_rows, sh.mode, ws, s, fused ? &epi : nullptr, M)) {
         printf("%s: launch refused\n", sh.name);
         break;
       }

@@ -58,9 +58,13 @@ __global__ void __launch_bounds__(64, 1) k_stream(const __grid_constant__ CUtens
   if (threadIdx.x == 0) {
     int st = 0;
     uint32_t ph = 0;
+    long long tw = 0, ti = 0;
     for (int r = 0; r < reps; ++r)
       for (int kb = 0; kb < kbn; ++kb) {
+        const long long a0 = clock64();
         wait_v<WM>(&empty[st], ph ^ 1);
+        const long long a1 = clock64();
+        tw += a1 - a0;
         mbar_expect_tx(&full[st], stage_bytes);
         for (int b = 0; b < boxes; ++b)
           if (linear)
@@ -69,8 +73,10 @@ __global__ void __launch_bounds__(64, 1) k_stream(const __grid_constant__ CUtens
           else
             tma_load_2d(smem + st * stage_bytes + b * box_rows * 128, &map, &full[st], kb * 64,
                       (band * boxes + b) * box_rows);
+        ti += clock64() - a1;
         if (++st == stages) { st = 0; ph ^= 1; }
       }
+    if (blockIdx.x == 0) { cyc[1] = tw; cyc[2] = ti; }
   } else if (threadIdx.x == 32) {
     int st = 0;
     uint32_t ph = 0;
@@ -80,7 +86,7 @@ __global__ void __launch_bounds__(64, 1) k_stream(const __grid_constant__ CUtens
         mbar_arrive(&empty[st]);
         if (++st == stages) { st = 0; ph ^= 1; }
       }
-    if (blockIdx.x == 0) *cyc = clock64() - t0;
+    if (blockIdx.x == 0) cyc[0] = clock64() - t0;
   }
 }
 
@@ -109,7 +115,7 @@ int main() {
   void* flush;
   cudaMalloc(&flush, (size_t)256 << 20);
   long long* cyc;
-  cudaMalloc(&cyc, 8);
+  cudaMalloc(&cyc, 24);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
@@ -134,7 +140,7 @@ int main() {
       {1, 128, 1, 6, false, 0, 1},  {148, 128, 1, 6, false, 0, 1}, {148, 128, 2, 6, false, 0, 1},
       {1, 128, 1, 6, true, 0, 2},   {148, 128, 1, 6, true, 0, 2},  {148, 128, 2, 6, false, 0, 2},
   };
-  printf("%2s %3s %5s %5s %5s %6s %3s  %9s %9s %8s %9s\n", "wm", "lin", "ctas", "rows", "boxes", "stages", "L2", "us", "GB/s", "GB/s/SM", "cyc/stage");
+  printf("%2s %3s %5s %5s %5s %6s %3s  %9s %9s %8s %9s %8s %8s\n", "wm", "lin", "ctas", "rows", "boxes", "stages", "L2", "us", "GB/s", "GB/s/SM", "cyc/stage", "wait/st", "issue/st");
   for (const Cfg& c : cfgs) {
     CUtensorMap map;
     if (!make_tma_2d_bf16(W, rows, K, K, 64, c.box_rows, &map)) { printf("map failed\n"); return 1; }
@@ -156,11 +162,12 @@ int main() {
       cudaEventElapsedTime(&ms, e0, e1);
       best = ms < best ? ms : best;
     }
-    long long hc = 0;
-    cudaMemcpy(&hc, cyc, 8, cudaMemcpyDeviceToHost);
+    long long hcs[3] = {0, 0, 0};
+    cudaMemcpy(hcs, cyc, 24, cudaMemcpyDeviceToHost);
+    const long long hc = hcs[0];
     const double bytes = (double)c.ctas * reps * (K / 64) * stage_bytes;
-    printf("%2d %3d %5d %5d %5d %6d %3s  %9.1f %9.0f %8.1f %9.0f\n", c.wm, c.lin, c.ctas, c.box_rows, c.boxes, c.stages, c.l2 ? "yes" : "no",
-           best * 1e3, bytes / (best * 1e-3) / 1e9, bytes / (best * 1e-3) / 1e9 / c.ctas, (double)hc / (reps * (K / 64)));
+    printf("%2d %3d %5d %5d %5d %6d %3s  %9.1f %9.0f %8.1f %9.0f %8.0f %8.0f\n", c.wm, c.lin, c.ctas, c.box_rows, c.boxes, c.stages, c.l2 ? "yes" : "no",
+           best * 1e3, bytes / (best * 1e-3) / 1e9, bytes / (best * 1e-3) / 1e9 / c.ctas, (double)hc / (reps * (K / 64)), (double)hcs[1] / (reps * (K / 64)), (double)hcs[2] / (reps * (K / 64)));
   }
   {
     const size_t n = (size_t)rows * K * 2 / 16;

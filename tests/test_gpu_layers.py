@@ -150,15 +150,39 @@ def test_layer_stages(model, B, nreq, prompt, taps, page):
 
 
 def test_layer_stages_multicast_gemm(monkeypatch):
-    """Same stage-wise parity with the opt-in 4-CTA TMA-multicast GEMM clusters (4 m-tiles of rows)."""
+    """Same stage-wise parity with the opt-in 4-CTA TMA-multicast GEMM clusters (4 m-tiles of rows) of
+    the one-CTA-per-tile GEMM."""
+    monkeypatch.setenv("FOCUS_GEMM_PAIR", "0")
     monkeypatch.setenv("FOCUS_GEMM_MC", "1")
     test_layer_stages(M8B4, 16, 26, 40, (0, 1), 64)
 
 
+def test_layer_stages_single_cta_gemm(monkeypatch):
+    """Stage-wise parity with the one-CTA-per-tile tcgen05 GEMM (cta_group::1) instead of CTA pairs."""
+    monkeypatch.setenv("FOCUS_GEMM_PAIR", "0")
+    test_layer_stages(M8B4, 16, 26, 40, (0, 1), 64)
+
+
+def test_layer_stages_pair_stream_k_gemm(monkeypatch):
+    """Stage-wise parity with the opt-in stream-K schedule of the CTA-pair GEMM (units cut at pair
+    boundaries, later pieces' fp32 partials added by the first piece in pair order), including grids
+    where some pairs own no stage (tiny GEMMs)."""
+    monkeypatch.setenv("FOCUS_GEMM_PSK", "1")
+    test_layer_stages(M8B4, 16, 26, 40, (0, 1), 64)
+    test_layer_stages(MINI128, 16, 3, 1100, (0, 1, 2), 16)
+
+
 def test_layer_stages_stream_k_attention(monkeypatch):
     """Stage-wise parity with the opt-in stream-K attention schedule (pairs cut at CTA boundaries,
-    merged by the combine kernel) on a long-context, multi-request case."""
+    merged in-kernel by the last-arriving piece) on a long-context, multi-request case."""
     monkeypatch.setenv("FOCUS_ATTN_SK", "1")
+    test_layer_stages(MINI128, 16, 3, 1100, (0, 1, 2), 16)
+
+
+def test_layer_stages_tail_split(monkeypatch):
+    """Stage-wise parity with the opt-in tail split (the units of the last partial round of the attention
+    grid are cut into key ranges, one per idle CTA, merged in-kernel by the last-arriving piece)."""
+    monkeypatch.setenv("FOCUS_ATTN_TAIL", "1")
     test_layer_stages(MINI128, 16, 3, 1100, (0, 1, 2), 16)
 
 
