@@ -167,7 +167,7 @@ enum {
 /* Per-kernel-kind device time measured with CUDA events on the context stream around every launch
  * while profiling is on (for the roofline report; adds event records between launches). */
 enum {
-  FOCUS_PROF_SETUP = 0, FOCUS_PROF_EMBED, FOCUS_PROF_RMSNORM, FOCUS_PROF_GEMM_QKV, FOCUS_PROF_ROPE_STORE,
+  FOCUS_PROF_SETUP = 0, FOCUS_PROF_EMBED, FOCUS_PROF_RMSNORM, FOCUS_PROF_GEMM_QKV, FOCUS_PROF_ROPE_STORE /* RoPE: unfused store, or the per-row factor tables */,
   FOCUS_PROF_ATTN, FOCUS_PROF_IMPORTANCE, FOCUS_PROF_GEMM_O, FOCUS_PROF_GEMM_GU, FOCUS_PROF_SILU,
   FOCUS_PROF_GEMM_DOWN, FOCUS_PROF_SELECT, FOCUS_PROF_GATHER, FOCUS_PROF_GEMM_LM, FOCUS_PROF_VOCAB,
   FOCUS_PROF_COMMIT, FOCUS_PROF_KINDS

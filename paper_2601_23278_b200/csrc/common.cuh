@@ -106,6 +106,10 @@ void launch_rope_store(const float* qkv_f32, const RowInfo* rows, const int* M_d
                        int n_q_heads, const float* rope_cos, const float* rope_sin,
                        const focus_req_state* st, KVView kv, bf16* qkv_out, Counters* cnt,
                        cudaStream_t s);
+// Per-row RoPE factors, transposed: out[f][r] = cos(pos_r * w_f), out[64 + f][r] = sin(pos_r * w_f)
+// (ld = row stride), copied from the fp64-built tables, for the fused QKV epilogue (head_dim 128).
+void launch_rope_rows(const RowInfo* rows, const int* M_dev, int M_max, const float* rcos, const float* rsin,
+                      float* out, int ld, cudaStream_t s);
 void launch_silu_mul(const float* gu, const int* M_dev, int M_max, int d_ff, bf16* act, cudaStream_t s);
 void launch_gather_rows(const float* x, const bf16* qkv, int qkv_dim, int q_dim, const int* src,
                         const int* M_dev, int M_max, int d, float* x_out, bf16* q_out, cudaStream_t s);
@@ -122,7 +126,7 @@ struct GemmWs {                 // split-K partials + per-tile semaphores (carve
 struct GemmEpi {
   bf16* out; int ldo;                  // SWIGLU: act [M][d_ff]; QKV_ROPE: qkv [M][(Hq+2Hkv) dh]
   const RowInfo* rows;                 // QKV_ROPE: per-row (slot, j, pos) for RoPE angle and KV slot
-  const float* rcos; const float* rsin;
+  const float* ropeT; int rope_ld;     // QKV_ROPE: launch_rope_rows table of these rows ([128][rope_ld])
   const focus_req_state* st;
   KVView kv;
   int n_q_heads;
@@ -162,6 +166,7 @@ struct AttnArgs {
   int stream_k;                 // 1: stream-K over key tiles (balanced CTAs; attention without importance)
   int tail_split;               // 1: units of the last partial round are key-split across the idle CTAs
   int l2_prefetch;              // K/V tiles past the smem rings to prefetch into L2
+  int nch_fixed;                // 1: every non-causal unit runs the 64-row softmax variant (one hot copy)
   void* plan_units;             // unit table [grid][UCAP] precomputed by k_attn_plan, or nullptr
   int* plan_n;                  // [grid] units per CTA (nullptr: the kernel builds its table itself)
 };

@@ -79,6 +79,8 @@ struct focus_ctx {
   bf16* Vpool = nullptr;
   float* rope_cos = nullptr;
   float* rope_sin = nullptr;
+  float* ropeT_P = nullptr;     // per-row RoPE factors of the P rows / S rows ([128][max_rows])
+  float* ropeT_S = nullptr;
   int* page_table = nullptr;
   focus_req_state* st = nullptr;
   int* out_tokens = nullptr;
@@ -184,6 +186,8 @@ size_t carve(focus_ctx* x, char* base) {
   x->act = (bf16*)take(R * ff * 2);
   const size_t RL = (size_t)c.max_requests * x->B;   // logit rows <= retained masked rows
   x->logits = (float*)take(RL * V * 4);
+  x->ropeT_P = (float*)take(R * 128 * 4);
+  x->ropeT_S = (float*)take(R * 128 * 4);
   x->rowP = (RowInfo*)take(R * sizeof(RowInfo));
   x->rowS = (RowInfo*)take(R * sizeof(RowInfo));
   x->rowL = (RowInfo*)take(RL * sizeof(RowInfo));
@@ -334,7 +338,11 @@ struct RowSpace {             // the rows a layer piece runs on
   int M_max;
   const RowInfo* rows;
   int M_est;                  // host estimate of the live count (last step's counter; tile-shape choice only)
+  const float* ropeT;         // launch_rope_rows table of these rows (fused QKV epilogue)
 };
+
+// fused QKV epilogue (tensor-core GEMM, head_dim 128) in use: it reads the per-row RoPE tables
+bool fused_qkv(const focus_ctx* x) { return gemm_backend() == 1 && x->cfg.head_dim == 128; }
 
 void qkv_piece(focus_ctx* x, int l, int tl, float* xr, const RowSpace& rs) {
   const focus_config& c = x->cfg;
@@ -345,10 +353,10 @@ void qkv_piece(focus_ctx* x, int l, int tl, float* xr, const RowSpace& rs) {
   // tensor-core GEMM with the RoPE + paged-KV-store epilogue (head_dim 128); otherwise GEMM -> fp32 ->
   // k_rope_store
   GemmEpi e{};
-  e.out = x->qkv; e.ldo = x->qkv_dim; e.rows = rs.rows; e.rcos = x->rope_cos; e.rsin = x->rope_sin;
+  e.out = x->qkv; e.ldo = x->qkv_dim; e.rows = rs.rows; e.ropeT = rs.ropeT; e.rope_ld = x->max_rows;
   e.st = x->st; e.kv = kv_view(x, l); e.n_q_heads = c.n_q_heads; e.cnt = x->cnt;
   bool fused = false;
-  LAUNCH(GEMM_QKV, fused = gemm_backend() == 1 &&
+  LAUNCH(GEMM_QKV, fused = fused_qkv(x) &&
                            launch_gemm_tc(x->h, c.d_model, x->max_rows, x->Wqkv[l], x->qkv_dim, c.d_model, nullptr, 0,
                                           rs.M_dev, rs.M_max, GEMM_QKV_ROPE, x->gws, s, &e, rs.M_est));
   if (!fused) {
@@ -416,6 +424,7 @@ AttnArgs attn_args(focus_ctx* x, int l, const bf16* q, int ldq, int n_req, const
   a.stream_k = getenv("FOCUS_ATTN_SK") ? 1 : 0;   // opt-in stream-K (measured slower than the tail split)
   a.tail_split = getenv("FOCUS_ATTN_TAIL") ? 1 : 0;   // opt-in: measured no faster at C3
   a.l2_prefetch = getenv("FOCUS_ATTN_PF") ? std::max(0, atoi(getenv("FOCUS_ATTN_PF"))) : 0;   // opt-in
+  a.nch_fixed = getenv("FOCUS_ATTN_NCH4") ? 1 : 0;
   a.imp_scratch = x->attn_scratch;
   a.trace = (l == x->trace_layer && x->cfg.debug_taps >= 0) ? x->attn_trace : nullptr;
   return a;
@@ -612,7 +621,9 @@ focus_status focus_kv_append(focus_ctx* x, int32_t req_id, const int32_t* prompt
     if ((rc = upload(x, x->tokP, prompt + c0, (size_t)n * 4)) != FOCUS_OK) return rc;
     if ((rc = upload(x, x->rowP, rows.data(), (size_t)n * sizeof(RowInfo))) != FOCUS_OK) return rc;
     LAUNCH(EMBED, launch_embed(x->tokP, nullptr, n, x->E, c.d_model, x->x, s));
-    RowSpace rs{nullptr, n, x->rowP, n};
+    RowSpace rs{nullptr, n, x->rowP, n, x->ropeT_P};
+    if (fused_qkv(x))
+      LAUNCH(ROPE_STORE, launch_rope_rows(x->rowP, nullptr, n, x->rope_cos, x->rope_sin, x->ropeT_P, x->max_rows, s));
     for (int l = 0; l < c.n_layers; ++l) {
       qkv_piece(x, l, -1000, x->x, rs);
       AttnArgs a = attn_args(x, l, x->qkv, x->qkv_dim, 0, nullptr, 2);
@@ -680,8 +691,10 @@ focus_status focus_step_block(focus_ctx* x, const int32_t* ids, int32_t n_req) {
   // last step's live sizes (async pinned copy) as tile-shape estimates; the first step uses the maxima
   Counters est = *x->cnt_host;
   if (est.M_P <= 0 || est.M_P > maxP) { est.M_P = maxP; est.M_S = maxP; est.M_L = maxP; }
-  RowSpace rsP{MP, maxP, x->rowP, est.M_P};
-  RowSpace rsS{MS, maxP, x->rowS, est.M_S};
+  RowSpace rsP{MP, maxP, x->rowP, est.M_P, x->ropeT_P};
+  RowSpace rsS{MS, maxP, x->rowS, est.M_S, x->ropeT_S};
+  if (fused_qkv(x))
+    LAUNCH(ROPE_STORE, launch_rope_rows(x->rowP, MP, maxP, x->rope_cos, x->rope_sin, x->ropeT_P, x->max_rows, s));
   // A2 layer 0 fully on P (+ fused importance I0)
   // attention unit tables of the P-row launches (layer 0, layer-1 importance), once per step
   AttnArgs a0 = attn_args(x, 0, x->qkv, x->qkv_dim, n_req, x->offP, 0);
@@ -722,6 +735,8 @@ focus_status focus_step_block(focus_ctx* x, const int32_t* ids, int32_t n_req) {
     sa.cnt = x->cnt;
     LAUNCH(SELECT, launch_select_plan(sa, s));
   }
+  if (fused_qkv(x) && c.n_layers > 1)
+    LAUNCH(ROPE_STORE, launch_rope_rows(x->rowS, MS, maxP, x->rope_cos, x->rope_sin, x->ropeT_S, x->max_rows, s));
   LAUNCH(GATHER, launch_gather_rows(x->x, x->qkv, x->qkv_dim, x->q_dim, x->srcP, MS, maxP, c.d_model, x->x2, x->qS, s));
   tap(x, 1, TAP_QS, x->qS, (size_t)maxP * x->q_dim * 2);
   // attention unit tables of the S-row launches (layer-1 suffix, layers >= 2), once per step

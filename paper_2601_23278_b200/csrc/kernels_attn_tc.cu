@@ -78,7 +78,8 @@ constexpr int OFF_RED = OFF_STAT + 2 * NQM * 4; // float [4][64]
 constexpr int OFF_FLAG = OFF_RED + 4 * 64 * 4;  // int [2][4]
 constexpr int OFF_ONES = OFF_FLAG + 64;         // 128 B of bf16 ones (A operand of the row-sum MMA)
 constexpr int OFF_MERGE = OFF_ONES + 128;       // float [MAXS + 1][NQM] split-merge scales + 1/l
-constexpr int OFF_UTAB = OFF_MERGE + (MAXS + 1) * NQM * 4;
+constexpr int OFF_OST = OFF_MERGE + (MAXS + 1) * NQM * 4;   // bf16 [NQM][DH] output staging (rows r, heads g)
+constexpr int OFF_UTAB = OFF_OST + NQM * DH * 2;
 constexpr int SMEM_BYTES = OFF_UTAB + UCAP * 80 + 1024;
 
 struct Unit {
@@ -873,7 +874,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           default: softmax_unit<4, true, IMP_ONLY>(a, xr, it, g, th, ss, tr); break;
         }
       } else {
-        switch (nch) {
+        switch (a.nch_fixed ? 4 : nch) {
           case 1: softmax_unit<1, false, IMP_ONLY>(a, xr, it, g, th, ss, tr); break;
           case 2: softmax_unit<2, false, IMP_ONLY>(a, xr, it, g, th, ss, tr); break;
           case 3: softmax_unit<3, false, IMP_ONLY>(a, xr, it, g, th, ss, tr); break;
@@ -887,6 +888,26 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const int d = threadIdx.x - 256;
     const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
     Tracer tr(d == 0 ? a.trace : nullptr, 5);
+    // Output rows leave through shared memory: element (query row n = r*G + g, lane d) goes to
+    // ost[n * DH + d], i.e. block row r's G heads are one contiguous G*DH*2-byte run, matching the
+    // output row [r0 + r][kvh*G*DH, (kvh+1)*G*DH); one bulk async copy per block row then writes it
+    // (instead of 2-byte scattered stores from every thread).
+    __nv_bfloat16* ost = reinterpret_cast<__nv_bfloat16*>(smem + OFF_OST);
+    auto stage_begin = [&]() {                     // the previous unit's bulk stores have read ost
+      if (d == 0) bulk_wait_read0();
+      named_bar(2, 128);
+    };
+    auto stage_flush = [&](const Unit& xr) {       // all 128 threads
+      fence_proxy_async();
+      named_bar(2, 128);
+      if (d == 0) {
+        const int nr = (xr.nq + G - 1) / G;
+        for (int r = 0; r < nr; ++r)
+          bulk_store_s2g(a.out + (size_t)(xr.r0 + r) * a.ldo + (size_t)xr.kvh * G * DH,
+                         smem_u32(ost + (size_t)r * G * DH), (uint32_t)(G * DH * 2));
+        bulk_commit();
+      }
+    };
     for (int it = 0; it < n_my; ++it) {
       const Unit& xr = utab[it];
       const int nq = xr.nq, nch = (nq + 15) >> 4;
@@ -897,7 +918,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       tr.ev(1);
       tc_fence_after();
       if (xr.nsplit == 1) {
-        // O / l straight to the bf16 output rows, 16 query rows at a time
+        // O / l -> bf16 staging, 16 query rows at a time, then one bulk store per block row
+        stage_begin();
 #pragma unroll 1
         for (int c = 0; c < nch; ++c) {
           uint32_t r[16], rl[16];
@@ -905,18 +927,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           tmem_ld32x16(tmem + lane_base + L_COL + ob * NQM + 16 * c, rl);
           tmem_wait_ld();
 #pragma unroll
-          for (int e = 0; e < 16; ++e) {
-            const int n = 16 * c + e;
-            if (n < nq) {
-              const int row = xr.r0 + n / G, head = xr.kvh * G + n % G;
-              a.out[(size_t)row * a.ldo + head * DH + d] =
-                  __float2bfloat16_rn(__uint_as_float(r[e]) / __uint_as_float(rl[e]));
-            }
-          }
+          for (int e = 0; e < 16; ++e)
+            if (16 * c + e < nq)
+              ost[(16 * c + e) * DH + d] = __float2bfloat16_rn(__uint_as_float(r[e]) / __uint_as_float(rl[e]));
         }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&ofree[ob]);
+        stage_flush(xr);
         tr.ev(2);
       } else {
         // split piece: partial (unnormalised O^T rows, running max, row sum) -> workspace; the
@@ -950,6 +968,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         named_bar(2, 128);
         if (merge_flag == xr.nsplit - 1) {               // last piece: merge
           __threadfence();
+          stage_begin();
           const int ns = xr.nsplit;
           float* fsc = reinterpret_cast<float*>(smem + OFF_MERGE);   // [MAXS][NQM] scales, [MAXS][..] 1/l
           if (d < nq) {
@@ -987,20 +1006,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
               for (int e = 0; e < 16; ++e) acc[e] += v[e] * fsc[s2 * NQM + n0 + e];
             }
 #pragma unroll
-            for (int e = 0; e < 16; ++e) {
-              const int n = n0 + e;
-              if (n < nq) {
-                const int row = xr.r0 + n / G, head = xr.kvh * G + n % G;
-                a.out[(size_t)row * a.ldo + head * DH + d] = __float2bfloat16_rn(acc[e] * fsc[MAXS * NQM + n]);
-              }
-            }
+            for (int e = 0; e < 16; ++e)
+              if (n0 + e < nq) ost[(n0 + e) * DH + d] = __float2bfloat16_rn(acc[e] * fsc[MAXS * NQM + n0 + e]);
           }
           if (d == 0) a.sem[xr.pair] = 0;                 // re-arm for the next launch
-          named_bar(2, 128);                             // fsc reuse by the next merge
+          stage_flush(xr);                               // (its barrier also orders fsc reuse by the next merge)
         }
         tr.ev(2);
       }
     }
+    if (d == 0) bulk_wait0();                        // output rows written before the CTA retires
   }
   __syncthreads();
   if (warp == 3) {

@@ -251,6 +251,10 @@ __device__ __forceinline__ void epilogue_tile(Chunk&& chunk, int row0, int M, in
     if (row < M) ri = epi.rows[row];
     if (row < M && ri.j >= 0 && ((epi.st[ri.slot].committed >> ri.j) & 1ull)) atomicExch(&epi.cnt->invariant, 1);
     const int hkv = epi.kv.n_kv_heads;
+    // this row's paged KV slot (kv head 0), looked up once per tile: the store loop below then has no
+    // dependent page-table load per 16-B chunk
+    const unsigned long long kv_row = row < M ? (unsigned long long)kv_offset(epi.kv, ri.slot, ri.pos, 0) : 0ull;
+    const size_t kv_head_stride = (size_t)epi.kv.page_size * epi.kv.head_dim;
 #pragma unroll 1
     for (int hh = 0; hh < BN / 128; ++hh) {
       const int head = nt * (BN / 128) + hh;              // 0..Hq-1 q, then k, then v
@@ -263,20 +267,15 @@ __device__ __forceinline__ void epilogue_tile(Chunk&& chunk, int row0, int M, in
         chunk(hh * 128 + c0, lo);
         chunk(hh * 128 + c0 + 64, hi);
         if (!is_v && row < M) {
-          const float4* cr = reinterpret_cast<const float4*>(epi.rcos + (size_t)ri.pos * 64 + c0);
-          const float4* sr = reinterpret_cast<const float4*>(epi.rsin + (size_t)ri.pos * 64 + c0);
+          const float* cr = epi.ropeT + (size_t)c0 * epi.rope_ld + row;          // [f][row]: coalesced
+          const float* sr = cr + (size_t)64 * epi.rope_ld;
 #pragma unroll
-          for (int i4 = 0; i4 < 8; ++i4) {
-            const float4 c4 = __ldg(cr + i4), s4 = __ldg(sr + i4);
-            const float cc[4] = {c4.x, c4.y, c4.z, c4.w}, ss[4] = {s4.x, s4.y, s4.z, s4.w};
-#pragma unroll
-            for (int t = 0; t < 4; ++t) {
-              const int i = 4 * i4 + t;
-              const float y1 = lo[i] * cc[t] - hi[i] * ss[t];
-              const float y2 = hi[i] * cc[t] + lo[i] * ss[t];
-              lo[i] = y1;
-              hi[i] = y2;
-            }
+          for (int i = 0; i < 32; ++i) {
+            const float cc = __ldg(cr + (size_t)i * epi.rope_ld), ss = __ldg(sr + (size_t)i * epi.rope_ld);
+            const float y1 = lo[i] * cc - hi[i] * ss;
+            const float y2 = hi[i] * cc + lo[i] * ss;
+            lo[i] = y1;
+            hi[i] = y2;
           }
         }
         // staged row: chunks 0..3 = bf16 cols [c0, c0+32), chunks 4..7 = cols [c0+64, c0+96)
@@ -295,11 +294,11 @@ __device__ __forceinline__ void epilogue_tile(Chunk&& chunk, int row0, int M, in
         for (int i = 0; i < 8; ++i) {
           const int r = 4 * i + rr, rw = row0 + r;
           const uint4 x = lds128(epi_slot(buf, r, jj));
-          const int slot = __shfl_sync(0xffffffffu, ri.slot, r), pos = __shfl_sync(0xffffffffu, ri.pos, r);
+          const unsigned long long kvo = __shfl_sync(0xffffffffu, kv_row, r);
           if (rw < M) {
             *reinterpret_cast<uint4*>(epi.out + (size_t)rw * epi.ldo + head * 128 + col) = x;
             if (is_k || is_v)
-              *reinterpret_cast<uint4*>((is_v ? epi.kv.V : epi.kv.K) + kv_offset(epi.kv, slot, pos, kvh) + col) = x;
+              *reinterpret_cast<uint4*>((is_v ? epi.kv.V : epi.kv.K) + kvo + (size_t)kvh * kv_head_stride + col) = x;
           }
         }
         __syncwarp();
@@ -951,7 +950,8 @@ bool launch_gemm_tc(const bf16* A, int lda, int a_rows, const bf16* W, int N, in
   const bool pair_mode = !(pm_e && pm_e[0] == '0');
   if (pair_mode) {
     const long long units256 = (long long)((m + 2 * BM - 1) / (2 * BM)) * ((N + 255) / 256);
-    const bool narrow2 = mode != GEMM_SWIGLU && 4 * units256 <= (num_sms() * 11) / 10 && getenv("FOCUS_GEMM_BN256") == nullptr;
+    const bool narrow2 = mode != GEMM_SWIGLU && getenv("FOCUS_GEMM_BN256") == nullptr &&
+                         (4 * units256 <= (num_sms() * 11) / 10 || getenv("FOCUS_GEMM_BN128") != nullptr);
     // k-atoms per stage (measured at the C3 shapes): 2 for 128-wide tiles (4 stages of 48 KB), 1 for
     // 256-wide tiles (6 stages of 32 KB); FOCUS_GEMM_KA=1|2 forces one
     static int ka_env = -1;

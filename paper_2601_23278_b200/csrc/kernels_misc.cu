@@ -176,6 +176,31 @@ void launch_rmsnorm(const float* x, const int* src_map, const int* M_dev, int M_
   launch_pdl(k_rmsnorm, dim3(M_max), dim3(256), 0, s, x, src_map, M_dev, M_max, d, eps, out);
 }
 
+// ------------------------------------------------------------------ per-row RoPE factors (transposed)
+// The fused QKV epilogue owns one row per thread; with the factors stored [f][row] a warp's load of
+// factor f for its 32 consecutive rows is one coalesced 128-B line instead of 32 scattered table rows.
+__global__ void k_rope_rows(const RowInfo* __restrict__ rows, const int* __restrict__ M_dev, int M_max,
+                            const float* __restrict__ rcos, const float* __restrict__ rsin, float* __restrict__ out,
+                            int ld) {
+  pdl_trigger();
+  pdl_wait();
+  const int M = live_rows(M_dev, M_max);
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < 64 * M_max; e += gridDim.x * blockDim.x) {
+    const int f = e / M_max, r = e - f * M_max;
+    if (r >= M) continue;
+    const int p = rows[r].pos;
+    out[(size_t)f * ld + r] = rcos[(size_t)p * 64 + f];
+    out[(size_t)(64 + f) * ld + r] = rsin[(size_t)p * 64 + f];
+  }
+}
+
+void launch_rope_rows(const RowInfo* rows, const int* M_dev, int M_max, const float* rcos, const float* rsin,
+                      float* out, int ld, cudaStream_t s) {
+  if (M_max <= 0) return;
+  const int blocks = std::min(4 * num_sms(), (64 * M_max + 255) / 256);
+  launch_pdl(k_rope_rows, dim3(blocks), dim3(256), 0, s, rows, M_dev, M_max, rcos, rsin, out, ld);
+}
+
 // ------------------------------------------------------------------ RoPE + paged KV store
 // q, k rotated (rotate-half pairs (k, k+dh/2), angle pos*theta^(-2k/dh) from a host-built fp64
 // table), rounded to bf16; k, v stored at the row's KV slot of the paged pool ("sparse KV fill",

@@ -73,7 +73,7 @@ int main(int argc, char** argv) {
   for (size_t i = 0; i < hpt.size(); ++i) hpt[i] = (int)i;
   RowInfo* drows;
   int* dpt;
-  float *rc, *rs;
+  float* rc;
   focus_req_state* dst;
   Counters* dcnt;
   bf16 *kp, *vp, *eout;
@@ -81,10 +81,8 @@ int main(int argc, char** argv) {
   cudaMemcpy(drows, hrows.data(), max_rows * sizeof(RowInfo), cudaMemcpyHostToDevice);
   cudaMalloc(&dpt, hpt.size() * 4);
   cudaMemcpy(dpt, hpt.data(), hpt.size() * 4, cudaMemcpyHostToDevice);
-  cudaMalloc(&rc, 2048 * 64 * 4);
-  cudaMalloc(&rs, 2048 * 64 * 4);
-  cudaMemset(rc, 0, 2048 * 64 * 4);
-  cudaMemset(rs, 0, 2048 * 64 * 4);
+  cudaMalloc(&rc, (size_t)max_rows * 128 * 4);   // per-row RoPE factor table [128][max_rows]
+  cudaMemset(rc, 0, (size_t)max_rows * 128 * 4);
   cudaMalloc(&dst, n_slots * sizeof(focus_req_state));
   cudaMemset(dst, 0, n_slots * sizeof(focus_req_state));
   cudaMalloc(&dcnt, sizeof(Counters));
@@ -95,8 +93,8 @@ int main(int argc, char** argv) {
   cudaMalloc(&eout, (size_t)max_rows * 12288 * 2);
   GemmEpi epi{};
   epi.rows = drows;
-  epi.rcos = rc;
-  epi.rsin = rs;
+  epi.ropeT = rc;
+  epi.rope_ld = max_rows;
   epi.st = dst;
   epi.cnt = dcnt;
   epi.kv = KVView{kp, vp, dpt, max_pages, page, n_kvh, 128};
