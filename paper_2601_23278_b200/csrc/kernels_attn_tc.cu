@@ -658,6 +658,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   const int rpc = NQM / G;
 
   pdl_trigger();
+  if (threadIdx.x == 0 && a.trace) {               // debug: entry clock and global time
+    unsigned long long gt;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+    a.trace[((size_t)blockIdx.x * 8 + 7) * kTraceEv + 1] = clock64();
+    a.trace[((size_t)blockIdx.x * 8 + 7) * kTraceEv + 2] = gt;
+  }
   if (threadIdx.x < 64) ones[threadIdx.x] = 0x3F80;   // bf16 1.0
   if (threadIdx.x == 0) {
     for (int i = 0; i < SK; ++i) { mbar_init(&kfull[i], 1); mbar_init(&kempty[i], 1); }
@@ -723,6 +729,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
       };
       const int pf = a.l2_prefetch;                // tiles past the ring to warm in L2
+      const uint64_t pol = l2_policy_evict_first();  // the KV stream is read once per layer and step
       for (int k = 0; k < n_my; ++k) {
         const Unit& x = utab[k];
         tr.ev(0);
@@ -740,8 +747,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             const int pidx = min(pos / ps, a.kv.max_pages - 1);
             const int page = a.kv.page_table[(size_t)x.slot * a.kv.max_pages + pidx];
             const int row = (int)((size_t)a.layer * layer_rows + ((size_t)page * H + x.kvh) * ps + pos % ps);
-            tma_load_2d(dst + pc * pr * 128, map, &fullb[slot], 0, row);
-            tma_load_2d(dst + HALF_KV + pc * pr * 128, map, &fullb[slot], 64, row);
+            if (a.kv_hint) {
+              tma_load_2d_hint(dst + pc * pr * 128, map, &fullb[slot], 0, row, pol);
+              tma_load_2d_hint(dst + HALF_KV + pc * pr * 128, map, &fullb[slot], 64, row, pol);
+            } else {
+              tma_load_2d(dst + pc * pr * 128, map, &fullb[slot], 0, row);
+              tma_load_2d(dst + HALF_KV + pc * pr * 128, map, &fullb[slot], 64, row);
+            }
           }
         }
       }
@@ -1021,6 +1033,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   if (warp == 3) {
     tc_fence_after();
     tmem_free<TMEM_COLS>(tmem);
+  }
+  if (threadIdx.x == 0 && a.trace) {
+    unsigned long long gt;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+    a.trace[((size_t)blockIdx.x * 8 + 7) * kTraceEv + 3] = clock64();
+    a.trace[((size_t)blockIdx.x * 8 + 7) * kTraceEv + 4] = gt;
   }
 }
 

@@ -519,6 +519,14 @@ __device__ __forceinline__ void tma_load_3d_pair(void* dst, const CUtensorMap* m
       "l"((uint64_t)map), "r"(bar_cluster), "r"(x), "r"(y), "r"(z)
       : "memory");
 }
+__device__ __forceinline__ void tma_load_3d_pair_hint(void* dst, const CUtensorMap* map, uint32_t bar_cluster, int x,
+                                                      int y, int z, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], "
+      "[%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(dst)),
+      "l"((uint64_t)map), "r"(bar_cluster), "r"(x), "r"(y), "r"(z), "l"(pol)
+      : "memory");
+}
 
 // development trace (scripts/gemm_bench.cu): per CTA, 3 roles x 256 clock64 stamps (producer after each
 // empty wait, MMA after each full wait, epilogue after each tfull wait / at the end); null = off
@@ -537,7 +545,9 @@ template <int MODE, int BN, int KA>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     k_gemm_pair(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, float* __restrict__ C,
                 int ldc, int N, int K, const int* __restrict__ M_dev, int M_max, const GemmEpi epi, int m_hint,
-                float* __restrict__ ws, int* __restrict__ sem, int sk) {
+                float* __restrict__ ws, int* __restrict__ sem, int flags) {
+  const int sk = flags & 1;                             // bit 0: stream-K schedule
+  const bool hints = (flags & 2) != 0;                  // bit 1: L2 hints (weights evict-first, activations evict-last)
   using G = GP<BN, KA>;
   constexpr int STAGES = G::STAGES, STAGE_BYTES = G::STAGE_BYTES;
   extern __shared__ uint8_t smem_raw[];
@@ -620,6 +630,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (warp == 0) {
     if (lane == 0) {
       const uint32_t full_l = mapa_shared(smem_u32(full), 0);
+      const uint64_t pol_a = l2_policy_evict_last(), pol_b = l2_policy_evict_first();
       int stage = 0;
       uint32_t phase = 0;
       long long w = w_lo;
@@ -632,8 +643,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           stamp(0);
           if (rank == 0) mbar_expect_tx(&full[stage], 2 * STAGE_BYTES);
           const uint32_t fb = full_l + stage * 8;
-          tma_load_3d_pair(sA + stage * G::A_STAGE, &mapA, fb, 0, mp * 2 * BM + (int)rank * BM, ks * KA);
-          tma_load_3d_pair(sB + stage * G::B_STAGE, &mapB, fb, 0, nt * BN + (int)rank * (BN / 2), ks * KA);
+          if (hints) {
+            tma_load_3d_pair_hint(sA + stage * G::A_STAGE, &mapA, fb, 0, mp * 2 * BM + (int)rank * BM, ks * KA, pol_a);
+            tma_load_3d_pair_hint(sB + stage * G::B_STAGE, &mapB, fb, 0, nt * BN + (int)rank * (BN / 2), ks * KA, pol_b);
+          } else {
+            tma_load_3d_pair(sA + stage * G::A_STAGE, &mapA, fb, 0, mp * 2 * BM + (int)rank * BM, ks * KA);
+            tma_load_3d_pair(sB + stage * G::B_STAGE, &mapB, fb, 0, nt * BN + (int)rank * (BN / 2), ks * KA);
+          }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -922,6 +938,12 @@ static bool launch_pair(const bf16* A, int lda, int a_rows, const bf16* W, int N
     pf_on = (ev && ev[0] == '1') ? 1 : 0;   // measured: no gain in the step (default off)
   }
   const int pf_hint = pf_on ? m : 0;
+  static int hint_on = -1;
+  if (hint_on < 0) {
+    const char* eh = getenv("FOCUS_GEMM_L2HINT");      // L2 eviction hints on the operand streams
+    hint_on = (eh && eh[0] == '0') ? 0 : 1;
+  }
+  sk |= hint_on << 1;
   switch (mode) {
     case GEMM_ADD: launch_pair_k<GEMM_ADD, BN, KA>(grid, s, ma, mb, C, ldc, N, K, M_dev, M_max, e, pf_hint, ws, sk); break;
     case GEMM_SWIGLU:

@@ -39,3 +39,14 @@ for cta in range(d.shape[0]):
     last = max((t for r in range(6) for _, t in events(cta, r)), default=t0)
     ends.append(last - t0)
 print("CTA span k cycles: min %.1f med %.1f max %.1f" % (min(ends) / 1e3, np.median(ends) / 1e3, max(ends) / 1e3))
+
+# entry -> t0 (prologue + PDL wait + plan load) and kernel extent in global time (ns)
+r7 = d[:, 7, :5].astype(np.int64)
+if (r7[:, 2] > 0).all() and (r7[:, 4] > 0).all():
+    pro = (r7[:, 0] & MASK) - (r7[:, 1] & MASK)
+    tail = (r7[:, 3] & MASK) - (r7[:, 0] & MASK)
+    print("prologue (entry->t0) k cycles: min %.1f med %.1f max %.1f" % (pro.min() / 1e3, np.median(pro) / 1e3, pro.max() / 1e3))
+    print("t0->exit k cycles: min %.1f med %.1f max %.1f" % (tail.min() / 1e3, np.median(tail) / 1e3, tail.max() / 1e3))
+    e0, e1 = r7[:, 2], r7[:, 4]
+    print("global time: first entry -> last exit %.1f us; entries spread %.1f us; exits spread %.1f us" %
+          ((e1.max() - e0.min()) / 1e3, (e0.max() - e0.min()) / 1e3, (e1.max() - e1.min()) / 1e3))
