@@ -141,11 +141,16 @@ def run_focus(args):
     D.barrier(dev)
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ncu_step = bool(os.environ.get("FOCUS_NCU_STEP"))  # ncu --profile-from-start off: capture timed step 1 only
     with Clocks(local) as clk:
         ev0.record(st)
-        for _ in range(args.steps):
+        for i in range(args.steps):
+            if ncu_step and i == 0:
+                torch.cuda.profiler.start()
             ctx.focus_step_block(rids)
             ctx.focus_commit(rids)
+            if ncu_step and i == 0:
+                torch.cuda.profiler.stop()
         ev1.record(st)
         torch.cuda.synchronize()
     D.barrier(dev)

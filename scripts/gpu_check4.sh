@@ -1,0 +1,5 @@
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || { tail -30 gpurun_out/build.log; exit 1; }
+timeout 600 python -m pytest tests/test_gpu_layers.py -x -q > gpurun_out/pytest_layers.log 2>&1; tail -3 gpurun_out/pytest_layers.log
+nvcc -gencode arch=compute_100a,code=sm_100a -O2 -std=c++17 -I include scripts/gemm_bench.cu -o /tmp/gemm_bench -Lpaper_2601_23278_b200 -lfocus -Xlinker -rpath=$PWD/paper_2601_23278_b200 2>/dev/null || exit 1
+for M in 428 728; do timeout 120 /tmp/gemm_bench $M; FOCUS_GEMM_TMARED=0 GEMM_TAG=redv4 timeout 120 /tmp/gemm_bench $M; done 2>&1 | grep -E "M=|o\(|down|check o|check down"
+bash scripts/gpu_variants.sh "tmared:" "redv4:FOCUS_GEMM_TMARED=0" "tmared2:"
