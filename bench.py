@@ -169,6 +169,14 @@ def run_focus(args):
     res = [torch.empty(n_req * rsz, dtype=torch.uint8).pin_memory() for _ in range(2)]
     done = [None, None]
     e2e_steps = max(1, min(args.steps, 20))
+    # start the e2e window at the same phase of the block cycle (B decode steps + 1 flush step per
+    # block under the synthetic dynamics) as the timed window, so both windows hold the same mix of
+    # decode and flush steps; the phase-alignment steps are untimed
+    cyc = run.method.block_size + 1
+    for _ in range((args.warmup - (args.warmup + args.steps)) % cyc):
+        ctx.focus_step_block(rids)
+        ctx.focus_commit(rids)
+    ctx.focus_sync()
     dec0 = tok_sum()
     host_decoded = 0
 

@@ -54,7 +54,7 @@ enum { FOCUS_STRATEGY_FOCUS = 0, FOCUS_STRATEGY_NONE = 1, FOCUS_STRATEGY_FIXED_T
 typedef struct {
   /* backbone (SURVEY A-M1: Qwen3-like GQA + RoPE + SwiGLU + RMSNorm; weights random-init) */
   int32_t n_layers;        /* >= 2 (layer 0 and layer 1 are structurally distinct, Alg.1)      */
-  int32_t d_model;         /* multiple of 64                                                   */
+  int32_t d_model;         /* multiple of 64, at most 8192                                      */
   int32_t n_q_heads, n_kv_heads;  /* n_q_heads % n_kv_heads == 0 (GQA)                         */
   int32_t head_dim;        /* even, multiple of 16, <= 128                                     */
   int32_t d_ff;            /* multiple of 128                                                  */

@@ -126,7 +126,7 @@ focus_status cuda_status(cudaError_t e) {
 }
 
 bool valid_config(const focus_config& c) {
-  if (c.n_layers < 2 || c.d_model <= 0 || c.d_model % 64) return false;
+  if (c.n_layers < 2 || c.d_model <= 0 || c.d_model % 64 || c.d_model > 8192) return false;   // rmsnorm: row in registers
   if (c.n_q_heads <= 0 || c.n_kv_heads <= 0 || c.n_q_heads % c.n_kv_heads) return false;
   if (!(c.head_dim == 16 || c.head_dim == 32 || c.head_dim == 64 || c.head_dim == 128)) return false;
   if (c.d_ff <= 0 || c.d_ff % kGuGroup) return false;

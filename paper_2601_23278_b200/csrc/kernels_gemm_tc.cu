@@ -172,36 +172,9 @@ __device__ __forceinline__ uint32_t pack_bf2(float a, float b) {
 // warp's first tile row (this thread's row = row0 + lane), rows >= M are not written.
 template <int MODE, int BN, typename Chunk>
 __device__ __forceinline__ void epilogue_tile(Chunk&& chunk, int row0, int M, int nt, int N, float* __restrict__ C,
-                                              int ldc, const GemmEpi& epi, uint32_t buf,
-                                              const CUtensorMap* mapC = nullptr) {
+                                              int ldc, const GemmEpi& epi, uint32_t buf) {
   const int lane = threadIdx.x & 31;
   const int rr = lane >> 3, jj = lane & 7;              // read-back: row 4i + rr, 16-B chunk jj
-  if (MODE == GEMM_ADD && mapC != nullptr) {
-    // residual += acc by TMA reduce-add: the staged 32 x 32 fp32 box (128-B swizzled rows, the layout
-    // of the tensor map) is added at L2 in one bulk operation; two staging buffers alternate so the
-    // next chunk's TMEM load overlaps the previous reduction.  Rows >= M are staged as zeros (the box
-    // covers them; x + 0 leaves them unchanged).  One contributor per element: fl(x + acc), as before.
-    const bool live = row0 + lane < M;
-#pragma unroll 1
-    for (int c0 = 0, b = 0; c0 < BN; c0 += 32, b ^= 1) {
-      float v[32];
-      chunk(c0, v);
-      const uint32_t sb = buf + b * EPI_BUF;
-      if (lane == 0) bulk_wait_read1();                 // the reduction issued two chunks ago has read sb
-      __syncwarp();
-#pragma unroll
-      for (int j = 0; j < 8; ++j) sts128(epi_slot(sb, lane, j), live ? f4_bits(v + 4 * j) : make_uint4(0, 0, 0, 0));
-      fence_proxy_async();
-      __syncwarp();
-      if (lane == 0 && nt * BN + c0 < N) {
-        tma_reduce_add_2d(mapC, sb, nt * BN + c0, row0);
-        bulk_commit();
-      }
-    }
-    if (lane == 0) bulk_wait_read0();                   // staging free for the next tile
-    __syncwarp();
-    return;
-  }
   if constexpr (MODE == GEMM_STORE || MODE == GEMM_ADD) {
     const bool vec_ok = (ldc % 4) == 0 && (((uintptr_t)C) & 15) == 0;
 #pragma unroll 1
@@ -537,7 +510,7 @@ struct GP {
   static constexpr int B_STAGE = B_ATOM * KA;
   static constexpr int STAGE_BYTES = A_STAGE + B_STAGE;
   static constexpr int STAGES = (192 * 1024) / STAGE_BYTES;
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 2 * EPI_SMEM + 1024 + 256;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_SMEM + 1024 + 256;
 };
 
 __device__ __forceinline__ void tma_load_3d_pair(void* dst, const CUtensorMap* map, uint32_t bar_cluster, int x, int y,
@@ -574,8 +547,7 @@ template <int MODE, int BN, int KA>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     k_gemm_pair(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, float* __restrict__ C,
                 int ldc, int N, int K, const int* __restrict__ M_dev, int M_max, const GemmEpi epi, int m_hint,
-                float* __restrict__ ws, int* __restrict__ sem, int flags,
-                const __grid_constant__ CUtensorMap mapC) {
+                float* __restrict__ ws, int* __restrict__ sem, int flags) {
   const int sk = flags & 1;                             // bit 0: stream-K schedule
   const bool hints = (flags & 2) != 0;                  // bit 1: L2 hints (weights evict-first, activations evict-last)
   using G = GP<BN, KA>;
@@ -584,8 +556,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * G::A_STAGE;
-  const uint32_t epi_buf = smem_u32(smem + STAGES * STAGE_BYTES) + (uint32_t)(((threadIdx.x >> 5) & 3) * 2 * EPI_BUF);
-  uint64_t* bars = (uint64_t*)(smem + STAGES * STAGE_BYTES + 2 * EPI_SMEM);
+  const uint32_t epi_buf = smem_u32(smem + STAGES * STAGE_BYTES) + (uint32_t)(((threadIdx.x >> 5) & 3) * 32 * 128);
+  uint64_t* bars = (uint64_t*)(smem + STAGES * STAGE_BYTES + EPI_SMEM);
   uint64_t* full = bars;                                // [STAGES]  (leader's are the live ones)
   uint64_t* empty = bars + STAGES;                      // [STAGES]  (both CTAs, by the leader's commit)
   uint64_t* tfull = bars + 2 * STAGES;                  // [2]       (both CTAs, by the leader's commit)
@@ -769,7 +741,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             for (int i = 0; i < 32; ++i) v[i] += __ldcg(pp + (size_t)i * BM);
           }
         };
-        epilogue_tile<MODE, BN>(chunk, row - lane, M, nt, N, C, ldc, epi, epi_buf, (flags & 4) ? &mapC : nullptr);
+        epilogue_tile<MODE, BN>(chunk, row - lane, M, nt, N, C, ldc, epi, epi_buf);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(tempty_l + acc * 8);
@@ -782,7 +754,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
       if (threadIdx.x == 128) stamp(2);
     }
-    if (lane == 0) bulk_wait0();                        // TMA reductions complete before the CTA retires
   }
   __syncthreads();
   cluster_sync();                                       // no CTA leaves while its peer may still signal it
@@ -820,21 +791,6 @@ bool get_map(const void* ptr, int rows, int cols, int ld, int box_rows, CUtensor
   const bool ok = ka == 0 ? make_tma_2d_bf16(ptr, rows, cols, ld, BK, box_rows, &m)
                           : make_tma_3d_bf16(ptr, BK, rows, cols / BK, (uint64_t)ld * 2, BK * 2, BK, box_rows, ka, &m);
   if (!ok) return false;
-  cache.emplace(k, m);
-  *out = m;
-  return true;
-}
-
-// fp32 [rows][cols] map with 32 x 32 boxes (GEMM_ADD reduce epilogue), cached like get_map
-bool get_map_f32(const void* ptr, int rows, int cols, int ld, CUtensorMap* out) {
-  static std::mutex mu;
-  static std::unordered_map<MapKey, CUtensorMap, MapKeyHash> cache;
-  std::lock_guard<std::mutex> g(mu);
-  const MapKey k{ptr, rows, cols, ld, 32, -1};
-  auto it = cache.find(k);
-  if (it != cache.end()) { *out = it->second; return true; }
-  CUtensorMap m;
-  if (!make_tma_2d_f32(ptr, rows, cols, ld, 32, &m)) return false;
   cache.emplace(k, m);
   *out = m;
   return true;
@@ -929,7 +885,7 @@ static bool launch_bn(const bf16* A, int lda, int a_rows, const bf16* W, int N, 
 template <int MODE, int BN, int KA>
 static void launch_pair_k(int grid, cudaStream_t s, const CUtensorMap& ma, const CUtensorMap& mb, float* C, int ldc,
                           int N, int K, const int* M_dev, int M_max, const GemmEpi& e, int m_hint, const GemmWs& ws,
-                          int sk, const CUtensorMap& mc) {
+                          int sk) {
   using namespace tc;
   constexpr int SMEM = GP<BN, KA>::SMEM_BYTES;
   static bool attr = false;
@@ -951,7 +907,7 @@ static void launch_pair_k(int grid, cudaStream_t s, const CUtensorMap& ma, const
   at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = pdl_enabled() ? 2 : 1;
-  cudaLaunchKernelEx(&cfg, k_gemm_pair<MODE, BN, KA>, ma, mb, C, ldc, N, K, M_dev, M_max, e, m_hint, ws.ptr, ws.sem, sk, mc);
+  cudaLaunchKernelEx(&cfg, k_gemm_pair<MODE, BN, KA>, ma, mb, C, ldc, N, K, M_dev, M_max, e, m_hint, ws.ptr, ws.sem, sk);
 }
 
 template <int BN, int KA>
@@ -990,23 +946,14 @@ static bool launch_pair(const bf16* A, int lda, int a_rows, const bf16* W, int N
     hint_on = (eh && eh[0] == '0') ? 0 : 1;
   }
   sk |= hint_on << 1;
-  // GEMM_ADD: residual += acc by TMA reduce-add boxes (FOCUS_GEMM_TMARED=0: per-thread red.global.add)
-  CUtensorMap mc{};
-  static int red_on = -1;
-  if (red_on < 0) {
-    const char* er = getenv("FOCUS_GEMM_TMARED");
-    red_on = (er && er[0] == '0') ? 0 : 1;
-  }
-  if (mode == GEMM_ADD && red_on && !(sk & 1) && (ldc % 4) == 0 && (((uintptr_t)C) & 15) == 0 &&
-      get_map_f32(C, a_rows, N, ldc, &mc))
-    sk |= 4;
+
   switch (mode) {
-    case GEMM_ADD: launch_pair_k<GEMM_ADD, BN, KA>(grid, s, ma, mb, C, ldc, N, K, M_dev, M_max, e, pf_hint, ws, sk, mc); break;
+    case GEMM_ADD: launch_pair_k<GEMM_ADD, BN, KA>(grid, s, ma, mb, C, ldc, N, K, M_dev, M_max, e, pf_hint, ws, sk); break;
     case GEMM_SWIGLU:
-      if constexpr (BN == 2 * kGuGroup) launch_pair_k<GEMM_SWIGLU, BN, KA>(grid, s, ma, mb, C, ldc, N, K, M_dev, M_max, e, pf_hint, ws, sk, mc);
+      if constexpr (BN == 2 * kGuGroup) launch_pair_k<GEMM_SWIGLU, BN, KA>(grid, s, ma, mb, C, ldc, N, K, M_dev, M_max, e, pf_hint, ws, sk);
       break;
-    case GEMM_QKV_ROPE: launch_pair_k<GEMM_QKV_ROPE, BN, KA>(grid, s, ma, mb, C, ldc, N, K, M_dev, M_max, e, pf_hint, ws, sk, mc); break;
-    default: launch_pair_k<GEMM_STORE, BN, KA>(grid, s, ma, mb, C, ldc, N, K, M_dev, M_max, e, pf_hint, ws, sk, mc);
+    case GEMM_QKV_ROPE: launch_pair_k<GEMM_QKV_ROPE, BN, KA>(grid, s, ma, mb, C, ldc, N, K, M_dev, M_max, e, pf_hint, ws, sk); break;
+    default: launch_pair_k<GEMM_STORE, BN, KA>(grid, s, ma, mb, C, ldc, N, K, M_dev, M_max, e, pf_hint, ws, sk);
   }
   return true;
 }

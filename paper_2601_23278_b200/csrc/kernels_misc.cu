@@ -1,3 +1,4 @@
+#include <cstdio>
 // Small HBM-bound kernels of the decode step: weight init, step setup (P/M/U masks, ragged row
 // maps), embedding gather, RMSNorm, RoPE + paged KV store, SwiGLU, row compaction gather.
 #include "common.cuh"
@@ -136,43 +137,54 @@ void launch_embed(const int* tok, const int* M_dev, int M_max, const bf16* E, in
 __global__ void k_rmsnorm(const float* __restrict__ x, const int* __restrict__ src_map,
                           const int* __restrict__ M_dev, int M_max, int d, float eps,
                           bf16* __restrict__ out) {
+  // one row per block; the row stays in registers between the sum of squares and the scaling
+  // (one read of x), vector loads/stores, d <= 4 * 256 * kRmsVec
+  constexpr int kRmsVec = 8;
   pdl_trigger();
   pdl_wait();
   const int r = blockIdx.x;
   if (r >= live_rows(M_dev, M_max)) return;
   const int src = src_map ? src_map[r] : r;
   const float* xr = x + (size_t)src * d;
+  float4 v[kRmsVec];
   float ss = 0.f;
-  for (int c = threadIdx.x * 4; c < d; c += blockDim.x * 4) {
-    const float4 v = *reinterpret_cast<const float4*>(xr + c);
-    ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+#pragma unroll
+  for (int i = 0; i < kRmsVec; ++i) {
+    const int c = (i * blockDim.x + threadIdx.x) * 4;
+    v[i] = c < d ? __ldcg(reinterpret_cast<const float4*>(xr + c)) : make_float4(0.f, 0.f, 0.f, 0.f);
+    ss += v[i].x * v[i].x + v[i].y * v[i].y + v[i].z * v[i].z + v[i].w * v[i].w;
   }
   __shared__ float red[32];
   for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
   __syncthreads();
   if (threadIdx.x < 32) {
-    float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
-    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (threadIdx.x == 0) red[0] = v;
+    float t = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+    for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (threadIdx.x == 0) red[0] = t;
   }
   __syncthreads();
   const float inv = 1.0f / sqrtf(red[0] / (float)d + eps);
   bf16* o = out + (size_t)r * d;
-  for (int c = threadIdx.x * 4; c < d; c += blockDim.x * 4) {
-    const float4 v = *reinterpret_cast<const float4*>(xr + c);
-    __nv_bfloat162 lo = __floats2bfloat162_rn(v.x * inv, v.y * inv);
-    __nv_bfloat162 hi = __floats2bfloat162_rn(v.z * inv, v.w * inv);
-    uint2 pk;
-    pk.x = *reinterpret_cast<uint32_t*>(&lo);
-    pk.y = *reinterpret_cast<uint32_t*>(&hi);
-    *reinterpret_cast<uint2*>(o + c) = pk;
+#pragma unroll
+  for (int i = 0; i < kRmsVec; ++i) {
+    const int c = (i * blockDim.x + threadIdx.x) * 4;
+    if (c < d) {
+      __nv_bfloat162 lo = __floats2bfloat162_rn(v[i].x * inv, v[i].y * inv);
+      __nv_bfloat162 hi = __floats2bfloat162_rn(v[i].z * inv, v[i].w * inv);
+      uint2 pk;
+      pk.x = *reinterpret_cast<uint32_t*>(&lo);
+      pk.y = *reinterpret_cast<uint32_t*>(&hi);
+      *reinterpret_cast<uint2*>(o + c) = pk;
+    }
   }
 }
 
 void launch_rmsnorm(const float* x, const int* src_map, const int* M_dev, int M_max, int d, float eps,
                     bf16* out, cudaStream_t s) {
   if (M_max <= 0) return;
+  // the register-resident row needs d <= 256 threads * 8 float4 (every SDAR shape: d <= 4096)
+  if (d > 256 * 8 * 4 || d % 4) { std::fprintf(stderr, "libfocus: rmsnorm width %d unsupported\n", d); return; }
   launch_pdl(k_rmsnorm, dim3(M_max), dim3(256), 0, s, x, src_map, M_dev, M_max, d, eps, out);
 }
 

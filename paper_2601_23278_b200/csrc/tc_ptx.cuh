@@ -40,16 +40,8 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 __device__ __forceinline__ void bulk_store_s2g(void* gdst, uint32_t ssrc, uint32_t bytes) {
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(ssrc), "r"(bytes) : "memory");
 }
-// TMA reduce-add of a shared-memory box into global memory (element type from the tensor map)
-__device__ __forceinline__ void tma_reduce_add_2d(const CUtensorMap* map, uint32_t ssrc, int x, int y) {
-  asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
-                   (uint64_t)map),
-               "r"(ssrc), "r"(x), "r"(y)
-               : "memory");
-}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
@@ -323,9 +315,6 @@ __device__ __forceinline__ uint32_t sw128_off(int r, int c) {
 }  // namespace tc
 
 // Host: cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda needed).
-// 2-D fp32 tensor [rows][cols], row stride ld_elems, box [box_rows][32] (128 B rows), 128-B swizzle
-bool make_tma_2d_f32(const void* ptr, uint64_t rows, uint64_t cols, uint64_t ld_elems, uint32_t box_rows,
-                     CUtensorMap* out);
 bool make_tma_2d_bf16(const void* ptr, uint64_t rows, uint64_t cols, uint64_t ld_elems, uint32_t box_cols,
                       uint32_t box_rows, CUtensorMap* out);
 bool make_tma_3d_bf16(const void* ptr, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t s1_bytes, uint64_t s2_bytes,
