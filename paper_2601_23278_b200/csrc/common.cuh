@@ -122,6 +122,14 @@ struct GemmWs {                 // split-K partials + per-tile semaphores (carve
   int* sem;
   size_t sem_count;
 };
+// One work unit of the tensor-core attention kernel (request i of the call, query-row chunk, kv head,
+// key split; key tiles [t_lo, t_hi) of 128 keys), as planned once per step by k_attn_plan.
+struct AttnUnit {
+  int i, chunk, kvh, sp, nsplit, slot, r0, nr, nq, kbeg, kend, t_lo, t_hi, s0, pos_base, pair;
+  uint64_t P;
+  int want_imp, pad;
+};
+
 // Fused-epilogue parameters (tensor-core GEMM only).
 struct GemmEpi {
   bf16* out; int ldo;                  // SWIGLU: act [M][d_ff]; QKV_ROPE: qkv [M][(Hq+2Hkv) dh]
@@ -131,6 +139,12 @@ struct GemmEpi {
   KVView kv;
   int n_q_heads;
   Counters* cnt;
+  // QKV_ROPE, layers >= 2: L2 prefetch of the next attention launch's context K/V.  While the GEMM
+  // runs, its idle warp prefetches the first pf_tiles key tiles (context keys only: the block's own
+  // slots are being written by this GEMM) of the units the attention CTAs run first
+  const AttnUnit* pf_units;            // plan [pf_grid][pf_ucap] (nullptr: off)
+  const int* pf_n;                     // [pf_grid] units per attention CTA
+  int pf_grid, pf_ucap, pf_tiles;
 };
 // a_rows: allocated rows of A (TMA bounds); M_dev/M_max: live / maximum rows of this call.
 void launch_gemm(const bf16* A, int lda, int a_rows, const bf16* W, int N, int K, float* C, int ldc,
@@ -181,6 +195,7 @@ void launch_attention_tc(const CUtensorMap& mk, const CUtensorMap& mv, const CUt
                          cudaStream_t s);
 bool launch_attention_plan(const AttnArgs& a, cudaStream_t s);
 int attn_tc_plan_capacity();
+int attn_tc_grid(const AttnArgs& a);   // CTAs of a tensor-core attention launch (0: nothing to do)
 
 struct SelectArgs {
   const int* req_list; int n_req;

@@ -69,6 +69,7 @@ struct focus_ctx {
   void* plan_units[4] = {};       // per-step attention unit tables: layer 0, layer-1 importance,
   int* plan_n[4] = {};            // layer-1 suffix, layers >= 2
   int trace_layer = -1;
+  int pf_tiles = 0, pf_grid = 0;  // QKV-GEMM L2 prefetch of the attention's first K/V tiles (per CTA)
   int* attn_sem = nullptr;
   // weights
   bf16* E = nullptr;
@@ -339,6 +340,7 @@ struct RowSpace {             // the rows a layer piece runs on
   const RowInfo* rows;
   int M_est;                  // host estimate of the live count (last step's counter; tile-shape choice only)
   const float* ropeT;         // launch_rope_rows table of these rows (fused QKV epilogue)
+  bool pf_attn = false;       // the following attention launch uses plan slot 3 (layers >= 2)
 };
 
 // fused QKV epilogue (tensor-core GEMM, head_dim 128) in use: it reads the per-row RoPE tables
@@ -355,6 +357,13 @@ void qkv_piece(focus_ctx* x, int l, int tl, float* xr, const RowSpace& rs) {
   GemmEpi e{};
   e.out = x->qkv; e.ldo = x->qkv_dim; e.rows = rs.rows; e.ropeT = rs.ropeT; e.rope_ld = x->max_rows;
   e.st = x->st; e.kv = kv_view(x, l); e.n_q_heads = c.n_q_heads; e.cnt = x->cnt;
+  if (rs.pf_attn && x->pf_tiles > 0) {         // layers >= 2: warm L2 with the attention's first K/V tiles
+    e.pf_units = static_cast<const AttnUnit*>(x->plan_units[3]);
+    e.pf_n = x->plan_n[3];
+    e.pf_grid = x->pf_grid;
+    e.pf_ucap = attn_tc_plan_capacity();
+    e.pf_tiles = x->pf_tiles;
+  }
   bool fused = false;
   LAUNCH(GEMM_QKV, fused = fused_qkv(x) &&
                            launch_gemm_tc(x->h, c.d_model, x->max_rows, x->Wqkv[l], x->qkv_dim, c.d_model, nullptr, 0,
@@ -746,13 +755,25 @@ focus_status focus_step_block(focus_ctx* x, const int32_t* ids, int32_t n_req) {
   AttnArgs a2 = attn_args(x, 1, x->qS, x->q_dim, n_req, x->offS, 0);
   AttnArgs a3 = attn_args(x, 2, x->qkv, x->qkv_dim, n_req, x->offS, 1);
   if (x->attn_tc && plan_attention(x, a2, 2)) ++x->launches;
-  if (x->attn_tc && c.n_layers > 2 && plan_attention(x, a3, 3)) ++x->launches;
+  x->pf_tiles = 0;
+  if (x->attn_tc && c.n_layers > 2 && plan_attention(x, a3, 3)) {
+    ++x->launches;
+    static int pf_env = -1;
+    if (pf_env < 0) {
+      const char* e = getenv("FOCUS_ATTN_L2PF_TILES");
+      pf_env = e ? std::max(0, atoi(e)) : 0;
+    }
+    x->pf_tiles = pf_env;
+    x->pf_grid = attn_tc_grid(a3);
+  }
   // A6 layer-1 suffix on S: keys = context + whole block
   LAUNCH(ATTN, run_attention(x, a2));
   out_mlp_piece(x, 1, 1, x->x2, rsS);
   // A7 layers 2.. on S: keys = context + block [0, R'] (same unit table for every layer)
+  RowSpace rsS2 = rsS;
+  rsS2.pf_attn = true;
   for (int l = 2; l < c.n_layers; ++l) {
-    qkv_piece(x, l, l, x->x2, rsS);
+    qkv_piece(x, l, l, x->x2, rsS2);
     AttnArgs a = a3;
     const AttnArgs al = attn_args(x, l, x->qkv, x->qkv_dim, n_req, x->offS, 1);
     a.kv = al.kv;

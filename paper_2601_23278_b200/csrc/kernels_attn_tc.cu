@@ -82,11 +82,7 @@ constexpr int OFF_OST = OFF_MERGE + (MAXS + 1) * NQM * 4;   // bf16 [NQM][DH] ou
 constexpr int OFF_UTAB = OFF_OST + NQM * DH * 2;
 constexpr int SMEM_BYTES = OFF_UTAB + UCAP * 80 + 1024;
 
-struct Unit {
-  int i, chunk, kvh, sp, nsplit, slot, r0, nr, nq, kbeg, kend, t_lo, t_hi, s0, pos_base, pair;
-  uint64_t P;
-  int want_imp, pad;
-};
+using Unit = AttnUnit;
 static_assert(sizeof(Unit) == 80, "unit descriptor size");
 
 // debug trace: role r of this CTA appends clock64 stamps (event kind in the top 8 bits)
@@ -1091,7 +1087,9 @@ static void launch_tc(const CUtensorMap& mk, const CUtensorMap& mv, const CUtens
   launch_pdl(attn::k_attn_tc<IMP>, dim3(grid), dim3(attn::NTHREADS), attn::SMEM_BYTES, s, mk, mv, mq, a);
 }
 
-static int attn_grid(const AttnArgs& a) {
+int attn_tc_grid(const AttnArgs& a);
+static int attn_grid(const AttnArgs& a) { return attn_tc_grid(a); }
+int attn_tc_grid(const AttnArgs& a) {
   const int G = a.n_q_heads / a.kv.n_kv_heads;
   const int rpc = attn::NQM / G;
   int max_units;

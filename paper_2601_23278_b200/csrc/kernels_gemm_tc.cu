@@ -686,6 +686,34 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         mma_commit_pair(&tfull[acc]);
       }
     }
+  } else if (warp == 3) {
+    if constexpr (MODE == GEMM_QKV_ROPE) {
+      // L2 prefetch of the next attention launch's context K/V (see GemmEpi::pf_units): attention CTA
+      // c's first units, pf_tiles key tiles each, spread over this GEMM's CTAs.  Context pages are
+      // complete (committed in earlier steps); the plan comes from this step's k_attn_plan, which
+      // completed before this kernel's griddepcontrol.wait returned.
+      if (lane == 0 && epi.pf_units != nullptr && epi.pf_tiles > 0) {
+        const KVView& kv = epi.kv;
+        const uint32_t page_bytes = (uint32_t)kv.page_size * kv.head_dim * 2;
+        const int tile_keys = 128;
+        for (int c = blockIdx.x; c < epi.pf_grid; c += gridDim.x) {
+          const int n = min(epi.pf_n[c], epi.pf_ucap);
+          int budget = epi.pf_tiles;
+          for (int k = 0; k < n && budget > 0; ++k) {
+            const AttnUnit& u = epi.pf_units[(size_t)c * epi.pf_ucap + k];
+            for (int t = u.t_lo; t < u.t_hi && budget > 0; ++t, --budget) {
+              const int k0 = t * tile_keys, k1 = min(k0 + tile_keys, u.s0);   // context keys only
+              for (int pos = k0; pos < k1; pos += kv.page_size) {
+                const int page = kv.page_table[(size_t)u.slot * kv.max_pages + pos / kv.page_size];
+                const size_t off = (((size_t)page * kv.n_kv_heads + u.kvh) * kv.page_size) * kv.head_dim;
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(kv.K + off), "r"(page_bytes) : "memory");
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(kv.V + off), "r"(page_bytes) : "memory");
+              }
+            }
+          }
+        }
+      }
+    }
   } else if (warp >= 4) {
     const int q = warp - 4;
     const int rl = q * 32 + lane;                        // this thread's row within the CTA's 128
