@@ -550,6 +550,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 float* __restrict__ ws, int* __restrict__ sem, int flags) {
   const int sk = flags & 1;                             // bit 0: stream-K schedule
   const bool hints = (flags & 2) != 0;                  // bit 1: L2 hints (weights evict-first, activations evict-last)
+  const int epoch = flags >> 3;                         // bits 3..: launch epoch of the ordered split-K flags
   using G = GP<BN, KA>;
   constexpr int STAGES = G::STAGES, STAGE_BYTES = G::STAGE_BYTES;
   extern __shared__ uint8_t smem_raw[];
@@ -618,8 +619,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   auto empty_range = [&](int qq) { return (long long)qq * W / n_pairs == (long long)(qq + 1) * W / n_pairs; };
   struct PSeg { int u, k0, k1; };
   // segment i of this pair (valid while the returned u < units)
+  // Ordered split-K (flags bit 2, GEMM_ADD, one wave): pair p computes half p & 1 of the k-blocks of
+  // unit p >> 1; half 0 adds its partial to the residual first and raises the unit's flag, half 1
+  // waits for the flag before adding its own, so the result is fl(fl(x + acc_0) + acc_1) on every run.
+  const bool split2 = MODE == GEMM_ADD && (flags & 4) && !sk && 2 * units <= n_pairs && (ks_n % 2) == 0;
   auto seg_at = [&](int i, long long& w) -> PSeg {
     PSeg g;
+    if (split2) {
+      g.u = i == 0 ? pair >> 1 : units;
+      g.k0 = (pair & 1) * (ks_n / 2);
+      g.k1 = g.k0 + ks_n / 2;
+      return g;
+    }
     if (!sk) { g.u = pair + i * n_pairs; g.k0 = 0; g.k1 = ks_n; return g; }
     if (w >= w_hi) { g.u = units; g.k0 = g.k1 = 0; return g; }
     g.u = (int)(w / ks_n);
@@ -730,7 +741,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       tc_fence_after();
       const int row = mp * 2 * BM + (int)rank * BM + rl;
       const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
-      if (g.k0 > 0) {
+      if (g.k0 > 0 && !split2) {
         // later piece of a cut unit: fp32 partial -> this CTA's slot, then flag it for the finaliser
 #pragma unroll 1
         for (int c0 = 0; c0 < BN; c0 += 32) {
@@ -748,7 +759,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       } else {
         // whole unit, or the first piece: add the partials of the pieces that follow (pairs
         // pair+1 .. owner(last stage of the unit), same CTA rank), in pair order
-        const int q1 = g.k1 < ks_n ? owner((long long)(g.u + 1) * ks_n - 1) : pair;
+        const int q1 = (g.k1 < ks_n && !split2) ? owner((long long)(g.u + 1) * ks_n - 1) : pair;
+        int* sflag = sem + 2048 + 2 * g.u + (int)rank;   // ordered split-K flag of this unit's rows
+        if (split2 && g.k0 > 0) {                        // half 1: half 0 has added its partial
+          if (threadIdx.x == 128) {
+            int f = 0;
+            do {
+              asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(f) : "l"(sflag) : "memory");
+            } while (f != epoch);
+          }
+          named_bar(1, 128);
+        }
         if (q1 > pair) {
           if (threadIdx.x == 128)
             for (int qq = pair + 1; qq <= q1; ++qq) {
@@ -773,6 +794,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(tempty_l + acc * 8);
+        if (split2 && g.k0 == 0) {                       // half 0: residual updated -> release the flag
+          __threadfence();
+          named_bar(1, 128);
+          if (threadIdx.x == 128) asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(sflag), "r"(epoch) : "memory");
+        }
         if (q1 > pair) {
           named_bar(1, 128);                             // every thread has read the partials
           if (threadIdx.x == 128)
@@ -941,7 +967,7 @@ static void launch_pair_k(int grid, cudaStream_t s, const CUtensorMap& ma, const
 template <int BN, int KA>
 static bool launch_pair(const bf16* A, int lda, int a_rows, const bf16* W, int N, int K, float* C, int ldc,
                         const int* M_dev, int M_max, GemmMode mode, const GemmWs& ws, cudaStream_t s, const GemmEpi* epi,
-                        int m) {
+                        int m, bool split2 = false) {
   using namespace tc;
   if ((mode == GEMM_SWIGLU || mode == GEMM_QKV_ROPE) && (!epi || N % BN)) return false;
   if (mode == GEMM_SWIGLU && BN != 2 * kGuGroup) return false;
@@ -960,7 +986,10 @@ static bool launch_pair(const bf16* A, int lda, int a_rows, const bf16* W, int N
   if (ws.ptr == nullptr || ws.sem == nullptr || ws.sem_count < (size_t)2 * np ||
       ws.bytes < (size_t)2 * np * BM * BN * sizeof(float))
     sk = 0;
-  const int grid = sk ? 2 * np : (int)std::max<long long>(2, std::min<long long>(np, units) * 2);
+  const bool split2_ok = split2 && mode == GEMM_ADD && !sk && ws.sem != nullptr && ws.sem_count >= 2048 + 2 * (size_t)np &&
+                         (K / (BK * KA)) % 2 == 0 && 2 * units <= np;
+  const int grid = sk ? 2 * np
+                      : (int)std::max<long long>(2, std::min<long long>(np, split2_ok ? 2 * units : units) * 2);
   const GemmEpi e = epi ? *epi : GemmEpi{};
   static int pf_on = -1;
   if (pf_on < 0) {
@@ -974,6 +1003,12 @@ static bool launch_pair(const bf16* A, int lda, int a_rows, const bf16* W, int N
     hint_on = (eh && eh[0] == '0') ? 0 : 1;
   }
   sk |= hint_on << 1;
+  // GEMM_ADD, 256-wide tiles, one wave even with two k-halves per unit: ordered split-K (see kernel)
+  if (split2_ok) {
+    static unsigned epoch = 0;
+    epoch = epoch % 0xFFFFFFu + 1;
+    sk |= 4 | (int)(epoch << 3);
+  }
 
   switch (mode) {
     case GEMM_ADD: launch_pair_k<GEMM_ADD, BN, KA>(grid, s, ma, mb, C, ldc, N, K, M_dev, M_max, e, pf_hint, ws, sk); break;
@@ -1013,6 +1048,16 @@ bool launch_gemm_tc(const bf16* A, int lda, int a_rows, const bf16* W, int N, in
       ka_env = (e && (e[0] == '1' || e[0] == '2')) ? e[0] - '0' : 0;
     }
     const int ka = ka_env ? ka_env : (narrow2 ? 2 : 1);
+    // GEMM_ADD whose 256-wide units fit one wave twice over: 256-wide tiles with ordered split-K
+    // (FOCUS_GEMM_SPLIT2=0: off) instead of 128-wide tiles, halving the activation re-reads
+    static int s2_env = -1;
+    if (s2_env < 0) {
+      const char* e = getenv("FOCUS_GEMM_SPLIT2");
+      s2_env = (e && e[0] == '0') ? 0 : 1;
+    }
+    // (measured at M = 428: down, K = 12288, 57 -> 53 us; O, K = 4096, 29 -> 33 us, so only for deep K)
+    if (s2_env && mode == GEMM_ADD && 2 * units256 <= num_sms() / 2 && K >= 8192 && K % (2 * BK) == 0 && ka_env == 0)
+      return launch_pair<256, 1>(A, lda, a_rows, W, N, K, C, ldc, M_dev, M_max, mode, ws, s, epi, m, true);
     if (ka == 2 && K % (2 * BK) == 0) {
       if (narrow2) return launch_pair<128, 2>(A, lda, a_rows, W, N, K, C, ldc, M_dev, M_max, mode, ws, s, epi, m);
       return launch_pair<256, 2>(A, lda, a_rows, W, N, K, C, ldc, M_dev, M_max, mode, ws, s, epi, m);
