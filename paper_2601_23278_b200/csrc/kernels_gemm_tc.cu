@@ -622,13 +622,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   // Ordered split-K (flags bit 2, GEMM_ADD, one wave): pair p computes half p & 1 of the k-blocks of
   // unit p >> 1; half 0 adds its partial to the residual first and raises the unit's flag, half 1
   // waits for the flag before adding its own, so the result is fl(fl(x + acc_0) + acc_1) on every run.
-  const bool split2 = MODE == GEMM_ADD && (flags & 4) && !sk && 2 * units <= n_pairs && (ks_n % 2) == 0;
+  const bool split2 = MODE == GEMM_ADD && (flags & 4) && !sk && 2 * units <= n_pairs && ks_n >= 4;
   auto seg_at = [&](int i, long long& w) -> PSeg {
     PSeg g;
     if (split2) {
+      // half 0 takes ks_n / 32 fewer k-blocks: its residual add then overlaps half 1's last k-blocks
+      const int h0 = ks_n / 2 - ks_n / 32;
       g.u = i == 0 ? pair >> 1 : units;
-      g.k0 = (pair & 1) * (ks_n / 2);
-      g.k1 = g.k0 + ks_n / 2;
+      g.k0 = (pair & 1) ? h0 : 0;
+      g.k1 = (pair & 1) ? ks_n : h0;
       return g;
     }
     if (!sk) { g.u = pair + i * n_pairs; g.k0 = 0; g.k1 = ks_n; return g; }
