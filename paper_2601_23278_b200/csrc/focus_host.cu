@@ -4,6 +4,7 @@
 // The step (focus_step_block) is a fixed sequence of stream-ordered launches with no host sync and
 // no device->host copy; ragged sizes (M_P, M_S, M_logit) live in device counters and every kernel
 // reads them, so grids are sized by host-known upper bounds (n_req * B).
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstdio>
@@ -116,6 +117,20 @@ struct focus_ctx {
   size_t prof_used = 0;
   std::vector<int> prof_kind;                    // per record
   focus_prof_entry prof_acc[FOCUS_PROF_KINDS];
+  // whole-step CUDA graphs: the launch sequence of focus_step_block for one request
+  // list and one tile-shape estimate bucket, captured once and replayed
+  struct StepGraph {
+    std::vector<int32_t> list;
+    int bucket[3];
+    cudaGraphExec_t exec = nullptr;
+    int32_t* list_host = nullptr;   // pinned copy of the list: the captured H2D copy reads it
+    uint64_t launches = 0;
+    uint64_t last_use = 0;
+  };
+  std::vector<StepGraph> graphs;
+  uint64_t graph_clock = 0;
+  const int32_t* upload_src = nullptr;   // graph capture: the request list's pinned source
+  cudaStream_t cap_stream = nullptr;      // capture stream (the context stream may be the legacy one)
 };
 
 namespace {
@@ -313,6 +328,8 @@ void prof_collect(focus_ctx* x) {
 
 // Stage `bytes` of host data in the pinned ring and copy them to `dst` on the stream.
 focus_status upload(focus_ctx* x, void* dst, const void* src, size_t bytes) {
+  if (x->upload_src)   // graph capture: a memcpy node reading the graph's own pinned buffer
+    return cuda_status(cudaMemcpyAsync(dst, x->upload_src, bytes, cudaMemcpyHostToDevice, x->stream));
   Upload& u = x->up;
   if (bytes > u.cap / Upload::kSlots) {           // large: synchronous copy
     return cuda_status(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, x->stream)) == FOCUS_OK
@@ -586,6 +603,11 @@ focus_status focus_destroy(focus_ctx* x) {
   cudaStreamSynchronize(x->stream);
   for (int i = 0; i < Upload::kSlots; ++i) cudaEventDestroy(x->up.ev[i]);
   for (cudaEvent_t e : x->prof_events) cudaEventDestroy(e);
+  for (auto& g : x->graphs) {
+    cudaGraphExecDestroy(g.exec);
+    cudaFreeHost(g.list_host);
+  }
+  if (x->cap_stream) cudaStreamDestroy(x->cap_stream);
   cudaFreeHost(x->up.host);
   cudaFreeHost(x->cnt_host);
   delete x;
@@ -680,14 +702,96 @@ static focus_status check_list(focus_ctx* x, const int32_t* ids, int32_t n) {
   return FOCUS_OK;
 }
 
+static focus_status enqueue_step(focus_ctx* x, const int32_t* ids, int32_t n_req);
+
+static bool graphs_enabled(const focus_ctx* x) {
+  static int env = -1;
+  if (env < 0) {
+    const char* e = getenv("FOCUS_GRAPH");
+    env = (e && e[0] == '0') ? 0 : 1;
+  }
+  return env == 1 && !x->prof_on && x->cfg.debug_taps == 0 && x->trace_layer < 0;
+}
+
 focus_status focus_step_block(focus_ctx* x, const int32_t* ids, int32_t n_req) {
   if (!x) return FOCUS_ERR_STATE;
   if (x->step_pending) return FOCUS_ERR_STATE;
   focus_status rc = check_list(x, ids, n_req);
   if (rc != FOCUS_OK) return rc;
+  const bool same_list = x->last_list.size() == (size_t)n_req && std::equal(ids, ids + n_req, x->last_list.begin());
   x->pending_list.assign(ids, ids + n_req);
   x->step_pending = true;
   if (n_req == 0) return FOCUS_OK;
+  if (!graphs_enabled(x)) return enqueue_step(x, ids, n_req);
+  // graph key: the request list and the tile-shape estimate (last step's live row counts, 64-row
+  // buckets) that the launch sequence bakes in; device-side sizes keep any replay exact
+  const int maxP = n_req * x->B;
+  Counters est = *x->cnt_host;
+  if (est.M_P <= 0 || est.M_P > maxP) { est.M_P = maxP; est.M_S = maxP; est.M_L = maxP; }
+  const int bucket[3] = {est.M_P / 64, est.M_S / 64, est.M_L / 64};
+  ++x->graph_clock;
+  // a graph of this list whose estimates are all within one bucket is replayed (so the step-to-step
+  // jitter of the live row counts does not re-capture); block-start / flush steps, whose row counts
+  // differ a lot, get graphs of their own (up to 8 graphs, least recently used evicted)
+  for (auto& g : x->graphs) {
+    if (g.list.size() != (size_t)n_req || !std::equal(ids, ids + n_req, g.list.begin())) continue;
+    bool near = true;
+    for (int k = 0; k < 3; ++k) near = near && std::abs(g.bucket[k] - bucket[k]) < 2;
+    if (!near) continue;
+    g.last_use = x->graph_clock;
+    x->launches += g.launches;
+    x->last_list = x->pending_list;
+    return cuda_status(cudaGraphLaunch(g.exec, x->stream));
+  }
+  // capture only in a steady state (the same list as the previous step); otherwise launch eagerly
+  if (!same_list) return enqueue_step(x, ids, n_req);
+  focus_ctx::StepGraph g;
+  g.list.assign(ids, ids + n_req);
+  for (int i = 0; i < 3; ++i) g.bucket[i] = bucket[i];
+  if (cudaMallocHost(&g.list_host, (size_t)n_req * 4) != cudaSuccess) return FOCUS_ERR_CUDA;
+  std::memcpy(g.list_host, ids, (size_t)n_req * 4);
+  cudaGraph_t graph = nullptr;
+  const uint64_t l0 = x->launches;
+  if (!x->cap_stream && cudaStreamCreateWithFlags(&x->cap_stream, cudaStreamNonBlocking) != cudaSuccess) {
+    cudaFreeHost(g.list_host);
+    return FOCUS_ERR_CUDA;
+  }
+  // capture on the private stream (capturing the legacy default stream is not allowed); the graph is
+  // then launched on the context stream, so stream order is unchanged
+  cudaStream_t user = x->stream;
+  x->stream = x->cap_stream;
+  if ((rc = cuda_status(cudaStreamBeginCapture(x->stream, cudaStreamCaptureModeThreadLocal))) != FOCUS_OK) {
+    x->stream = user;
+    cudaFreeHost(g.list_host);
+    return rc;
+  }
+  x->upload_src = g.list_host;
+  rc = enqueue_step(x, ids, n_req);
+  x->upload_src = nullptr;
+  const cudaError_t ec = cudaStreamEndCapture(x->stream, &graph);
+  x->stream = user;
+  if (rc == FOCUS_OK && ec == cudaSuccess) rc = cuda_status(cudaGraphInstantiate(&g.exec, graph, 0));
+  else if (rc == FOCUS_OK) rc = cuda_status(ec);
+  if (graph) cudaGraphDestroy(graph);
+  if (rc != FOCUS_OK) {
+    cudaFreeHost(g.list_host);
+    return rc;
+  }
+  g.launches = x->launches - l0;
+  g.last_use = x->graph_clock;
+  if (x->graphs.size() >= 8) {   // keep the 8 most recently used
+    auto lru = std::min_element(x->graphs.begin(), x->graphs.end(),
+                                [](const focus_ctx::StepGraph& a, const focus_ctx::StepGraph& b) { return a.last_use < b.last_use; });
+    cudaGraphExecDestroy(lru->exec);
+    cudaFreeHost(lru->list_host);
+    x->graphs.erase(lru);
+  }
+  x->graphs.push_back(g);
+  return cuda_status(cudaGraphLaunch(x->graphs.back().exec, x->stream));
+}
+
+static focus_status enqueue_step(focus_ctx* x, const int32_t* ids, int32_t n_req) {
+  focus_status rc;
   const focus_config& c = x->cfg;
   cudaStream_t s = x->stream;
   // the request list is uploaded every step (pinned staging, async): the step's host input

@@ -1,0 +1,50 @@
+"""Whole-step CUDA graphs: a run whose steps replay captured graphs must commit
+exactly the same tokens and end in exactly the same request state as the eager launch sequence.
+
+The graph switch (FOCUS_GRAPH) is read once per process, so each mode runs in its own interpreter.
+"""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+_SCRIPT = r"""
+import json, sys
+sys.path.insert(0, %(root)r)
+from paper_2601_23278_b200 import FocusContext, make_config
+from paper_2601_23278_b200.runner import generate, prefill_all
+from oracle.engine import request_prompts
+from synth import get_config
+from synth.configs import ModelConfig
+run = get_config("C1").with_(model=ModelConfig(n_layers=4, d_model=256, n_q_heads=8, n_kv_heads=2, head_dim=128,
+                             d_ff=512, vocab=97, rope_theta=1e6), n_requests=6, prompt_len=300, gen_len=32)
+ctx = FocusContext(make_config(run))
+rids = prefill_all(ctx, request_prompts(run), run.gen_len)
+generate(ctx, rids, keep_log=False)
+ctx.focus_sync()
+toks = [list(map(int, ctx.focus_get_tokens(r))) for r in rids]
+st = ctx.states()
+print(json.dumps({"tokens": toks, "steps": [int(st[r].total_steps) for r in rids],
+                  "sums": [int(st[r].token_sum) for r in rids], "launches": int(ctx.launches())}))
+"""
+
+
+def _run(graph: str):
+    env = dict(os.environ, FOCUS_GRAPH=graph)
+    out = subprocess.run([sys.executable, "-c", _SCRIPT % {"root": ROOT}], env=env, capture_output=True, text=True,
+                         timeout=600, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    return json.loads(out.stdout.strip().splitlines()[-1])
+
+
+def test_graph_replay_matches_eager():
+    eager, graph = _run("0"), _run("1")
+    assert graph["tokens"] == eager["tokens"]
+    assert graph["steps"] == eager["steps"] and graph["sums"] == eager["sums"]
+    assert graph["launches"] == eager["launches"]      # replays account the captured launches
