@@ -170,15 +170,19 @@ __device__ __forceinline__ uint32_t pack_bf2(float a, float b) {
 // `chunk(c0, v)` yields 32 consecutive fp32 accumulator columns [c0, c0+32) of this thread's row of the
 // tile (TMEM or merged split partials); it must be called uniformly by the whole warp.  row0 = the
 // warp's first tile row (this thread's row = row0 + lane), rows >= M are not written.
+// part / nparts: the tile's columns are split into nparts equal groups (of 32-column chunks, SwiGLU
+// 64-column pairs, RoPE half-head pairs) and this warp emits group `part` (two warps per TMEM lane
+// quarter share a tile when nparts = 2).
 template <int MODE, int BN, typename Chunk>
 __device__ __forceinline__ void epilogue_tile(Chunk&& chunk, int row0, int M, int nt, int N, float* __restrict__ C,
-                                              int ldc, const GemmEpi& epi, uint32_t buf) {
+                                              int ldc, const GemmEpi& epi, uint32_t buf, int part = 0,
+                                              int nparts = 1) {
   const int lane = threadIdx.x & 31;
   const int rr = lane >> 3, jj = lane & 7;              // read-back: row 4i + rr, 16-B chunk jj
   if constexpr (MODE == GEMM_STORE || MODE == GEMM_ADD) {
     const bool vec_ok = (ldc % 4) == 0 && (((uintptr_t)C) & 15) == 0;
 #pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 32) {
+    for (int c0 = part * (BN / nparts); c0 < (part + 1) * (BN / nparts); c0 += 32) {
       float v[32];
       chunk(c0, v);
 #pragma unroll
@@ -213,7 +217,7 @@ __device__ __forceinline__ void epilogue_tile(Chunk&& chunk, int row0, int M, in
     // act[row][128 nt + c] = bf16(silu(gate_c) * up_c); two 32-column groups (64 bf16 = 128 B) per staging
     static_assert(BN == 2 * kGuGroup, "gate/up interleave must match the tile");
 #pragma unroll 1
-    for (int c0 = 0; c0 < kGuGroup; c0 += 64) {
+    for (int c0 = part * (kGuGroup / nparts); c0 < (part + 1) * (kGuGroup / nparts); c0 += 64) {
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         float gv[32], uv[32];
@@ -257,14 +261,16 @@ __device__ __forceinline__ void epilogue_tile(Chunk&& chunk, int row0, int M, in
     // dependent page-table load per 16-B chunk
     const unsigned long long kv_row = row < M ? (unsigned long long)kv_offset(epi.kv, ri.slot, ri.pos, 0) : 0ull;
     const size_t kv_head_stride = (size_t)epi.kv.page_size * epi.kv.head_dim;
+    // (head, 32-column half-pair) steps of the tile, split evenly between the parts
+    constexpr int kSteps = (BN / 128) * 2;
 #pragma unroll 1
-    for (int hh = 0; hh < BN / 128; ++hh) {
+    for (int st = part * (kSteps / nparts); st < (part + 1) * (kSteps / nparts); ++st) {
+      const int hh = st >> 1, c0 = (st & 1) * 32;
       const int head = nt * (BN / 128) + hh;              // 0..Hq-1 q, then k, then v
       const bool is_v = head >= epi.n_q_heads + hkv;
       const bool is_k = !is_v && head >= epi.n_q_heads;
       const int kvh = head - epi.n_q_heads - (is_v ? hkv : 0);
-#pragma unroll 1
-      for (int c0 = 0; c0 < 64; c0 += 32) {
+      {
         float lo[32], hi[32];
         chunk(hh * 128 + c0, lo);
         chunk(hh * 128 + c0 + 64, hi);
@@ -510,7 +516,7 @@ struct GP {
   static constexpr int B_STAGE = B_ATOM * KA;
   static constexpr int STAGE_BYTES = A_STAGE + B_STAGE;
   static constexpr int STAGES = (192 * 1024) / STAGE_BYTES;
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_SMEM + 1024 + 256;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 2 * EPI_SMEM + 1024 + 256;   // + staging of warps 0-3
 };
 
 __device__ __forceinline__ void tma_load_3d_pair(void* dst, const CUtensorMap* map, uint32_t bar_cluster, int x, int y,
@@ -557,8 +563,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * G::A_STAGE;
-  const uint32_t epi_buf = smem_u32(smem + STAGES * STAGE_BYTES) + (uint32_t)(((threadIdx.x >> 5) & 3) * 32 * 128);
-  uint64_t* bars = (uint64_t*)(smem + STAGES * STAGE_BYTES + EPI_SMEM);
+  // epilogue staging: warps 4-7 use the first 16 KB, warps 0-3 (last-tile helpers) the second
+  const uint32_t epi_buf = smem_u32(smem + STAGES * STAGE_BYTES) + (uint32_t)(((threadIdx.x >> 5) & 3) * 32 * 128) +
+                           (threadIdx.x < 128 ? (uint32_t)EPI_SMEM : 0u);
+  uint64_t* bars = (uint64_t*)(smem + STAGES * STAGE_BYTES + 2 * EPI_SMEM);
   uint64_t* full = bars;                                // [STAGES]  (leader's are the live ones)
   uint64_t* empty = bars + STAGES;                      // [STAGES]  (both CTAs, by the leader's commit)
   uint64_t* tfull = bars + 2 * STAGES;                  // [2]       (both CTAs, by the leader's commit)
@@ -623,6 +631,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   // unit p >> 1; half 0 adds its partial to the residual first and raises the unit's flag, half 1
   // waits for the flag before adding its own, so the result is fl(fl(x + acc_0) + acc_1) on every run.
   const bool split2 = MODE == GEMM_ADD && (flags & 4) && !sk && 2 * units <= n_pairs && ks_n >= 4;
+  // a pair with a single data-parallel unit (the decode shapes' QKV / O / down GEMMs) emits it with 8
+  // warps: warps 0-3 are idle by then and the epilogue is not overlapped with any MMA
+  const bool joint = !sk && !split2;
+  const int n_mine = (!sk && !split2 && pair < units) ? (units - pair + n_pairs - 1) / n_pairs : 0;
   auto seg_at = [&](int i, long long& w) -> PSeg {
     PSeg g;
     if (split2) {
@@ -792,7 +804,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             for (int i = 0; i < 32; ++i) v[i] += __ldcg(pp + (size_t)i * BM);
           }
         };
-        epilogue_tile<MODE, BN>(chunk, row - lane, M, nt, N, C, ldc, epi, epi_buf);
+        const bool shared_tile = joint && n_mine == 1;
+        epilogue_tile<MODE, BN>(chunk, row - lane, M, nt, N, C, ldc, epi, epi_buf, 0, shared_tile ? 2 : 1);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(tempty_l + acc * 8);
@@ -810,6 +823,24 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
       if (threadIdx.x == 128) stamp(2);
     }
+  }
+  if (warp < 4 && joint && n_mine == 1) {
+    // warps 0-3: second column half of this pair's last unit (TMEM lane quarter = warp)
+    __syncwarp();
+    const int it = n_mine - 1, u = pair + it * n_pairs;
+    const int mp = u % m_pairs, nt = u / m_pairs;
+    const int acc = it & 1;
+    // follow every accumulator hand-off in order: a parity wait only identifies a phase while the
+    // barrier is less than two phases ahead, and these warps arrive here long before the last unit
+    for (int i = 0; i < n_mine; ++i) mbar_wait(&tfull[i & 1], (i >> 1) & 1);
+    __syncwarp();                                       // converged for the .sync.aligned TMEM loads
+    tc_fence_after();
+    const int q = warp;
+    const int row = mp * 2 * BM + (int)rank * BM + q * 32 + lane;
+    const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
+    auto chunk = [&](int c0, float* v) { tmem_ld32(taddr + c0, v); };
+    epilogue_tile<MODE, BN>(chunk, row - lane, M, nt, N, C, ldc, epi, epi_buf, 1, 2);
+    tc_fence_before();
   }
   __syncthreads();
   cluster_sync();                                       // no CTA leaves while its peer may still signal it
