@@ -181,6 +181,7 @@ struct AttnArgs {
   int tail_split;               // 1: units of the last partial round are key-split across the idle CTAs
   int l2_prefetch;              // K/V tiles past the smem rings to prefetch into L2
   int kv_hint;                  // 1: K/V tiles loaded with the L2 evict-first policy
+  int page_skip;                // 1: K/V boxes holding no key of the unit are not loaded
   int nch_fixed;                // 1: every non-causal unit runs the 64-row softmax variant (one hot copy)
   void* plan_units;             // unit table [grid][UCAP] precomputed by k_attn_plan, or nullptr
   int* plan_n;                  // [grid] units per CTA (nullptr: the kernel builds its table itself)

@@ -661,6 +661,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     a.trace[((size_t)blockIdx.x * 8 + 7) * kTraceEv + 2] = gt;
   }
   if (threadIdx.x < 64) ones[threadIdx.x] = 0x3F80;   // bf16 1.0
+  // K/V rings zeroed once: boxes past a unit's last key are not loaded, so the rows they would have
+  // filled must hold finite values (P = 0 there, and 0 * finite = 0 in the PV MMA)
+  for (int i = threadIdx.x; i < (SK + SV) * KV_BYTES / 16; i += NTHREADS)
+    reinterpret_cast<uint4*>(sK)[i] = make_uint4(0, 0, 0, 0);
   if (threadIdx.x == 0) {
     for (int i = 0; i < SK; ++i) { mbar_init(&kfull[i], 1); mbar_init(&kempty[i], 1); }
     for (int i = 0; i < SV; ++i) { mbar_init(&vfull[i], 1); mbar_init(&vempty[i], 1); }
@@ -736,9 +740,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           if (pf > 0 && t + NS + pf < x.t_hi) prefetch_tile(x, t + NS + pf);
           mbar_wait(&emptyb[slot], ((g / NS) & 1) ^ 1);
           tr.ev(1);
-          mbar_expect_tx(&fullb[slot], KV_BYTES);
+          // only the boxes that hold keys of [kbeg, kend): the tail of a unit's last tile (and the head
+          // of an importance-only tile) is not streamed; those smem rows keep finite data (the rings
+          // are zeroed at kernel start) and the softmax masks their keys (P = 0)
+          const int pc0 = a.page_skip ? max(0, (x.kbeg - t * KT) / pr) : 0;
+          const int pc1 = a.page_skip ? min(KT / pr, (x.kend - t * KT + pr - 1) / pr) : KT / pr;
+          mbar_expect_tx(&fullb[slot], (uint32_t)(pc1 - pc0) * pr * 256);
           uint8_t* dst = ring + slot * KV_BYTES;
-          for (int pc = 0; pc < KT / pr; ++pc) {
+          for (int pc = pc0; pc < pc1; ++pc) {
             const int pos = t * KT + pc * pr;
             const int pidx = min(pos / ps, a.kv.max_pages - 1);
             const int page = a.kv.page_table[(size_t)x.slot * a.kv.max_pages + pidx];
