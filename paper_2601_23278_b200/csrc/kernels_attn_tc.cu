@@ -59,15 +59,16 @@ constexpr int P_CHUNK = (KT / 8) * 128;         // 2 KB: 8 query rows x 128 keys
 constexpr int P_BYTES = (NQM / 8) * P_CHUNK;    // 16 KB
 constexpr int TMEM_COLS = 512;
 constexpr int O_COL = 0;                        // O^T buffers [0, 64), [64, 128)
-constexpr int S_COL = 2 * NQM;                  // S^T buffers [128, 192), [192, 256)
-constexpr int L_COL = 4 * NQM;                  // row-sum buffers [256, 320), [320, 384): ONES . P^T
+constexpr int NSB = 3;                          // S^T buffers: QK^T runs up to NSB tiles ahead of PV
+constexpr int S_COL = 2 * NQM;                  // S^T buffers [128, 192), [192, 256), [256, 320)
+constexpr int L_COL = (2 + NSB) * NQM;          // row-sum buffers [320, 384), [384, 448): ONES . P^T
 constexpr int MAXS = 16;                        // split partials merged through smem
 constexpr int OFF_Q = 0;
 constexpr int OFF_K = OFF_Q + 2 * Q_BYTES;
 constexpr int OFF_V = OFF_K + SK * KV_BYTES;
 constexpr int OFF_P = OFF_V + SV * KV_BYTES;
 constexpr int OFF_BAR = OFF_P + 2 * P_BYTES;
-constexpr int N_BARS = 2 * SK + 2 * SV + 2 * 9;
+constexpr int N_BARS = 2 * SK + 2 * SV + 2 * 9 + 2 * (NSB - 2);
 constexpr int OFF_MISC = OFF_BAR + 8 * N_BARS + 16;
 constexpr int OFF_M = OFF_MISC;                 // float [NQM] running max (log2 units)
 constexpr int OFF_ALPHA = OFF_M + NQM * 4;      // float [NQM]
@@ -221,8 +222,8 @@ __device__ __forceinline__ void softmax_unit(const AttnArgs& a, const Unit& xr, 
   }
   named_bar(1, 128);
   for (int t = xr.t_lo; t < xr.t_hi; ++t, ++g) {
-    const uint32_t sb = g & 1, pb = g & 1;
-    mbar_wait(&ss.sfull[sb], (g >> 1) & 1);
+    const uint32_t sb = g % NSB, pb = g & 1;
+    mbar_wait(&ss.sfull[sb], (g / NSB) & 1);
     tr.ev(1);
     tc_fence_after();
     const int k = t * KT + L;
@@ -625,9 +626,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   uint64_t* vempty = vfull + SV;           // [SV]
   uint64_t* qfull = vempty + SV;           // [2]
   uint64_t* qempty = qfull + 2;            // [2]
-  uint64_t* sfull = qempty + 2;            // [2]
-  uint64_t* sfree = sfull + 2;             // [2]  (4 softmax warps)
-  uint64_t* pfull = sfree + 2;             // [2]  (4 softmax warps)
+  uint64_t* sfull = qempty + 2;            // [NSB]
+  uint64_t* sfree = sfull + NSB;           // [NSB]  (4 softmax warps)
+  uint64_t* pfull = sfree + NSB;           // [2]  (4 softmax warps)
   uint64_t* pvdone = pfull + 2;            // [2]
   uint64_t* ofull = pvdone + 2;            // [2]
   uint64_t* ofree = ofull + 2;             // [2]  (4 epilogue warps)
@@ -668,9 +669,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   if (threadIdx.x == 0) {
     for (int i = 0; i < SK; ++i) { mbar_init(&kfull[i], 1); mbar_init(&kempty[i], 1); }
     for (int i = 0; i < SV; ++i) { mbar_init(&vfull[i], 1); mbar_init(&vempty[i], 1); }
+    for (int i = 0; i < NSB; ++i) { mbar_init(&sfull[i], 1); mbar_init(&sfree[i], 4); }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&qfull[i], 1); mbar_init(&qempty[i], 1);
-      mbar_init(&sfull[i], 1); mbar_init(&sfree[i], 4);
       mbar_init(&pfull[i], 4); mbar_init(&pvdone[i], 1);
       mbar_init(&ofull[i], 1); mbar_init(&ofree[i], 4);
       mbar_init(&statfull[i], 4);
@@ -781,9 +782,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           mbar_wait(&qfull[ob], (qu >> 1) & 1);
           tr.ev(2);
         }
-        const uint32_t ks = qg % SK, sb = qg & 1;
+        const uint32_t ks = qg % SK, sb = qg % NSB;
         mbar_wait(&kfull[ks], (qg / SK) & 1);
-        mbar_wait(&sfree[sb], ((qg >> 1) & 1) ^ 1);
+        tr.ev(3);
+        mbar_wait(&sfree[sb], ((qg / NSB) & 1) ^ 1);
+        tr.ev(4);
         tc_fence_after();
         const int NQ = (x.nq + 15) & ~15;
         const uint32_t idesc_qk = idesc_bf16(KT, NQ, false, false);
@@ -816,6 +819,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         if (first) mbar_wait(&ofree[ob], ((pu >> 1) & 1) ^ 1);
         const uint32_t vs = pg % SV;
         mbar_wait(&vfull[vs], (pg / SV) & 1);
+        tr.ev(6);
         tc_fence_after();
         const uint32_t dO = tmem + O_COL + ob * NQM;
         const uint32_t dl = tmem + L_COL + ob * NQM;
@@ -839,7 +843,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       tr.ev(0);
       if (!IMP_ONLY) {
         while (pu < n_my) {
-          while (qk_ready() && qg < pg + 2) issue_qk();
+          while (qk_ready() && qg < pg + NSB) issue_qk();
           issue_pv();
         }
       } else {
