@@ -1089,7 +1089,12 @@ bool launch_gemm_tc(const bf16* A, int lda, int a_rows, const bf16* W, int N, in
       s2_env = (e && e[0] == '0') ? 0 : 1;
     }
     // (measured at M = 428: down, K = 12288, 57 -> 53 us; O, K = 4096, 29 -> 33 us, so only for deep K)
-    if (s2_env && mode == GEMM_ADD && 2 * units256 <= num_sms() / 2 && K >= 8192 && K % (2 * BK) == 0 && ka_env == 0)
+    static int s2_mink = -1;
+    if (s2_mink < 0) {
+      const char* e = getenv("FOCUS_GEMM_SPLIT2_MINK");
+      s2_mink = e ? std::max(256, atoi(e)) : 8192;
+    }
+    if (s2_env && mode == GEMM_ADD && 2 * units256 <= num_sms() / 2 && K >= s2_mink && K % (2 * BK) == 0 && ka_env == 0)
       return launch_pair<256, 1>(A, lda, a_rows, W, N, K, C, ldc, M_dev, M_max, mode, ws, s, epi, m, true);
     if (ka == 2 && K % (2 * BK) == 0) {
       if (narrow2) return launch_pair<128, 2>(A, lda, a_rows, W, N, K, C, ldc, M_dev, M_max, mode, ws, s, epi, m);
