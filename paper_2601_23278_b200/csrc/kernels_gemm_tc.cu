@@ -556,7 +556,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 float* __restrict__ ws, int* __restrict__ sem, int flags) {
   const int sk = flags & 1;                             // bit 0: stream-K schedule
   const bool hints = (flags & 2) != 0;                  // bit 1: L2 hints (weights evict-first, activations evict-last)
-  const int epoch = flags >> 3;                         // bits 3..: launch epoch of the ordered split-K flags
+  const int nsplit = ((flags >> 3) & 3) + 1;            // bits 3-4: k-ranges per unit (ordered split-K)
+  const int epoch = flags >> 5;                         // bits 5..: launch epoch of the ordered split-K flags
   using G = GP<BN, KA>;
   constexpr int STAGES = G::STAGES, STAGE_BYTES = G::STAGE_BYTES;
   extern __shared__ uint8_t smem_raw[];
@@ -630,7 +631,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   // Ordered split-K (flags bit 2, GEMM_ADD, one wave): pair p computes half p & 1 of the k-blocks of
   // unit p >> 1; half 0 adds its partial to the residual first and raises the unit's flag, half 1
   // waits for the flag before adding its own, so the result is fl(fl(x + acc_0) + acc_1) on every run.
-  const bool split2 = MODE == GEMM_ADD && (flags & 4) && !sk && 2 * units <= n_pairs && ks_n >= 4;
+  const bool split2 = MODE == GEMM_ADD && (flags & 4) && !sk && nsplit * units <= n_pairs && ks_n >= 4 * nsplit;
+  // k-range boundaries of the ordered split: range h = [kb(h), kb(h + 1)); every range but the last
+  // gives up ks_n / 32 k-blocks to the last, so the adds of the earlier ranges overlap its tail
+  auto kb = [&](int h) { return h == 0 ? 0 : h == nsplit ? ks_n : h * ks_n / nsplit - ks_n / 32 * h / (nsplit - 1); };
   // a pair with a single data-parallel unit (the decode shapes' QKV / O / down GEMMs) emits it with 8
   // warps: warps 0-3 are idle by then and the epilogue is not overlapped with any MMA
   const bool joint = !sk && !split2;
@@ -638,11 +642,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   auto seg_at = [&](int i, long long& w) -> PSeg {
     PSeg g;
     if (split2) {
-      // half 0 takes ks_n / 32 fewer k-blocks: its residual add then overlaps half 1's last k-blocks
-      const int h0 = ks_n / 2 - ks_n / 32;
-      g.u = i == 0 ? pair >> 1 : units;
-      g.k0 = (pair & 1) ? h0 : 0;
-      g.k1 = (pair & 1) ? ks_n : h0;
+      g.u = i == 0 ? pair / nsplit : units;
+      g.k0 = kb(pair % nsplit);
+      g.k1 = kb(pair % nsplit + 1);
       return g;
     }
     if (!sk) { g.u = pair + i * n_pairs; g.k0 = 0; g.k1 = ks_n; return g; }
@@ -775,12 +777,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         // pair+1 .. owner(last stage of the unit), same CTA rank), in pair order
         const int q1 = (g.k1 < ks_n && !split2) ? owner((long long)(g.u + 1) * ks_n - 1) : pair;
         int* sflag = sem + 2048 + 2 * g.u + (int)rank;   // ordered split-K flag of this unit's rows
-        if (split2 && g.k0 > 0) {                        // half 1: half 0 has added its partial
+        const int hsplit = split2 ? pair % nsplit : 0;
+        if (split2 && hsplit > 0) {                      // range h: ranges 0..h-1 have added theirs
           if (threadIdx.x == 128) {
             int f = 0;
             do {
               asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(f) : "l"(sflag) : "memory");
-            } while (f != epoch);
+            } while (f != epoch * 4 + hsplit);
           }
           named_bar(1, 128);
         }
@@ -809,10 +812,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(tempty_l + acc * 8);
-        if (split2 && g.k0 == 0) {                       // half 0: residual updated -> release the flag
+        if (split2 && hsplit < nsplit - 1) {             // residual updated -> release the next range
           __threadfence();
           named_bar(1, 128);
-          if (threadIdx.x == 128) asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(sflag), "r"(epoch) : "memory");
+          if (threadIdx.x == 128)
+            asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(sflag), "r"(epoch * 4 + hsplit + 1) : "memory");
         }
         if (q1 > pair) {
           named_bar(1, 128);                             // every thread has read the partials
@@ -1000,7 +1004,7 @@ static void launch_pair_k(int grid, cudaStream_t s, const CUtensorMap& ma, const
 template <int BN, int KA>
 static bool launch_pair(const bf16* A, int lda, int a_rows, const bf16* W, int N, int K, float* C, int ldc,
                         const int* M_dev, int M_max, GemmMode mode, const GemmWs& ws, cudaStream_t s, const GemmEpi* epi,
-                        int m, bool split2 = false) {
+                        int m, int split = 1) {
   using namespace tc;
   if ((mode == GEMM_SWIGLU || mode == GEMM_QKV_ROPE) && (!epi || N % BN)) return false;
   if (mode == GEMM_SWIGLU && BN != 2 * kGuGroup) return false;
@@ -1019,10 +1023,10 @@ static bool launch_pair(const bf16* A, int lda, int a_rows, const bf16* W, int N
   if (ws.ptr == nullptr || ws.sem == nullptr || ws.sem_count < (size_t)2 * np ||
       ws.bytes < (size_t)2 * np * BM * BN * sizeof(float))
     sk = 0;
-  const bool split2_ok = split2 && mode == GEMM_ADD && !sk && ws.sem != nullptr && ws.sem_count >= 2048 + 2 * (size_t)np &&
-                         (K / (BK * KA)) % 2 == 0 && 2 * units <= np;
+  const bool split2_ok = split > 1 && mode == GEMM_ADD && !sk && ws.sem != nullptr &&
+                         ws.sem_count >= 2048 + 2 * (size_t)np && split * units <= np;
   const int grid = sk ? 2 * np
-                      : (int)std::max<long long>(2, std::min<long long>(np, split2_ok ? 2 * units : units) * 2);
+                      : (int)std::max<long long>(2, std::min<long long>(np, split2_ok ? split * units : units) * 2);
   const GemmEpi e = epi ? *epi : GemmEpi{};
   static int pf_on = -1;
   if (pf_on < 0) {
@@ -1039,8 +1043,8 @@ static bool launch_pair(const bf16* A, int lda, int a_rows, const bf16* W, int N
   // GEMM_ADD, 256-wide tiles, one wave even with two k-halves per unit: ordered split-K (see kernel)
   if (split2_ok) {
     static unsigned epoch = 0;
-    epoch = epoch % 0xFFFFFFu + 1;
-    sk |= 4 | (int)(epoch << 3);
+    epoch = epoch % 0xFFFFFu + 1;                      // flag values epoch * 4 + h stay below 2^22
+    sk |= 4 | ((split - 1) << 3) | (int)(epoch << 5);
   }
 
   switch (mode) {
@@ -1094,8 +1098,20 @@ bool launch_gemm_tc(const bf16* A, int lda, int a_rows, const bf16* W, int N, in
       const char* e = getenv("FOCUS_GEMM_SPLIT2_MINK");
       s2_mink = e ? std::max(256, atoi(e)) : 8192;
     }
-    if (s2_env && mode == GEMM_ADD && 2 * units256 <= num_sms() / 2 && K >= s2_mink && K % (2 * BK) == 0 && ka_env == 0)
-      return launch_pair<256, 1>(A, lda, a_rows, W, N, K, C, ldc, M_dev, M_max, mode, ws, s, epi, m, true);
+    // ordered split into S k-ranges (at least 8 k-blocks each, S units in one wave): two ranges for deep
+    // K at the C3 shapes.  S up to 4 (FOCUS_GEMM_SPLIT_MAX) was measured slower on the C2 shapes (O
+    // 0.53 -> 0.93 ms/step: the ordered chain of residual adds costs more than the extra SMs give)
+    static int s_cap = -1;
+    if (s_cap < 0) {
+      const char* e = getenv("FOCUS_GEMM_SPLIT_MAX");
+      s_cap = e ? std::max(2, std::min(4, atoi(e))) : 2;
+    }
+    if (s2_env && mode == GEMM_ADD && ka_env == 0) {
+      const int ks_n = K / BK;
+      const int smax = (int)std::min<long long>(s_cap, std::min<long long>((num_sms() / 2) / std::max<long long>(1, units256), ks_n / 8));
+      if (smax >= 3 || (smax == 2 && K >= s2_mink))
+        return launch_pair<256, 1>(A, lda, a_rows, W, N, K, C, ldc, M_dev, M_max, mode, ws, s, epi, m, smax);
+    }
     if (ka == 2 && K % (2 * BK) == 0) {
       if (narrow2) return launch_pair<128, 2>(A, lda, a_rows, W, N, K, C, ldc, M_dev, M_max, mode, ws, s, epi, m);
       return launch_pair<256, 2>(A, lda, a_rows, W, N, K, C, ldc, M_dev, M_max, mode, ws, s, epi, m);
