@@ -626,12 +626,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const long long w_lo = sk ? (long long)pair * W / n_pairs : 0, w_hi = sk ? (long long)(pair + 1) * W / n_pairs : 0;
   auto owner = [&](long long x) { return (int)(((x + 1) * n_pairs + W - 1) / W) - 1; };
   auto empty_range = [&](int qq) { return (long long)qq * W / n_pairs == (long long)(qq + 1) * W / n_pairs; };
-  struct PSeg { int u, k0, k1; };
+  struct PSeg { int u, k0, k1, h; };
   // segment i of this pair (valid while the returned u < units)
   // Ordered split-K (flags bit 2, GEMM_ADD, one wave): pair p computes half p & 1 of the k-blocks of
   // unit p >> 1; half 0 adds its partial to the residual first and raises the unit's flag, half 1
   // waits for the flag before adding its own, so the result is fl(fl(x + acc_0) + acc_1) on every run.
-  const bool split2 = MODE == GEMM_ADD && (flags & 4) && !sk && nsplit * units <= n_pairs && ks_n >= 4 * nsplit;
+  // (the split depends only on the GEMM's shape, never on the live row count, so every row's result
+  // is the same whatever the batch: the ordered ranges are data-parallel segments (unit, range) in
+  // increasing order, and a range only waits on the previous range of its unit, a smaller segment,
+  // so the persistent pairs cannot deadlock)
+  const bool split2 = MODE == GEMM_ADD && (flags & 4) && !sk && ks_n >= 4 * nsplit;
   // k-range boundaries of the ordered split: range h = [kb(h), kb(h + 1)); every range but the last
   // gives up ks_n / 32 k-blocks to the last, so the adds of the earlier ranges overlap its tail
   auto kb = [&](int h) { return h == 0 ? 0 : h == nsplit ? ks_n : h * ks_n / nsplit - ks_n / 32 * h / (nsplit - 1); };
@@ -641,10 +645,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const int n_mine = (!sk && !split2 && pair < units) ? (units - pair + n_pairs - 1) / n_pairs : 0;
   auto seg_at = [&](int i, long long& w) -> PSeg {
     PSeg g;
+    g.h = 0;
     if (split2) {
-      g.u = i == 0 ? pair / nsplit : units;
-      g.k0 = kb(pair % nsplit);
-      g.k1 = kb(pair % nsplit + 1);
+      const int j = pair + i * n_pairs;
+      if (j >= nsplit * units) { g.u = units; g.k0 = g.k1 = 0; return g; }
+      g.u = j / nsplit;
+      g.h = j % nsplit;
+      g.k0 = kb(g.h);
+      g.k1 = kb(g.h + 1);
       return g;
     }
     if (!sk) { g.u = pair + i * n_pairs; g.k0 = 0; g.k1 = ks_n; return g; }
@@ -777,7 +785,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         // pair+1 .. owner(last stage of the unit), same CTA rank), in pair order
         const int q1 = (g.k1 < ks_n && !split2) ? owner((long long)(g.u + 1) * ks_n - 1) : pair;
         int* sflag = sem + 2048 + 2 * g.u + (int)rank;   // ordered split-K flag of this unit's rows
-        const int hsplit = split2 ? pair % nsplit : 0;
+        const int hsplit = split2 ? g.h : 0;
         if (split2 && hsplit > 0) {                      // range h: ranges 0..h-1 have added theirs
           if (threadIdx.x == 128) {
             int f = 0;
@@ -1024,7 +1032,7 @@ static bool launch_pair(const bf16* A, int lda, int a_rows, const bf16* W, int N
       ws.bytes < (size_t)2 * np * BM * BN * sizeof(float))
     sk = 0;
   const bool split2_ok = split > 1 && mode == GEMM_ADD && !sk && ws.sem != nullptr &&
-                         ws.sem_count >= 2048 + 2 * (size_t)np && split * units <= np;
+                         ws.sem_count >= 2048 + 2 * ((size_t)M_max + 2 * BM - 1) / (2 * BM) * ((N + BN - 1) / BN);
   const int grid = sk ? 2 * np
                       : (int)std::max<long long>(2, std::min<long long>(np, split2_ok ? split * units : units) * 2);
   const GemmEpi e = epi ? *epi : GemmEpi{};
@@ -1106,11 +1114,12 @@ bool launch_gemm_tc(const bf16* A, int lda, int a_rows, const bf16* W, int N, in
       const char* e = getenv("FOCUS_GEMM_SPLIT_MAX");
       s_cap = e ? std::max(2, std::min(4, atoi(e))) : 2;
     }
-    if (s2_env && mode == GEMM_ADD && ka_env == 0) {
+    // the decision uses the GEMM's shape only (K >= FOCUS_GEMM_SPLIT2_MINK), never the row count, so
+    // results are batch invariant
+    if (s2_env && mode == GEMM_ADD && ka_env == 0 && K >= s2_mink) {
       const int ks_n = K / BK;
-      const int smax = (int)std::min<long long>(s_cap, std::min<long long>((num_sms() / 2) / std::max<long long>(1, units256), ks_n / 8));
-      if (smax >= 3 || (smax == 2 && K >= s2_mink))
-        return launch_pair<256, 1>(A, lda, a_rows, W, N, K, C, ldc, M_dev, M_max, mode, ws, s, epi, m, smax);
+      const int sp = std::min(s_cap, ks_n / 8);
+      if (sp >= 2) return launch_pair<256, 1>(A, lda, a_rows, W, N, K, C, ldc, M_dev, M_max, mode, ws, s, epi, m, sp);
     }
     if (ka == 2 && K % (2 * BK) == 0) {
       if (narrow2) return launch_pair<128, 2>(A, lda, a_rows, W, N, K, C, ldc, M_dev, M_max, mode, ws, s, epi, m);

@@ -48,3 +48,19 @@ def test_graph_replay_matches_eager():
     assert graph["tokens"] == eager["tokens"]
     assert graph["steps"] == eager["steps"] and graph["sums"] == eager["sums"]
     assert graph["launches"] == eager["launches"]      # replays account the captured launches
+
+
+def _full_run(graph: str):
+    env = dict(os.environ, FOCUS_GRAPH=graph)
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "full_run_check.py"), "C3"], env=env,
+                         capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = out.stdout.strip().splitlines()[-1]
+    assert "32768 tokens" in line, line                 # every request reached its 512th token
+    return line.split("digest ")[1]
+
+
+def test_c3_full_run_graph_matches_eager():
+    """BASELINE config C3 at full size (64 requests x 512 tokens, 544 steps): the graph-replayed run and
+    the eager run commit identical tokens (tile shapes baked into a graph never change a result)."""
+    assert _full_run("1") == _full_run("0")

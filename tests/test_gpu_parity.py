@@ -153,7 +153,12 @@ def test_resynced_rules_bit_exact(B, nreq, prompt, model):
         assert ctx.focus_get_tokens(r) == outputs[r]
 
 
-@pytest.mark.parametrize("model", [GQA_TINY, GQA_TC], ids=["simt", "tc"])
+# d_ff = 8192: the down projection (K = 8192) takes the ordered split-K path of the GEMM
+GQA_TC_DEEPFF = ModelConfig(n_layers=3, d_model=256, n_q_heads=8, n_kv_heads=2, head_dim=128, d_ff=8192, vocab=61,
+                            rope_theta=1e6)
+
+
+@pytest.mark.parametrize("model", [GQA_TINY, GQA_TC, GQA_TC_DEEPFF], ids=["simt", "tc", "tc_splitk"])
 def test_determinism_and_batch_invariance(model):
     from paper_2601_23278_b200.runner import generate, prefill_all
     run = get_config("C1").with_(model=model, method=MethodConfig(block_size=8), n_requests=5, gen_len=16)
