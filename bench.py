@@ -42,24 +42,44 @@ class Clocks:
          "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, gpu: int):
-        self.gpu, self.p = gpu, None
+        self.gpu, self.p, self.lines, self.th = gpu, None, [], None
+        self.t0 = self.t1 = 0.0
+
+    def _reader(self):
+        for line in self.p.stdout:
+            self.lines.append((time.time(), line))
 
     def __enter__(self):
+        # the sampler is started and its first sample awaited BEFORE the timed region begins (nvidia-smi
+        # takes a few hundred ms to start, longer than a short timed region); samples are time-stamped
+        # on arrival and the summary keeps those that fall inside the region
+        import threading
         try:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + self.Q, "--format=csv,noheader,nounits",
                                        "-lms", "25"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._reader, daemon=True)
+            self.th.start()
+            deadline = time.time() + 10.0
+            while not self.lines and time.time() < deadline and self.p.poll() is None:
+                time.sleep(0.01)
         except Exception:
             self.p = None
+        self.t0 = time.time()
         return self
 
     def __exit__(self, *a):
-        self.out = ""
+        self.t1 = time.time()
+        time.sleep(0.06)                                 # let the in-flight sample arrive
         if self.p is not None:
             self.p.terminate()
             try:
-                self.out, _ = self.p.communicate(timeout=5)
+                self.p.wait(timeout=5)
             except Exception:
-                self.out = ""
+                pass
+            if self.th is not None:
+                self.th.join(timeout=2)
+        inside = [ln for (t, ln) in self.lines if self.t0 - 0.03 <= t <= self.t1 + 0.03]
+        self.out = "".join(inside)
 
     def summary(self):
         rows = [r.split(",") for r in (self.out or "").strip().splitlines() if r.count(",") >= 7]
