@@ -74,6 +74,13 @@ typedef struct {
   int64_t kv_pages;        /* pages in the pool; 0 = max_requests * ceil(max_seq_len/page_size) */
   uint64_t weight_seed;    /* synthetic weights: counter hash of (seed, tensor, index)         */
   int32_t debug_taps;      /* 1 = reserve per-layer tap buffers for focus_debug_export         */
+  float logit_scale;       /* synthetic LM-head scale: W_lm = logit_scale * (recipe weights), so
+                              z = logit_scale * z_1 exactly.  A power of two in [2^-16, 2^16]
+                              (keeps W_lm exact in bf16); 0 means 1.  Sets the confidence regime
+                              of random weights: at 1 the max softmax probability over V = 151936
+                              stays far below tau (one fallback decode per step);
+                              larger scales make conf >= tau fire for several
+                              positions per step ("calibrated" run).  FOCUS_ERR_CONFIG otherwise. */
 } focus_config;
 
 typedef struct focus_ctx focus_ctx;

@@ -22,7 +22,7 @@ from __future__ import annotations
 import numpy as np
 
 from synth.configs import ModelConfig
-from synth.gen import (TID_EMBED, TID_LMHEAD, layer_tid, weight_matrix)
+from synth.gen import (TID_EMBED, TID_LMHEAD, layer_tid, logit_scale_log2, weight_matrix)
 
 from .numerics import attend, bf16_round, f32, rms_norm, rope, silu
 
@@ -67,7 +67,9 @@ class OracleWeights:
         if self._lm is not None:
             return self._lm
         c = self.cfg
-        lm = weight_matrix(TID_LMHEAD, c.vocab, c.d_model, c.d_model, self.seed).astype(np.float64)
+        # W_lm = logit_scale * recipe weights (a power of two: exact; focus_config::logit_scale)
+        lm = weight_matrix(TID_LMHEAD, c.vocab, c.d_model, c.d_model, self.seed,
+                           exp_offset=logit_scale_log2(c.logit_scale)).astype(np.float64)
         if self.cache:
             self._lm = lm
         return lm

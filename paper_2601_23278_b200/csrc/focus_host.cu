@@ -98,7 +98,15 @@ struct focus_ctx {
   TokConf* tokconf = nullptr;
   focus_commit_result* res_dev = nullptr;
   GemmWs gws{};
-  Counters* cnt_host = nullptr;   // pinned mirror of the device counters (previous step)
+  // pinned 2-slot ring of the device counters: step n copies its counters into slot n % 2 (after the
+  // step, outside any graph) and records cnt_ev[n % 2]; step n + 2 waits for that event and uses them
+  // as its tile-shape estimates.  The estimate of every step is thus a deterministic function of the
+  // computation (never of how far the host runs ahead), and the host stays at most ~2 steps ahead.
+  Counters* cnt_host = nullptr;
+  cudaEvent_t cnt_ev[2] = {};
+  bool cnt_valid[2] = {false, false};
+  uint64_t step_no = 0;
+  Counters est{};                 // this step's estimate (set by focus_step_block)
   void* taps[kTapCount] = {};
   size_t tap_bytes[kTapCount] = {};
   // host state
@@ -159,7 +167,20 @@ bool valid_config(const focus_config& c) {
   const int G = c.n_q_heads / c.n_kv_heads;
   if (G > kAttnQRows) return false;
   if ((c.n_q_heads * c.head_dim) % 64) return false;
+  if (c.logit_scale != 0.f) {                     // a power of two in [2^-16, 2^16] (W_lm stays exact)
+    int e = 0;
+    const float m = std::frexp(c.logit_scale, &e);
+    if (!(m == 0.5f) || e < -15 || e > 17) return false;
+  }
   return true;
+}
+
+// log2 of the LM-head scale (focus_config::logit_scale; 0 = 1)
+int logit_scale_log2(const focus_config& c) {
+  if (c.logit_scale == 0.f) return 0;
+  int e = 0;
+  std::frexp(c.logit_scale, &e);
+  return e - 1;
 }
 
 // Carve (or, with base == nullptr, size) the arena.  Returns bytes used.
@@ -523,8 +544,9 @@ focus_status focus_init(const focus_config* cfg, void* dev_arena, size_t arena_b
   // pinned staging ring
   x->up.cap = Upload::kSlots * 65536;
   if (cudaMallocHost(&x->up.host, x->up.cap) != cudaSuccess) { delete x; return FOCUS_ERR_CUDA; }
-  if (cudaMallocHost(&x->cnt_host, sizeof(Counters)) != cudaSuccess) { cudaFreeHost(x->up.host); delete x; return FOCUS_ERR_CUDA; }
-  std::memset(x->cnt_host, 0, sizeof(Counters));
+  if (cudaMallocHost(&x->cnt_host, 2 * sizeof(Counters)) != cudaSuccess) { cudaFreeHost(x->up.host); delete x; return FOCUS_ERR_CUDA; }
+  std::memset(x->cnt_host, 0, 2 * sizeof(Counters));
+  for (int i = 0; i < 2; ++i) cudaEventCreateWithFlags(&x->cnt_ev[i], cudaEventDisableTiming);
   for (int i = 0; i < Upload::kSlots; ++i) {
     cudaEventCreateWithFlags(&x->up.ev[i], cudaEventDisableTiming);
     cudaEventRecord(x->up.ev[i], s);
@@ -533,7 +555,7 @@ focus_status focus_init(const focus_config* cfg, void* dev_arena, size_t arena_b
   const uint64_t seed = c.weight_seed;
   const int d = c.d_model, ff = c.d_ff, qd = x->q_dim, kd = c.n_kv_heads * c.head_dim;
   launch_init_weights(x->E, c.vocab, d, 1, seed, weight_exp(d), 0, 0, s);
-  launch_init_weights(x->Wlm, c.vocab, d, 2, seed, weight_exp(d), 0, 0, s);
+  launch_init_weights(x->Wlm, c.vocab, d, 2, seed, weight_exp(d) + logit_scale_log2(c), 0, 0, s);
   for (int l = 0; l < c.n_layers; ++l) {
     const uint64_t t0 = 16ull * (l + 1);
     launch_init_weights(x->Wqkv[l], qd, d, t0 + 0, seed, weight_exp(d), 0, 0, s);
@@ -604,6 +626,7 @@ focus_status focus_destroy(focus_ctx* x) {
   cudaStreamSynchronize(x->stream);
   for (int i = 0; i < Upload::kSlots; ++i) cudaEventDestroy(x->up.ev[i]);
   for (cudaEvent_t e : x->prof_events) cudaEventDestroy(e);
+  for (int i = 0; i < 2; ++i) cudaEventDestroy(x->cnt_ev[i]);
   for (auto& g : x->graphs) {
     cudaGraphExecDestroy(g.exec);
     cudaFreeHost(g.list_host);
@@ -704,6 +727,7 @@ static focus_status check_list(focus_ctx* x, const int32_t* ids, int32_t n) {
 }
 
 static focus_status enqueue_step(focus_ctx* x, const int32_t* ids, int32_t n_req);
+static focus_status step_graph(focus_ctx* x, const int32_t* ids, int32_t n_req, bool same_list);
 
 static bool graphs_enabled(const focus_ctx* x) {
   static int env = -1;
@@ -723,22 +747,42 @@ focus_status focus_step_block(focus_ctx* x, const int32_t* ids, int32_t n_req) {
   x->pending_list.assign(ids, ids + n_req);
   x->step_pending = true;
   if (n_req == 0) return FOCUS_OK;
-  if (!graphs_enabled(x)) return enqueue_step(x, ids, n_req);
-  // graph key: the request list and the tile-shape estimate (last step's live row counts, 64-row
-  // buckets) that the launch sequence bakes in; device-side sizes keep any replay exact
+  // tile-shape estimate: the live row counts of the step before the previous one (see cnt_ev), in
+  // units of 256-row CTA-pair tiles -- the only granularity the GEMM launch shapes depend on
   const int maxP = n_req * x->B;
-  Counters est = *x->cnt_host;
-  if (est.M_P <= 0 || est.M_P > maxP) { est.M_P = maxP; est.M_S = maxP; est.M_L = maxP; }
-  const int bucket[3] = {est.M_P / 64, est.M_S / 64, est.M_L / 64};
+  {
+    const int slot = (int)(x->step_no & 1);
+    Counters e{};
+    if (x->cnt_valid[slot]) {
+      cudaEventSynchronize(x->cnt_ev[slot]);
+      e = x->cnt_host[slot];
+    }
+    if (e.M_P <= 0 || e.M_P > maxP) { e.M_P = maxP; e.M_S = maxP; e.M_L = maxP; }
+    e.M_S = std::min(std::max(e.M_S, 1), maxP);
+    e.M_L = std::min(std::max(e.M_L, 1), maxP);
+    x->est = e;
+  }
+  focus_status st = FOCUS_OK;
+  if (!graphs_enabled(x)) st = enqueue_step(x, ids, n_req);
+  else st = step_graph(x, ids, n_req, same_list);
+  if (st != FOCUS_OK) return st;
+  const int slot = (int)(x->step_no & 1);
+  cudaMemcpyAsync(x->cnt_host + slot, x->cnt, sizeof(Counters), cudaMemcpyDeviceToHost, x->stream);
+  cudaEventRecord(x->cnt_ev[slot], x->stream);
+  x->cnt_valid[slot] = true;
+  ++x->step_no;
+  return cuda_status(cudaGetLastError());
+}
+
+static focus_status step_graph(focus_ctx* x, const int32_t* ids, int32_t n_req, bool same_list) {
+  focus_status rc;
+  // graph key: the request list and the tile-shape estimate the launch sequence bakes in (the number
+  // of 256-row tiles of the P, S and logit rows); device-side sizes keep any replay exact
+  const int bucket[3] = {(x->est.M_P + 255) / 256, (x->est.M_S + 255) / 256, (x->est.M_L + 255) / 256};
   ++x->graph_clock;
-  // a graph of this list whose estimates are all within one bucket is replayed (so the step-to-step
-  // jitter of the live row counts does not re-capture); block-start / flush steps, whose row counts
-  // differ a lot, get graphs of their own (up to 8 graphs, least recently used evicted)
   for (auto& g : x->graphs) {
     if (g.list.size() != (size_t)n_req || !std::equal(ids, ids + n_req, g.list.begin())) continue;
-    bool near = true;
-    for (int k = 0; k < 3; ++k) near = near && std::abs(g.bucket[k] - bucket[k]) < 2;
-    if (!near) continue;
+    if (g.bucket[0] != bucket[0] || g.bucket[1] != bucket[1] || g.bucket[2] != bucket[2]) continue;
     g.last_use = x->graph_clock;
     x->launches += g.launches;
     x->last_list = x->pending_list;
@@ -780,7 +824,7 @@ focus_status focus_step_block(focus_ctx* x, const int32_t* ids, int32_t n_req) {
   }
   g.launches = x->launches - l0;
   g.last_use = x->graph_clock;
-  if (x->graphs.size() >= 8) {   // keep the 8 most recently used
+  if (x->graphs.size() >= 32) {   // keep the 32 most recently used
     auto lru = std::min_element(x->graphs.begin(), x->graphs.end(),
                                 [](const focus_ctx::StepGraph& a, const focus_ctx::StepGraph& b) { return a.last_use < b.last_use; });
     cudaGraphExecDestroy(lru->exec);
@@ -805,9 +849,7 @@ static focus_status enqueue_step(focus_ctx* x, const int32_t* ids, int32_t n_req
   const int* MS = &x->cnt->M_S;
   const int* ML = &x->cnt->M_L;
   LAUNCH(EMBED, launch_embed(x->tokP, MP, maxP, x->E, c.d_model, x->x, s));
-  // last step's live sizes (async pinned copy) as tile-shape estimates; the first step uses the maxima
-  Counters est = *x->cnt_host;
-  if (est.M_P <= 0 || est.M_P > maxP) { est.M_P = maxP; est.M_S = maxP; est.M_L = maxP; }
+  const Counters& est = x->est;   // tile-shape estimates (focus_step_block)
   RowSpace rsP{MP, maxP, x->rowP, est.M_P, x->ropeT_P};
   RowSpace rsS{MS, maxP, x->rowS, est.M_S, x->ropeT_S};
   if (fused_qkv(x))
@@ -892,7 +934,6 @@ static focus_status enqueue_step(focus_ctx* x, const int32_t* ids, int32_t n_req
   LAUNCH(GEMM_LM, launch_gemm(x->h, c.d_model, x->max_rows, x->Wlm, c.vocab, c.d_model, x->logits, c.vocab, ML, maxP,
                               GEMM_STORE, x->gws, s, est.M_L));
   LAUNCH(VOCAB, launch_vocab_reduce(x->logits, ML, maxP, c.vocab, x->mask_id, x->nch_vocab, x->vpart, s));
-  cudaMemcpyAsync(x->cnt_host, x->cnt, sizeof(Counters), cudaMemcpyDeviceToHost, s);   // next step's estimates
   return cuda_status(cudaGetLastError());
 }
 

@@ -557,7 +557,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const int sk = flags & 1;                             // bit 0: stream-K schedule
   const bool hints = (flags & 2) != 0;                  // bit 1: L2 hints (weights evict-first, activations evict-last)
   const int nsplit = ((flags >> 3) & 3) + 1;            // bits 3-4: k-ranges per unit (ordered split-K)
-  const int epoch = flags >> 5;                         // bits 5..: launch epoch of the ordered split-K flags
   using G = GP<BN, KA>;
   constexpr int STAGES = G::STAGES, STAGE_BYTES = G::STAGE_BYTES;
   extern __shared__ uint8_t smem_raw[];
@@ -791,7 +790,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             int f = 0;
             do {
               asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(f) : "l"(sflag) : "memory");
-            } while (f != epoch * 4 + hsplit);
+            } while (f != hsplit);
+            // the flags re-arm themselves: the last range is the flag's last reader in this launch, so
+            // every launch (and every replay of a captured graph) starts from 0 whatever units an
+            // earlier launch of a different row count touched
+            if (hsplit == nsplit - 1) *(volatile int*)sflag = 0;
           }
           named_bar(1, 128);
         }
@@ -824,7 +827,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           __threadfence();
           named_bar(1, 128);
           if (threadIdx.x == 128)
-            asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(sflag), "r"(epoch * 4 + hsplit + 1) : "memory");
+            asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(sflag), "r"(hsplit + 1) : "memory");
         }
         if (q1 > pair) {
           named_bar(1, 128);                             // every thread has read the partials
@@ -1020,9 +1023,11 @@ static bool launch_pair(const bf16* A, int lda, int a_rows, const bf16* W, int N
   CUtensorMap ma, mb;
   if (K % (BK * KA)) return false;
   if (!get_map(A, a_rows, K, lda, BM, &ma, KA) || !get_map(W, N, K, K, BN / 2, &mb, KA)) return false;
-  // one pair per unit of the expected row count, at most one CTA per SM.  Stream-K (every SM busy,
-  // units cut at pair boundaries) when the units do not fill whole waves of pairs
-  const long long units = (long long)((m + 2 * BM - 1) / (2 * BM)) * ((N + BN - 1) / BN);
+  // one pair per unit, at most one CTA per SM (opt-in stream-K: every SM busy, units cut at pair
+  // boundaries).  The grid comes from the row-count upper bound M_max (persistent pairs; pairs without a unit at the live
+  // count exit): the launch must not depend on the host's row-count estimate, which only picks the
+  // tile width, or a graph captured at a small estimate would starve a step with many rows
+  const long long units = (long long)((M_max + 2 * BM - 1) / (2 * BM)) * ((N + BN - 1) / BN);
   const int np = num_sms() / 2;
   // opt-in (FOCUS_GEMM_PSK=1, read per call): measured slower at the C3 shapes -- the fp32 partial
   // write + read of the cut units costs more than the idle SMs of the ragged last wave
@@ -1049,11 +1054,9 @@ static bool launch_pair(const bf16* A, int lda, int a_rows, const bf16* W, int N
   }
   sk |= hint_on << 1;
   // GEMM_ADD, 256-wide tiles, one wave even with two k-halves per unit: ordered split-K (see kernel)
-  if (split2_ok) {
-    static unsigned epoch = 0;
-    epoch = epoch % 0xFFFFFu + 1;                      // flag values epoch * 4 + h stay below 2^22
-    sk |= 4 | ((split - 1) << 3) | (int)(epoch << 5);
-  }
+  // (the per-unit flags hold h while range h may add; the last range resets them to 0, so nothing
+  // launch-specific is baked into a captured graph)
+  if (split2_ok) sk |= 4 | ((split - 1) << 3);
 
   switch (mode) {
     case GEMM_ADD: launch_pair_k<GEMM_ADD, BN, KA>(grid, s, ma, mb, C, ldc, N, K, M_dev, M_max, e, pf_hint, ws, sk); break;

@@ -39,7 +39,7 @@ class focus_config(C.Structure):
                 ("placeholder_mode", C.c_int32), ("strategy", C.c_int32), ("fixed_k", C.c_int32),
                 ("max_requests", C.c_int32), ("max_seq_len", C.c_int32), ("page_size", C.c_int32),
                 ("max_prefill_chunk", C.c_int32), ("kv_pages", C.c_int64), ("weight_seed", C.c_uint64),
-                ("debug_taps", C.c_int32)]
+                ("debug_taps", C.c_int32), ("logit_scale", C.c_float)]
 
 
 class focus_commit_result(C.Structure):
@@ -116,7 +116,7 @@ def make_config(run, max_requests: Optional[int] = None, max_seq_len: Optional[i
         placeholder_mode=me.placeholder_mode, strategy=me.strategy, fixed_k=me.fixed_k,
         max_requests=max_requests or run.n_requests, max_seq_len=max_seq_len, page_size=run.page_size,
         max_prefill_chunk=max_prefill_chunk, kv_pages=kv_pages, weight_seed=run.weight_seed,
-        debug_taps=1 if debug_taps else 0)
+        debug_taps=1 if debug_taps else 0, logit_scale=m.logit_scale)
 
 
 def focus_required_bytes(cfg: focus_config) -> int:

@@ -26,6 +26,7 @@ class ModelConfig:
     vocab: int
     rope_theta: float
     rms_eps: float = 1e-6
+    logit_scale: float = 1.0             # W_lm scale, a power of two (focus_config::logit_scale)
 
     @property
     def mask_token_id(self) -> int:

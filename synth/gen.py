@@ -83,20 +83,24 @@ def _fast():
     return _FAST or None
 
 
-def weight_values(tid: int, start: int, count: int, fan_in: int, seed: int = 0, fast: bool = True) -> np.ndarray:
-    """Flat weight elements [start, start+count) of tensor `tid` as float32."""
+def weight_values(tid: int, start: int, count: int, fan_in: int, seed: int = 0, fast: bool = True,
+                  exp_offset: int = 0) -> np.ndarray:
+    """Flat weight elements [start, start+count) of tensor `tid` as float32, times 2**exp_offset
+    (a power-of-two scale keeps every value exact in bf16; used for the LM-head logit_scale)."""
+    e = weight_scale_exp(fan_in) + exp_offset
     lib = _fast() if fast else None
     if lib is not None:
         out = np.empty(count, dtype=np.float32)
-        lib.synth_weight_values(out.ctypes.data, tid, start, count, seed, weight_scale_exp(fan_in))
+        lib.synth_weight_values(out.ctypes.data, tid, start, count, seed, e)
         return out
     u = _stream(tid, start, count, seed)
     k = (u >> np.uint64(56)).astype(np.int32)
-    return np.ldexp((2 * k - 255).astype(np.float32), weight_scale_exp(fan_in)).astype(np.float32)
+    return np.ldexp((2 * k - 255).astype(np.float32), e).astype(np.float32)
 
 
 def weight_matrix(tid: int, rows: int, cols: int, fan_in: int, seed: int = 0,
-                  row_lo: int = 0, row_hi: int | None = None, chunk: int = 1 << 28) -> np.ndarray:
+                  row_lo: int = 0, row_hi: int | None = None, chunk: int = 1 << 28,
+                  exp_offset: int = 0) -> np.ndarray:
     """Rows [row_lo, row_hi) of the logical [rows][cols] matrix, float32."""
     row_hi = rows if row_hi is None else row_hi
     n = (row_hi - row_lo) * cols
@@ -104,8 +108,18 @@ def weight_matrix(tid: int, rows: int, cols: int, fan_in: int, seed: int = 0,
     start = row_lo * cols
     for off in range(0, n, chunk):
         c = min(chunk, n - off)
-        out[off:off + c] = weight_values(tid, start + off, c, fan_in, seed)
+        out[off:off + c] = weight_values(tid, start + off, c, fan_in, seed, exp_offset=exp_offset)
     return out.reshape(row_hi - row_lo, cols)
+
+
+def logit_scale_log2(scale: float) -> int:
+    """log2 of a power-of-two LM-head scale (focus_config::logit_scale; 0 means 1)."""
+    if scale == 0:
+        return 0
+    m, e = math.frexp(scale)
+    if m != 0.5 or not -15 <= e <= 17:
+        raise ValueError(f"logit_scale must be a power of two in [2^-16, 2^16], got {scale}")
+    return e - 1
 
 
 def prompt_tokens(request_id: int, n: int, vocab: int) -> np.ndarray:

@@ -21,9 +21,10 @@ from paper_2601_23278_b200 import FocusContext, make_config
 from paper_2601_23278_b200.runner import generate, prefill_all
 from oracle.engine import request_prompts
 from synth import get_config
-from synth.configs import ModelConfig
-run = get_config("C1").with_(model=ModelConfig(n_layers=4, d_model=256, n_q_heads=8, n_kv_heads=2, head_dim=128,
-                             d_ff=512, vocab=97, rope_theta=1e6), n_requests=6, prompt_len=300, gen_len=32)
+from synth.configs import MethodConfig, ModelConfig
+spec = json.loads(sys.argv[1])
+run = get_config("C1").with_(model=ModelConfig(**spec["model"]), method=MethodConfig(**spec["method"]),
+                             n_requests=spec["n_requests"], prompt_len=spec["prompt_len"], gen_len=spec["gen_len"])
 ctx = FocusContext(make_config(run))
 rids = prefill_all(ctx, request_prompts(run), run.gen_len)
 generate(ctx, rids, keep_log=False)
@@ -35,16 +36,28 @@ print(json.dumps({"tokens": toks, "steps": [int(st[r].total_steps) for r in rids
 """
 
 
-def _run(graph: str):
+_SMALL = dict(model=dict(n_layers=4, d_model=256, n_q_heads=8, n_kv_heads=2, head_dim=128, d_ff=512, vocab=97,
+                         rope_theta=1e6), method=dict(block_size=4), n_requests=6, prompt_len=300, gen_len=32)
+# d_ff 8192: the down projection runs the ordered split-K; 24 requests x B = 16 give up to 384 P rows
+# (two 256-row tiles at layers 0-1) but fewer S rows, so some split-K flags are touched only by the
+# layer-0/1 launches -- they must be re-armed for the next replay of the same graph (logit_scale 16:
+# several decodes per step, so block phases and graph keys vary)
+_SPLITK = dict(model=dict(n_layers=4, d_model=256, n_q_heads=8, n_kv_heads=2, head_dim=128, d_ff=8192, vocab=97,
+                          rope_theta=1e6, logit_scale=16.0), method=dict(block_size=16), n_requests=24,
+               prompt_len=100, gen_len=64)
+
+
+def _run(graph: str, spec: dict):
     env = dict(os.environ, FOCUS_GRAPH=graph)
-    out = subprocess.run([sys.executable, "-c", _SCRIPT % {"root": ROOT}], env=env, capture_output=True, text=True,
-                         timeout=600, cwd=ROOT)
+    out = subprocess.run([sys.executable, "-c", _SCRIPT % {"root": ROOT}, json.dumps(spec)], env=env,
+                         capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert out.returncode == 0, out.stderr[-2000:]
     return json.loads(out.stdout.strip().splitlines()[-1])
 
 
-def test_graph_replay_matches_eager():
-    eager, graph = _run("0"), _run("1")
+@pytest.mark.parametrize("spec", [_SMALL, _SPLITK], ids=["small", "splitk_replay"])
+def test_graph_replay_matches_eager(spec):
+    eager, graph = _run("0", spec), _run("1", spec)
     assert graph["tokens"] == eager["tokens"]
     assert graph["steps"] == eager["steps"] and graph["sums"] == eager["sums"]
     assert graph["launches"] == eager["launches"]      # replays account the captured launches

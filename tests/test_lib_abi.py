@@ -48,11 +48,16 @@ def test_config_validation(lib):
     cfg = make_config(get_config("C1"))
     assert focus_required_bytes(cfg) > 0
     bad = [("alpha_num", 2), ("maxpool_kernel", 2), ("block_size", 65), ("block_size", 0), ("n_layers", 1),
-           ("n_kv_heads", 3), ("head_dim", 24), ("conf_threshold", 0.0), ("conf_threshold", 1.5)]
+           ("n_kv_heads", 3), ("head_dim", 24), ("conf_threshold", 0.0), ("conf_threshold", 1.5),
+           ("logit_scale", 3.0), ("logit_scale", -2.0), ("logit_scale", 2.0 ** 20)]
     for field, val in bad:
         c = make_config(get_config("C1"))
         setattr(c, field, val)
         assert focus_required_bytes(c) == 0, field
+    for ok in (0.0, 1.0, 16.0, 0.25):                   # powers of two (0 = 1)
+        c = make_config(get_config("C1"))
+        c.logit_scale = ok
+        assert focus_required_bytes(c) > 0, ok
     h = C.c_void_p()
     c = make_config(get_config("C1")); c.alpha_num = 1
     assert _lib().focus_init(C.byref(c), None, 0, None, C.byref(h)) == 2        # FOCUS_ERR_CONFIG

@@ -378,3 +378,26 @@ def test_integrated_scripted_trace():
     assert st.R == -1 and st.committed == set() and st.s == 8 and st.output == [7, 7, 7, 7]
     # next block's first K_hist uses the persisted statistics: ceil(3/2 * 4/3) = 2
     assert F.k_hist(3, 2, st.token_sum, st.total_steps) == 2
+
+
+def test_logit_scale_is_an_exact_power_of_two_scaling():
+    """focus_config::logit_scale (SURVEY 8(b), A-M3 "logit_scale * W_lm"): a power-of-two scale of the
+    recipe's LM-head weights, so z(s) = s * z(1) exactly and conf(s) = softmax max-prob at
+    temperature 1/s; non-powers of two are rejected."""
+    import dataclasses
+    from oracle.model import Backbone, OracleWeights
+    from synth.configs import ModelConfig
+    from synth.gen import logit_scale_log2
+    m1 = ModelConfig(n_layers=2, d_model=32, n_q_heads=2, n_kv_heads=1, head_dim=16, d_ff=64, vocab=41, rope_theta=1e4)
+    m8 = dataclasses.replace(m1, logit_scale=8.0)
+    w1, w8 = OracleWeights(m1).lm_head(), OracleWeights(m8).lm_head()
+    assert np.array_equal(w8, 8.0 * w1)
+    x = np.random.default_rng(0).standard_normal((3, 32))
+    z1 = Backbone(m1, OracleWeights(m1), "gpu").logits(x)
+    z8 = Backbone(m8, OracleWeights(m8), "gpu").logits(x)
+    fin = np.isfinite(z1)
+    assert np.array_equal(z8[fin], 8.0 * z1[fin])
+    assert [logit_scale_log2(s) for s in (0, 1, 2, 0.5, 65536)] == [0, 0, 1, -1, 16]
+    for bad in (3.0, 2.0 ** 20, -4.0):
+        with pytest.raises(ValueError):
+            logit_scale_log2(bad)
