@@ -3,17 +3,36 @@
   python bench.py [--gpus N --steps K --warmup W]            # our CUDA path (libfocus.so)
   python bench.py --impl reference [--steps K --warmup W]    # the CPU oracle on a bounded sample
 
-Workload (per GPU): C3 = SDAR-8B-shaped random-init model (36 layers, d 4096, GQA 32/8, d_ff 12288,
-vocab 151936), block 16, 64 requests, prompt 1024, gen 512 (BASELINE.json configs[2]).  Under
-torchrun each rank owns 64 requests of its own (request-level data parallel, weak scaling).
-A step = focus_step_block + focus_commit over all requests of the rank (the whole hot path).
+Default workload (per GPU): C3 = SDAR-8B-shaped random-init model (36 layers, d 4096, GQA 32/8, d_ff
+12288, vocab 151936), block 16, 64 requests, prompt 1024, gen 512 (BASELINE.json configs[2]).  With
+N GPUs each rank owns 64 requests of its own (request-level data parallel, weak scaling, no collective
+on the data path).  `--workload C4` is BASELINE configs[3]: 256 requests with prompt lengths uniform
+in [256, 4096], LPT-sharded over the N ranks (strong scaling: the global batch is fixed).
+`--gpus N` without a torchrun environment re-launches itself under torch.distributed.run.
+
+A step = focus_step_block + focus_commit over all requests of the rank (the whole hot path).  Each
+run decodes the WHOLE generation (every request to its gen_len) after an untimed prefill:
+  - W warm-up steps, then three device-timed windows of exactly K steps at the start, middle and end
+    of the generation (same phase of the B-decode + 1-flush block cycle, so context spans 1024-1536
+    at C3); `value` = the median window (barrier + synchronize around each window, CUDA events on the
+    library stream, max over ranks); `generation` = every post-warm-up step, device-timed;
+  - e2e: the whole generation again through the C ABI from host buffers (request list uploaded and
+    commit results read back to pinned memory every step), wall clock after the W warm-up steps;
+  - box-local baselines on the same inputs: strategy NONE (no eviction, the LMDeploy-like regime the
+    paper compares with, fig:ablation_throughput P:538-545) and the calibrated logit_scale run
+    (about 0.1 B tokens decoded per request-step, SURVEY 8(d));
+  - redundancy N_processed / N_decoded at layers 2+ (tab:reduce_ratio P:480-504) from device counters;
+  - per-kernel CUDA-event breakdown (2 profiled steps after the middle window) and the roofline of the
+    dominant kernel: max(FLOPs / tensor peak, bytes / HBM peak) per launch.
 Prints ONE JSON line on rank 0.
 """
 from __future__ import annotations
 
 import argparse
+import dataclasses
 import json
 import os
+import socket
 import subprocess
 import sys
 import time
@@ -23,6 +42,12 @@ sys.path.insert(0, ROOT)
 
 METRIC = "decoded tokens/sec (SDAR-8B-shaped, block 16) at 1/2/4/8 B200; % roofline"
 UNIT = "tokens/s"
+# calibrated LM-head scale per workload: mean decoded tokens per request-step ~ 0.1 B (the
+# fig:decoding_stats regime); C3 measured 1.59 at 16 (scripts/calibrate_logit_scale.py)
+CALIBRATED_SCALE = {"C2": 16.0, "C3": 16.0, "C4": 16.0, "C5": 16.0}
+MODEL_NAME = {"C2": "SDAR-1.7B-shaped (random init)", "C3": "SDAR-8B-shaped (random init)",
+              "C4": "SDAR-8B-shaped (random init)", "C5": "SDAR-8B-shaped (random init)",
+              "C1": "tiny block-diffusion model (random init)"}
 
 
 def peaks():
@@ -43,16 +68,17 @@ class Clocks:
 
     def __init__(self, gpu: int):
         self.gpu, self.p, self.lines, self.th = gpu, None, [], None
-        self.t0 = self.t1 = 0.0
+        self.spans = []
+        self.out = ""
 
     def _reader(self):
         for line in self.p.stdout:
             self.lines.append((time.time(), line))
 
-    def __enter__(self):
-        # the sampler is started and its first sample awaited BEFORE the timed region begins (nvidia-smi
-        # takes a few hundred ms to start, longer than a short timed region); samples are time-stamped
-        # on arrival and the summary keeps those that fall inside the region
+    def start(self):
+        # the sampler is started and its first sample awaited BEFORE the first timed window (nvidia-smi
+        # takes a few hundred ms to start); samples are time-stamped on arrival and the summary keeps
+        # those that fall inside a timed window
         import threading
         try:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + self.Q, "--format=csv,noheader,nounits",
@@ -64,11 +90,12 @@ class Clocks:
                 time.sleep(0.01)
         except Exception:
             self.p = None
-        self.t0 = time.time()
         return self
 
-    def __exit__(self, *a):
-        self.t1 = time.time()
+    def span(self, t0, t1):
+        self.spans.append((t0, t1))
+
+    def stop(self):
         time.sleep(0.06)                                 # let the in-flight sample arrive
         if self.p is not None:
             self.p.terminate()
@@ -78,7 +105,7 @@ class Clocks:
                 pass
             if self.th is not None:
                 self.th.join(timeout=2)
-        inside = [ln for (t, ln) in self.lines if self.t0 - 0.03 <= t <= self.t1 + 0.03]
+        inside = [ln for (t, ln) in self.lines if any(a - 0.03 <= t <= b + 0.03 for a, b in self.spans)]
         self.out = "".join(inside)
 
     def summary(self):
@@ -91,232 +118,469 @@ class Clocks:
         return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": float(rows[0][2]), "reasons": reasons, "samples": len(rows)}
 
 
+# ------------------------------------------------------------------------------------ host planning
+def gen_steps(run) -> int:
+    """Steps of a whole generation under the synthetic dynamics: each block takes B
+    decode steps (one fallback decode per request-step) + 1 flush step."""
+    B = run.method.block_size
+    return run.gen_len // B * (B + 1)
+
+
+def window_starts(total: int, warmup: int, steps: int, cyc: int) -> list:
+    """Starts of the three timed K-step windows: right after the warm-up, in the middle and at the end
+    of the generation, all at the warm-up's phase of the block cycle (same decode/flush mix); fewer
+    windows when the generation is too short to hold three disjoint ones."""
+    ph = warmup % cyc
+    last = total - steps
+    starts = [warmup]
+    if last >= warmup:
+        late = last - ((last - ph) % cyc)
+        mid = (warmup + late) // 2
+        mid -= (mid - ph) % cyc
+        for s in (mid, late):
+            if s >= starts[-1] + steps + 2 and s + steps <= total:    # disjoint, room for the profile pass
+                starts.append(s)
+    return starts
+
+
+def plan_requests(run, world: int, rank: int):
+    """(global request ids of this rank, {gid: prompt length}, scaling).  C4: fixed global batch with
+    mixed prompt lengths, LPT-sharded by cost L_prompt + gen/2 -> strong scaling.
+    Otherwise run.n_requests requests per rank (weak scaling)."""
+    from paper_2601_23278_b200 import dist as D
+    from synth.gen import prompt_lengths
+    if run.prompt_len_hi is not None:
+        lens = prompt_lengths(run.n_requests, run.prompt_len, run.prompt_len_hi).tolist()
+        costs = [L + run.gen_len / 2 for L in lens]
+        mine = D.shard_requests(run.n_requests, world, rank, costs)
+        return mine, {g: lens[g] for g in mine}, "strong"
+    n = run.n_requests
+    gids = list(range(rank * n, (rank + 1) * n))
+    return gids, {g: run.prompt_len for g in gids}, "weak"
+
+
 # ------------------------------------------------------------------------------------ algorithmic work
 def step_work(model, B, counters, states, rids):
-    """SURVEY 8(d) per-step algorithmic FLOPs / bytes by kernel family, from the step's live sizes."""
+    """SURVEY 8(d) per-step algorithmic FLOPs and bytes by kernel family, from the step's live sizes.
+    GEMM bytes: weights once + activation rows in/out; attention bytes: the K/V each request streams
+    (ctx + B at layers 0-1, ctx + R' + 1 at layers >= 2), FLOPs 4 H_q d_h per (query row, key)."""
     d, ff, V, L = model.d_model, model.d_ff, model.vocab, model.n_layers
     qkv = model.qkv_dim
     qd = model.n_q_heads * model.head_dim
     MP, MS, ML = counters
-    Wqkv, Wo, Wgu, Wd = d * qkv, qd * d, 2 * d * ff, d * ff
-    fl = {
-        "gemm_qkv": 2 * Wqkv * (2 * MP + (L - 2) * MS),
-        "gemm_o": 2 * Wo * (MP + (L - 1) * MS),
-        "gemm_gu": 2 * Wgu * (MP + (L - 1) * MS),
-        "gemm_down": 2 * Wd * (MP + (L - 1) * MS),
-        "gemm_lm": 2 * d * V * ML,
+    shapes = {  # family: (N, K, rows per step [(rows, launches)], out bytes per element read+written)
+        "gemm_qkv": (qkv, d, [(MP, 2), (MS, L - 2)], 2),
+        "gemm_o": (d, qd, [(MP, 1), (MS, L - 1)], 8),
+        "gemm_gu": (2 * ff, d, [(MP, 1), (MS, L - 1)], 1),
+        "gemm_down": (d, ff, [(MP, 1), (MS, L - 1)], 8),
+        "gemm_lm": (V, d, [(ML, 1)], 4),
     }
-    # weight bytes each GEMM family must stream once per step (bf16)
-    wb = {"gemm_qkv": 2 * Wqkv * L, "gemm_o": 2 * Wo * L, "gemm_gu": 2 * Wgu * L, "gemm_down": 2 * Wd * L,
-          "gemm_lm": 2 * d * V}
+    fl, by = {}, {}
+    for k, (N, K, parts, ob) in shapes.items():
+        fl[k] = sum(2 * r * N * K * n for r, n in parts)
+        by[k] = sum((2 * N * K + 2 * r * K + ob * r * N) * n for r, n in parts)
     kvb = 4 * model.n_kv_heads * model.head_dim          # K+V bf16 bytes per token per layer
-    attn_bytes = 0
+    attn_bytes = attn_flops = 0
     for r in rids:
         s = states[r]
-        if not s.active:
+        if not s.active or s.finished:
             continue
-        attn_bytes += kvb * (2 * (s.s + B) + (L - 2) * (s.s + s.R_new + 1))
-    return fl, wb, attn_bytes
+        nP = bin(int(s.P)).count("1")
+        nS = bin(int(s.S)).count("1")
+        attn_bytes += kvb * ((s.s + B) + (L - 2) * (s.s + s.R_new + 1) + (s.s + B))
+        attn_flops += 4 * qd * (nP * (s.s + B) + nS * (s.s + B) + (L - 2) * nS * (s.s + s.R_new + 1))
+    fl["attention"], by["attention"] = attn_flops, attn_bytes
+    return fl, by
 
 
-def build_ctx(run, n_req):
-    from paper_2601_23278_b200 import FocusContext, make_config
-    return FocusContext(make_config(run, max_requests=n_req))
+# ------------------------------------------------------------------------------------ the CUDA path
+class Rank:
+    """One rank's decode loop over the C ABI (libfocus through the ctypes binding)."""
+
+    def __init__(self, run, gids, lens, dev, **cfg_kw):
+        from paper_2601_23278_b200 import FocusContext, make_config
+        self.run, self.gids, self.lens, self.dev = run, gids, lens, dev
+        hi = max(lens.values()) if lens else run.prompt_len
+        self.ctx = FocusContext(make_config(run, max_requests=max(1, len(gids)), max_seq_len=hi + run.gen_len,
+                                            **cfg_kw))
+        self.rids = list(range(len(gids)))
+
+    def prefill(self):
+        import torch
+        from synth.gen import prompt_tokens
+        t0 = time.time()
+        for r, g in zip(self.rids, self.gids):
+            self.ctx.focus_kv_append(r, prompt_tokens(g, self.lens[g], self.run.model.vocab), self.run.gen_len)
+        torch.cuda.synchronize()
+        return time.time() - t0
+
+    def release(self):
+        for r in self.rids:
+            self.ctx.focus_release(r)
+
+    def step(self):
+        self.ctx.focus_step_block(self.rids)
+        self.ctx.focus_commit(self.rids)
+
+    def tok_sum(self):
+        s = self.ctx.states()
+        return sum(int(s[r].token_sum) for r in self.rids)
+
+    def all_finished(self):
+        s = self.ctx.states()
+        return all(s[r].finished for r in self.rids)
+
+    def close(self):
+        import torch
+        self.ctx.focus_destroy()
+        del self.ctx
+        torch.cuda.empty_cache()
+
+
+def _all_finished(rk, D):
+    return D.reduce_min(1.0 if rk.all_finished() else 0.0, rk.dev) > 0.5
+
+
+def decode_generation(rk, D, warmup, steps, starts, clk=None, prof_after=None, max_steps=100000):
+    """Decode the whole generation of the rank's requests.  Returns per-window and whole-generation
+    device timings (max over ranks) and the profiled step data when `prof_after` names a window."""
+    import torch
+    st, dev = rk.ctx.stream, rk.dev
+    cyc = rk.run.method.block_size + 1
+    for _ in range(warmup):
+        rk.step()
+    torch.cuda.synchronize()
+    windows, segs, prof = [], [], None
+    t = warmup
+    seg_dec0, seg_ev0 = rk.tok_sum(), None
+    D.barrier(dev)
+
+    def seg_begin():
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(st)
+        return e
+
+    def seg_end(e0, dec0, kind):
+        e1 = torch.cuda.Event(enable_timing=True)
+        e1.record(st)
+        torch.cuda.synchronize()
+        segs.append((kind, e0.elapsed_time(e1), rk.tok_sum() - dec0))
+
+    seg_ev0 = seg_begin()
+    n_since_check = 0
+    while t < max_steps:
+        if t in starts:
+            seg_end(seg_ev0, seg_dec0, "gap")
+            D.barrier(dev)
+            torch.cuda.synchronize()
+            dec0, l0 = rk.tok_sum(), rk.ctx.launches()
+            if clk is not None and not windows:
+                clk.start()
+            w0 = time.time()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            for _ in range(steps):
+                rk.step()
+            e1.record(st)
+            torch.cuda.synchronize()
+            if clk is not None:
+                clk.span(w0, time.time())
+            D.barrier(dev)
+            ms = e0.elapsed_time(e1)
+            dec = rk.tok_sum() - dec0
+            windows.append(dict(start=t, ms=ms, decoded=dec, launches=rk.ctx.launches() - l0))
+            segs.append(("window", ms, dec))
+            t += steps
+            if prof_after is not None and len(windows) == prof_after:
+                prof = profile_steps(rk, 2)
+                t += 2
+            seg_dec0, seg_ev0 = rk.tok_sum(), seg_begin()
+            n_since_check = 0
+            continue
+        rk.step()
+        t += 1
+        n_since_check += 1
+        if n_since_check >= cyc and t not in starts:
+            seg_end(seg_ev0, seg_dec0, "gap")
+            n_since_check = 0
+            if _all_finished(rk, D):
+                seg_ev0 = None
+                break
+            seg_dec0, seg_ev0 = rk.tok_sum(), seg_begin()
+    if seg_ev0 is not None:
+        seg_end(seg_ev0, seg_dec0, "gap")
+    while not _all_finished(rk, D) and t < max_steps:
+        e0, d0 = seg_begin(), rk.tok_sum()
+        rk.step()
+        t += 1
+        seg_end(e0, d0, "gap")
+    gen_ms = sum(ms for _, ms, _ in segs)
+    gen_dec = sum(dec for _, _, dec in segs)
+    return dict(windows=windows, gen_ms=gen_ms, gen_dec=gen_dec, steps_total=t, prof=prof)
+
+
+def profile_steps(rk, n):
+    """n steps with CUDA events around every launch (FOCUS_PROF kinds) plus the live sizes."""
+    c = rk.ctx
+    c.focus_set_profile(True)
+    fl_tot, by_tot = {}, {}
+    for _ in range(n):
+        c.focus_step_block(rk.rids)
+        c.focus_sync()
+        cnt = c.counters()
+        fl, by = step_work(rk.run.model, rk.run.method.block_size, (int(cnt[0]), int(cnt[1]), int(cnt[2])),
+                           c.states(), rk.rids)
+        for k in fl:
+            fl_tot[k] = fl_tot.get(k, 0) + fl[k]
+            by_tot[k] = by_tot.get(k, 0) + by[k]
+        c.focus_commit(rk.rids)
+    c.focus_sync()
+    prof = c.profile()
+    c.focus_set_profile(False)
+    return dict(prof=prof, flops=fl_tot, bytes=by_tot, steps=n)
+
+
+def e2e_generation(rk, D, warmup):
+    """The whole generation through the C ABI from host buffers, wall clock after `warmup` untimed
+    steps: every step uploads the request list (focus_step_block reads it from host memory) and reads
+    the commit results back into pinned host memory, double-buffered like a serving loop (step t's
+    results are parsed while step t+1 runs); it ends when the host has seen every request finish."""
+    import ctypes
+    import torch
+    from paper_2601_23278_b200.focus import focus_commit_result
+    c, st, dev, n = rk.ctx, rk.ctx.stream, rk.dev, len(rk.rids)
+    for _ in range(warmup):
+        rk.step()
+    c.focus_sync()
+    rsz = ctypes.sizeof(focus_commit_result)
+    res = [torch.empty(max(n, 1) * rsz, dtype=torch.uint8).pin_memory() for _ in range(2)]
+    done = [None, None]
+    dec0 = rk.tok_sum()
+    host_decoded, steps = 0, 0
+    finished = set()
+
+    def consume(k):
+        nonlocal host_decoded
+        done[k].synchronize()
+        arr = (focus_commit_result * n).from_address(res[k].data_ptr())
+        for x in arr:
+            host_decoded += int(x.n_new)
+            if x.finished:
+                finished.add(int(x.req_id))
+        done[k] = None
+
+    D.barrier(dev)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    i = 0
+    while len(finished) < n:
+        k = i & 1
+        if done[k] is not None:
+            consume(k)
+            if len(finished) >= n:
+                break
+        c.focus_step_block(rk.rids)
+        c.focus_commit(rk.rids, res[k].data_ptr())
+        done[k] = torch.cuda.Event()
+        done[k].record(st)
+        i += 1
+        steps += 1
+        if steps > 1000000:
+            raise RuntimeError("e2e generation did not finish")
+    for k in (0, 1):
+        if done[k] is not None:
+            consume(k)
+    c.focus_sync()
+    wall = time.perf_counter() - t0
+    dec = rk.tok_sum() - dec0
+    assert host_decoded == dec, (host_decoded, dec)
+    return dict(wall_s=wall, decoded=dec, steps=steps, rsz=rsz)
+
+
+def _agg_windows(win_lists, D, dev):
+    """Per window: decoded summed over ranks / device ms max over ranks."""
+    out = []
+    for w in win_lists:
+        ms = D.reduce_max(w["ms"], dev)
+        dec = D.reduce_sum(w["decoded"], dev)
+        out.append(dict(start=w["start"], ms=round(ms, 3), decoded=int(dec), launches=int(w["launches"]),
+                        value=round(dec / (ms / 1e3), 2)))
+    return out
+
+
+def roofline_report(pd, pk):
+    """Per kernel family: T_roof = max(FLOPs / tensor peak, bytes / HBM peak) against the CUDA-event
+    time of its launches (SURVEY 8(d) reporting); the dominant kernel's object for the JSON line."""
+    prof, fl, by, n = pd["prof"], pd["flops"], pd["bytes"], pd["steps"]
+    total_ms = sum(v["total_ms"] for v in prof.values()) or 1.0
+    traffic = {}
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get("dram_bytes_per_launch", {})
+    kernels, troof_sum = {}, 0.0
+    for k, v in prof.items():
+        if not v["launches"]:
+            continue
+        e = {"launches": v["launches"] // n, "ms_per_step": round(v["total_ms"] / n, 4),
+             "share": round(v["total_ms"] / total_ms, 4)}
+        if k in fl:
+            t_tc = fl[k] / (pk["tc_sus"] * 1e12) * 1e3
+            t_hbm = by[k] / (pk["hbm"] * 1e9) * 1e3
+            t_roof = max(t_tc, t_hbm)
+            troof_sum += t_roof
+            e.update(bound="tensor" if t_tc >= t_hbm else "hbm", roofline_ms=round(t_roof / n, 4),
+                     frac=round(t_roof / v["total_ms"], 4),
+                     tflops=round(fl[k] / (v["total_ms"] / 1e3) / 1e12, 2),
+                     gbs=round(by[k] / (v["total_ms"] / 1e3) / 1e9, 1))
+        kernels[k] = e
+    cands = [k for k in kernels if k in fl]
+    dom = max(cands, key=lambda k: prof[k]["total_ms"])
+    n_l = prof[dom]["launches"]
+    ms_l = prof[dom]["total_ms"] / n_l
+    e = kernels[dom]
+    if e["bound"] == "hbm":
+        ach = by[dom] / n_l / (ms_l / 1e3) / 1e9
+        roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": pk["hbm"], "unit": "GB/s",
+                "frac": round(ach / pk["hbm"], 4), "algorithmic_bytes_per_launch": round(by[dom] / n_l),
+                "peak_src": pk["src"] + " HBM copy"}
+    else:
+        ach = fl[dom] / n_l / (ms_l / 1e3) / 1e12
+        roof = {"bound": "tensor", "achieved": round(ach, 2), "peak": pk["tc_sus"], "unit": "TFLOP/s",
+                "frac": round(ach / pk["tc_sus"], 4), "flops_per_launch": round(fl[dom] / n_l),
+                "peak_src": pk["src"] + " sustained bf16"}
+    names = {"attention": "k_attn_tc (block-diffusion paged attention, tcgen05) per layer"}
+    roof.update(kernel=names.get(dom, f"k_gemm_pair ({dom}) per layer"), traffic=traffic.get(dom),
+                launch_ms=round(ms_l, 4), launches_per_step=n_l // n, share_of_step=e["share"],
+                timing="CUDA events around every launch on the library stream, 2 profiled steps after the middle window")
+    proj = ["gemm_qkv", "gemm_o", "gemm_gu", "gemm_down"]
+    g_ms = sum(prof[k]["total_ms"] for k in proj)
+    g_fl = sum(fl[k] for k in proj)
+    ach_all = g_fl / (g_ms / 1e3) / 1e12
+    gemms = {"bound": "tensor", "kernel": "all projection GEMMs", "achieved": round(ach_all, 2),
+             "peak": pk["tc_sus"], "unit": "TFLOP/s", "frac": round(ach_all / pk["tc_sus"], 4),
+             "share_of_step": round(g_ms / total_ms, 4)}
+    step = {"roofline_ms_per_step": round(troof_sum / n, 4), "measured_ms_per_step": round(total_ms / n, 4),
+            "frac": round(troof_sum / total_ms, 4),
+            "note": "sum over kernel families of max(F/TC, B/HBM) vs the profiled step (events serialise launches)"}
+    return roof, gemms, kernels, step
 
 
 def run_focus(args):
     import torch
     from paper_2601_23278_b200 import dist as D
-    from paper_2601_23278_b200.focus import focus_commit_result
     from synth import get_config
-    from synth.gen import prompt_tokens
 
     rank, world, local = D.init("nccl")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     run = get_config(args.workload)
-    n_req = run.n_requests
-    gids = list(range(rank * n_req, (rank + 1) * n_req))          # weak scaling: 64 requests per rank
-    ctx = build_ctx(run, n_req)
-    rids = list(range(n_req))
-    t0 = time.time()
-    for i, r in enumerate(rids):
-        ctx.focus_kv_append(r, prompt_tokens(gids[i], run.prompt_len, run.model.vocab), run.gen_len)
-    torch.cuda.synchronize()
-    prefill_s = time.time() - t0
-    st = ctx.stream
+    if args.logit_scale != 1.0:
+        run = run.with_(model=dataclasses.replace(run.model, logit_scale=args.logit_scale))
+    gids, lens, scaling = plan_requests(run, world, rank)
+    B = run.method.block_size
+    cyc = B + 1
+    T = gen_steps(run)
+    starts = window_starts(T, args.warmup, args.steps, cyc)
+    kw = dict(batch_invariant=args.batch_invariant)
 
-    def tok_sum():
-        s = ctx.states()
-        return sum(int(s[r].token_sum) for r in rids)
+    # ---- FOCUS: whole generation, three timed windows, profile pass after the middle window
+    rk = Rank(run, gids, lens, dev, **kw)
+    prefill_s = rk.prefill()
+    rows0 = rk.ctx.cumulative_rows()
+    clk = Clocks(local)
+    g = decode_generation(rk, D, args.warmup, args.steps, starts, clk, prof_after=min(2, len(starts)))
+    clk.stop()
+    rows1 = rk.ctx.cumulative_rows()
+    wins = _agg_windows(g["windows"], D, dev)
+    med = sorted(wins, key=lambda w: w["value"])[len(wins) // 2]
+    value = med["value"]
+    gen_ms = D.reduce_max(g["gen_ms"], dev)
+    gen_dec = D.reduce_sum(g["gen_dec"], dev)
+    dec_total = D.reduce_sum(sum(int(rk.ctx.states()[r].token_sum) for r in rk.rids), dev)
+    red_S = D.reduce_sum(rows1["sum_S"] - rows0["sum_S"], dev) / max(dec_total, 1)
+    red_P = D.reduce_sum(rows1["sum_P"] - rows0["sum_P"], dev) / max(dec_total, 1)
 
-    for _ in range(args.warmup):
-        ctx.focus_step_block(rids)
-        ctx.focus_commit(rids)
-    ctx.focus_sync()
+    # ---- e2e: the whole generation again from host buffers (same context, graphs already captured)
+    rk.release()
+    rk.prefill()
+    e = e2e_generation(rk, D, args.warmup)
+    e2e_val = D.reduce_sum(e["decoded"], dev) / D.reduce_max(e["wall_s"], dev)
+    rk.close()
 
-    # ---- timed: K steps, inputs resident in HBM, device-timed with events on the library stream
-    dec0 = tok_sum()
-    l0 = ctx.launches()
-    D.barrier(dev)
-    torch.cuda.synchronize()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ncu_step = bool(os.environ.get("FOCUS_NCU_STEP"))  # ncu --profile-from-start off: capture timed step 1 only
-    with Clocks(local) as clk:
-        ev0.record(st)
-        for i in range(args.steps):
-            if ncu_step and i == 0:
-                torch.cuda.profiler.start()
-            ctx.focus_step_block(rids)
-            ctx.focus_commit(rids)
-            if ncu_step and i == 0:
-                torch.cuda.profiler.stop()
-        ev1.record(st)
-        torch.cuda.synchronize()
-    D.barrier(dev)
-    ms = ev0.elapsed_time(ev1)
-    launches = ctx.launches() - l0
-    dec = tok_sum() - dec0
-    ms_max = D.reduce_max(ms, dev)
-    dec_all = D.reduce_sum(dec, dev)
-    value = dec_all / (ms_max / 1e3)
+    # ---- box-local baselines on the same inputs
+    extras = {}
+    if not args.no_extras:
+        from synth.configs import STRATEGY_NONE
+        for name, r2 in (("no_eviction", run.with_(method=dataclasses.replace(run.method, strategy=STRATEGY_NONE))),
+                         ("calibrated", run.with_(model=dataclasses.replace(
+                             run.model, logit_scale=CALIBRATED_SCALE.get(args.workload, 16.0))))):
+            rb = Rank(r2, gids, lens, dev, **kw)
+            rb.prefill()
+            c0 = rb.ctx.cumulative_rows()
+            gb = decode_generation(rb, D, args.warmup, args.steps, starts if name == "no_eviction" else [])
+            c1 = rb.ctx.cumulative_rows()
+            dec_b = D.reduce_sum(sum(int(rb.ctx.states()[r].token_sum) for r in rb.rids), dev)
+            st_b = D.reduce_sum(sum(int(rb.ctx.states()[r].total_steps) for r in rb.rids), dev)
+            gms = D.reduce_max(gb["gen_ms"], dev)
+            gdec = D.reduce_sum(gb["gen_dec"], dev)
+            x = {"generation": {"value": round(gdec / (gms / 1e3), 2), "decoded": int(gdec), "ms": round(gms, 1),
+                                "steps": gb["steps_total"]},
+                 "redundancy_layer2plus": round(D.reduce_sum(c1["sum_S"] - c0["sum_S"], dev) / max(dec_b, 1), 3),
+                 "redundancy_layers01": round(D.reduce_sum(c1["sum_P"] - c0["sum_P"], dev) / max(dec_b, 1), 3),
+                 "decoded_per_request_step": round(dec_b / max(st_b, 1), 3)}
+            if gb["windows"]:
+                wb = _agg_windows(gb["windows"], D, dev)
+                x["windows"] = wb
+                x["value"] = sorted(wb, key=lambda w: w["value"])[len(wb) // 2]["value"]
+            if name == "calibrated":
+                x["logit_scale"] = r2.model.logit_scale
+            rb.close()
+            extras[name] = x
+        fg = gen_dec / (gen_ms / 1e3)
+        extras["no_eviction"]["focus_speedup_generation"] = round(fg / extras["no_eviction"]["generation"]["value"], 3)
+        if "value" in extras["no_eviction"]:
+            extras["no_eviction"]["focus_speedup_windows"] = round(value / extras["no_eviction"]["value"], 3)
 
-    # ---- e2e: through the C ABI with host buffers; every step uploads the request list from host
-    # memory and copies its commit results (newly decoded tokens per request) back into pinned host
-    # memory.  The readback is double-buffered like a serving loop: step t's results are read on the
-    # host (event wait + parse) while step t+1 runs, since all decode state stays on the device.
-    rsz = __import__("ctypes").sizeof(focus_commit_result)
-    res = [torch.empty(n_req * rsz, dtype=torch.uint8).pin_memory() for _ in range(2)]
-    done = [None, None]
-    e2e_steps = max(1, min(args.steps, 20))
-    # start the e2e window at the same phase of the block cycle (B decode steps + 1 flush step per
-    # block under the synthetic dynamics) as the timed window, so both windows hold the same mix of
-    # decode and flush steps; the phase-alignment steps are untimed
-    cyc = run.method.block_size + 1
-    for _ in range((args.warmup - (args.warmup + args.steps)) % cyc):
-        ctx.focus_step_block(rids)
-        ctx.focus_commit(rids)
-    ctx.focus_sync()
-    dec0 = tok_sum()
-    host_decoded = 0
-
-    def consume(k):
-        nonlocal host_decoded
-        done[k].synchronize()
-        arr = (focus_commit_result * n_req).from_address(res[k].data_ptr())
-        host_decoded += sum(int(r.n_new) for r in arr)
-
-    D.barrier(dev)
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    for i in range(e2e_steps):
-        k = i & 1
-        if done[k] is not None:
-            consume(k)
-            done[k] = None
-        ctx.focus_step_block(rids)
-        ctx.focus_commit(rids, res[k].data_ptr())
-        done[k] = torch.cuda.Event()
-        done[k].record(st)
-    for i in (e2e_steps - 2, e2e_steps - 1):       # drain the last two steps' readbacks, in order
-        if i >= 0 and done[i & 1] is not None:
-            consume(i & 1)
-            done[i & 1] = None
-    ctx.focus_sync()
-    e2e_s = time.perf_counter() - t0
-    e2e_dec = tok_sum() - dec0
-    assert host_decoded == e2e_dec, (host_decoded, e2e_dec)
-    e2e_val = D.reduce_sum(e2e_dec, dev) / D.reduce_max(e2e_s, dev)
-
-    # ---- kernel breakdown: per-launch CUDA events (separate pass, 2 steps)
-    ctx.focus_set_profile(True)
-    fl_tot, wb_tot, ab_tot = {}, {}, 0
-    prof_steps = 2
-    for _ in range(prof_steps):
-        ctx.focus_step_block(rids)
-        ctx.focus_sync()
-        c = ctx.counters()
-        fl, wb, ab = step_work(run.model, run.method.block_size, (int(c[0]), int(c[1]), int(c[2])), ctx.states(), rids)
-        for k in fl:
-            fl_tot[k] = fl_tot.get(k, 0) + fl[k]
-            wb_tot[k] = wb_tot.get(k, 0) + wb[k]
-        ab_tot += ab
-        ctx.focus_commit(rids)
-    ctx.focus_sync()
-    prof = ctx.profile()
-    ctx.focus_set_profile(False)
     pk = peaks()
-    total_ms = sum(v["total_ms"] for v in prof.values()) or 1.0
-    kernels = {}
-    for k, v in prof.items():
-        if not v["launches"]:
-            continue
-        e = {"launches": v["launches"] // prof_steps, "ms_per_step": round(v["total_ms"] / prof_steps, 4),
-             "share": round(v["total_ms"] / total_ms, 4)}
-        if k in fl_tot:
-            tf = fl_tot[k] / (v["total_ms"] / 1e3) / 1e12
-            e.update(tflops=round(tf, 2), tc_frac=round(tf / pk["tc_sus"], 4),
-                     weight_gbs=round(wb_tot[k] / (v["total_ms"] / 1e3) / 1e9, 1))
-        if k == "attention":
-            gbs = ab_tot / (v["total_ms"] / 1e3) / 1e9
-            e.update(kv_gbs=round(gbs, 1), hbm_frac=round(gbs / pk["hbm"], 4))
-        kernels[k] = e
-    # roofline of the dominant kernel (largest share of the step), with per-launch DRAM traffic from the
-    # committed ncu capture (profiles/traffic.json) when present
-    traffic_map = {}
-    tp = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tp):
-        traffic_map = json.load(open(tp)).get("dram_bytes_per_launch", {})
-    cands = [k for k in ("attention", "gemm_gu", "gemm_down", "gemm_qkv", "gemm_o", "gemm_lm") if prof[k]["launches"]]
-    dom = max(cands, key=lambda k: prof[k]["total_ms"])
-    n_l = prof[dom]["launches"]
-    ms_l = prof[dom]["total_ms"] / n_l
-    if dom == "attention":
-        per_launch = ab_tot / n_l
-        ach = per_launch / (ms_l / 1e3) / 1e9
-        roofline = {"bound": "hbm", "kernel": "k_attn_tc (block-diffusion paged attention, tcgen05) per layer",
-                    "achieved": round(ach, 1), "peak": pk["hbm"], "unit": "GB/s", "frac": round(ach / pk["hbm"], 4),
-                    "traffic": traffic_map.get(dom), "algorithmic_bytes_per_launch": round(per_launch),
-                    "peak_src": pk["src"] + " HBM copy"}
-    else:
-        per_launch = fl_tot[dom] / n_l
-        ach = per_launch / (ms_l / 1e3) / 1e12
-        roofline = {"bound": "tensor", "kernel": f"k_gemm_tc ({dom}) per layer", "achieved": round(ach, 2),
-                    "peak": pk["tc_sus"], "unit": "TFLOP/s", "frac": round(ach / pk["tc_sus"], 4),
-                    "traffic": traffic_map.get(dom), "flops_per_launch": round(per_launch),
-                    "peak_src": pk["src"] + " sustained bf16"}
-    roofline.update(launch_ms=round(ms_l, 4), launches_per_step=n_l // prof_steps,
-                    share_of_step=round(prof[dom]["total_ms"] / total_ms, 4),
-                    timing="CUDA events around every launch on the library stream, 2 profiled steps after the timed region")
-    proj = ["gemm_qkv", "gemm_o", "gemm_gu", "gemm_down"]
-    g_ms = sum(prof[k]["total_ms"] for k in proj)
-    g_fl = sum(fl_tot[k] for k in proj)
-    ach_all = g_fl / (g_ms / 1e3) / 1e12
-    roofline_gemms = {"bound": "tensor", "kernel": "all projection GEMMs", "achieved": round(ach_all, 2),
-                      "peak": pk["tc_sus"], "unit": "TFLOP/s", "frac": round(ach_all / pk["tc_sus"], 4),
-                      "share_of_step": round(g_ms / total_ms, 4)}
-    stats = D.all_gather_stats([int(dec), int(launches), int(prefill_s * 1e3)], dev)
+    roof = gemms = kernels = stepr = None
+    if g["prof"] is not None:
+        roof, gemms, kernels, stepr = roofline_report(g["prof"], pk)
+    stats = D.all_gather_stats([int(g["gen_dec"]), len(gids), int(prefill_s * 1e3)], dev)
+    global_batch = int(D.reduce_sum(len(gids), dev))
 
     out = None
     if rank == 0:
         cpu = None if (args.no_cpu_baseline or world > 1) else cpu_baseline(args, run)
-        out = {"metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
-               "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 3), "higher_is_better": True,
-               "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded prompts, random-init weights)",
-               "config": {"workload": f"{run.name}: {run.description}", "model": "SDAR-8B-shaped (random init)",
-                          "requests_per_gpu": n_req, "global_batch": n_req * world, "block": run.method.block_size,
-                          "prompt_len": run.prompt_len, "gen_len": run.gen_len, "seq_len": run.prompt_len + run.gen_len,
-                          "alpha": "3/2", "tau": run.method.conf_threshold, "cache": "DC+",
+        out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+               "warmup": args.warmup, "ms_per_step": round(med["ms"] / args.steps, 3), "higher_is_better": True,
+               "scaling": scaling, "vs_baseline": None, "dtype": "bf16",
+               "data": "synthetic (seeded prompts, random-init weights)",
+               "config": {"workload": f"{run.name}: {run.description}", "model": MODEL_NAME.get(run.name, run.name),
+                          "requests_per_gpu": len(gids), "global_batch": global_batch,
+                          "block": B, "prompt_len": run.prompt_len if run.prompt_len_hi is None else
+                          f"{run.prompt_len}-{run.prompt_len_hi} (uniform, LPT-sharded)",
+                          "gen_len": run.gen_len, "alpha": f"{run.method.alpha_num}/{run.method.alpha_den}",
+                          "tau": run.method.conf_threshold, "cache": "DC+", "logit_scale": run.model.logit_scale,
+                          "batch_invariant": bool(args.batch_invariant),
                           "parallelism": f"request-sharded dp{world}",
                           "l2": "inputs larger than L2 every step (16.4 GB bf16 weights + KV stream)",
-                          "timed_steps_from": f"step {args.warmup + 1} of the decode (context {run.prompt_len}+)",
+                          "timed": f"median of {len(wins)} windows of {args.steps} steps at decode steps {[w['start'] + 1 for w in wins]} of {g['steps_total']}",
                           "prefill_s": round(prefill_s, 2)},
-               "e2e": {"value": round(e2e_val, 2), "unit": UNIT, "h2d_bytes_per_step": 4 * n_req,
-                       "d2h_bytes_per_step": n_req * rsz + 32, "steps": e2e_steps,
-                       "readback": "every step's commit results to pinned host memory, double-buffered"},
-               "gpu_launches": int(launches), "roofline": roofline, "roofline_gemms": roofline_gemms,
-               "kernels": kernels,
-               "clocks": clk.summary(), "decoded_in_window": int(dec_all), "per_rank": stats}
+               "windows": wins,
+               "generation": {"value": round(gen_dec / (gen_ms / 1e3), 2), "decoded": int(gen_dec),
+                              "ms": round(gen_ms, 1), "steps": g["steps_total"],
+                              "note": "every post-warm-up step of the whole generation, device time (profiled steps excluded)"},
+               "e2e": {"value": round(e2e_val, 2), "unit": UNIT, "h2d_bytes_per_step": 4 * len(gids),
+                       "d2h_bytes_per_step": len(gids) * e["rsz"], "steps": e["steps"],
+                       "readback": "every step's commit results to pinned host memory, double-buffered; whole generation after the warm-up"},
+               "gpu_launches": int(med["launches"]),
+               "redundancy": {"layer2plus": round(red_S, 3), "layers01": round(red_P, 3),
+                              "definition": "N_processed / N_decoded over the whole generation (tab:reduce_ratio P:480-504)"},
+               "clocks": clk.summary(), "per_rank": stats}
+        if roof is not None:
+            out.update(roofline=roof, roofline_gemms=gemms, kernels=kernels, step_roofline=stepr)
+        out.update(extras)
         if cpu is not None:
             out["cpu_baseline"] = cpu
         print(json.dumps(out), flush=True)
@@ -402,17 +666,43 @@ def run_reference(args):
     return out
 
 
-def main():
+# ------------------------------------------------------------------------------------ launcher
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def relaunch_cmd(argv, n: int, port: int) -> list:
+    """`bench.py --gpus N` outside torchrun: the same command under torch.distributed.run, one rank
+    per GPU, rendezvous on 127.0.0.1."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+            "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + list(argv)
+
+
+def parse_args(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=30)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="focus", choices=["focus", "reference"])
     ap.add_argument("--workload", default="C3")
+    ap.add_argument("--logit-scale", type=float, default=1.0)
+    ap.add_argument("--batch-invariant", type=int, default=0)
+    ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    args = ap.parse_args()
+    args = ap.parse_args(argv)
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
+    return args
+
+
+def main():
+    args = parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(subprocess.call(relaunch_cmd(sys.argv[1:], args.gpus, _free_port())))
     if args.impl == "reference":
         run_reference(args)
     else:

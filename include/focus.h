@@ -81,6 +81,12 @@ typedef struct {
                               stays far below tau (one fallback decode per step);
                               larger scales make conf >= tau fire for several
                               positions per step ("calibrated" run).  FOCUS_ERR_CONFIG otherwise. */
+  int32_t batch_invariant; /* 1 = a request's results never depend on which other requests share
+                              its steps (S:444 batch invariance, bit for bit): turns off the
+                              attention's load-balancing tail split, whose cut units merge two
+                              partial softmaxes (equal up to fp32 rounding).  Set it when requests
+                              are sharded across GPUs and per-request outputs must be identical at
+                              every world size.  0 = fastest (default).        */
 } focus_config;
 
 typedef struct focus_ctx focus_ctx;
@@ -143,7 +149,9 @@ focus_status focus_set_tap(focus_ctx* ctx, int32_t layer);
 
 enum {
   FOCUS_DBG_STATE = 1,      /* focus_req_state[max_requests]                                 */
-  FOCUS_DBG_COUNTERS = 2,   /* int32[8]: M_P, M_S, M_logit, invariant flag, ...              */
+  FOCUS_DBG_COUNTERS = 2,   /* int32[8] M_P, M_S, M_logit, invariant flag, rows per attention
+                               chunk, chunks per request, 2 pad; then int64[4] cumulative since
+                               focus_init: sum M_P, sum M_S, sum M_logit, steps               */
   FOCUS_DBG_ROWS_P = 3,     /* int32[M_P][4] (slot, j, abs pos, list index) of processed rows */
   FOCUS_DBG_ROWS_S = 4,     /* int32[M_S][4] retained rows                                   */
   FOCUS_DBG_ROWS_L = 5,     /* int32[M_logit][4] logit rows (S cap M)                        */

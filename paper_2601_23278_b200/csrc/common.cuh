@@ -55,6 +55,9 @@ struct Counters {
   int attn_rpc;     // query block rows per attention chunk (importance partials are per chunk)
   int n_chunks;     // chunks per request (ceil(B / attn_rpc))
   int pad[2];
+  // cumulative since focus_init (redundancy statistics, tab:reduce_ratio P:480-504): rows processed
+  // at layers 0-1 (sum M_P), rows kept for the later layers (sum M_S), logit rows (sum M_L), steps
+  long long sum_P, sum_S, sum_L, steps;
 };
 
 struct VocabPartial {   // running (max, sum exp(x - max), argmax) of a vocab chunk
@@ -150,6 +153,9 @@ struct GemmEpi {
 void launch_gemm(const bf16* A, int lda, int a_rows, const bf16* W, int N, int K, float* C, int ldc,
                  const int* M_dev, int M_max, GemmMode mode, const GemmWs& ws, cudaStream_t s, int m_est = 0);
 int gemm_backend();
+// tile configuration a tensor-core GEMM of this shape takes at m_est expected live rows (the graph
+// cache keys on it; kernels_gemm_tc.cu)
+int gemm_tc_choice(int N, int K, GemmMode mode, int M_max, int m_est);
 int num_sms();
 void gemm_set_backend(int b);
 

@@ -34,6 +34,7 @@ void launch_gemm(const bf16* A, int lda, int a_rows, const bf16* W, int N, int K
 namespace {
 
 constexpr int kTapCount = 10;
+constexpr size_t kMaxGraphs = 32;    // whole-step graphs kept (least recently used evicted)
 enum { TAP_X_IN = 0, TAP_H, TAP_QKV, TAP_ATTN, TAP_X_MID, TAP_H2, TAP_ACT, TAP_X_OUT, TAP_QS, TAP_ROWS };
 
 struct Upload {                 // pinned staging ring for small host->device copies
@@ -126,10 +127,10 @@ struct focus_ctx {
   std::vector<int> prof_kind;                    // per record
   focus_prof_entry prof_acc[FOCUS_PROF_KINDS];
   // whole-step CUDA graphs: the launch sequence of focus_step_block for one request
-  // list and one tile-shape estimate bucket, captured once and replayed
+  // list and one set of GEMM tile configurations, captured once and replayed
   struct StepGraph {
     std::vector<int32_t> list;
-    int bucket[3];
+    std::vector<int> key;           // tile configurations of the step's GEMMs (shape_key)
     cudaGraphExec_t exec = nullptr;
     int32_t* list_host = nullptr;   // pinned copy of the list: the captured H2D copy reads it
     uint64_t launches = 0;
@@ -167,6 +168,7 @@ bool valid_config(const focus_config& c) {
   const int G = c.n_q_heads / c.n_kv_heads;
   if (G > kAttnQRows) return false;
   if ((c.n_q_heads * c.head_dim) % 64) return false;
+  if (c.batch_invariant < 0 || c.batch_invariant > 1) return false;
   if (c.logit_scale != 0.f) {                     // a power of two in [2^-16, 2^16] (W_lm stays exact)
     int e = 0;
     const float m = std::frexp(c.logit_scale, &e);
@@ -471,7 +473,7 @@ AttnArgs attn_args(focus_ctx* x, int l, const bf16* q, int ldq, int n_req, const
   a.stream_k = getenv("FOCUS_ATTN_SK") ? 1 : 0;   // opt-in stream-K (measured slower than the tail split)
   // tail split on by default (FOCUS_ATTN_TAIL=0: off): with the bulk-store epilogue and evict-first KV
   // loads it shortens the layer launch by ~10% (clock64 trace) and the C3 step by ~1.5%
-  a.tail_split = (getenv("FOCUS_ATTN_TAIL") && getenv("FOCUS_ATTN_TAIL")[0] == '0') ? 0 : 1;
+  a.tail_split = (x->cfg.batch_invariant || (getenv("FOCUS_ATTN_TAIL") && getenv("FOCUS_ATTN_TAIL")[0] == '0')) ? 0 : 1;
   a.l2_prefetch = getenv("FOCUS_ATTN_PF") ? std::max(0, atoi(getenv("FOCUS_ATTN_PF"))) : 0;   // opt-in
   a.nch_fixed = getenv("FOCUS_ATTN_NCH4") ? 1 : 0;
   a.page_skip = (getenv("FOCUS_ATTN_PAGESKIP") && getenv("FOCUS_ATTN_PAGESKIP")[0] == '0') ? 0 : 1;
@@ -774,25 +776,30 @@ focus_status focus_step_block(focus_ctx* x, const int32_t* ids, int32_t n_req) {
   return cuda_status(cudaGetLastError());
 }
 
-static focus_status step_graph(focus_ctx* x, const int32_t* ids, int32_t n_req, bool same_list) {
-  focus_status rc;
-  // graph key: the request list and the tile-shape estimate the launch sequence bakes in (the number
-  // of 256-row tiles of the P, S and logit rows); device-side sizes keep any replay exact
-  const int bucket[3] = {(x->est.M_P + 255) / 256, (x->est.M_S + 255) / 256, (x->est.M_L + 255) / 256};
-  ++x->graph_clock;
-  for (auto& g : x->graphs) {
-    if (g.list.size() != (size_t)n_req || !std::equal(ids, ids + n_req, g.list.begin())) continue;
-    if (g.bucket[0] != bucket[0] || g.bucket[1] != bucket[1] || g.bucket[2] != bucket[2]) continue;
-    g.last_use = x->graph_clock;
-    x->launches += g.launches;
-    x->last_list = x->pending_list;
-    return cuda_status(cudaGraphLaunch(g.exec, x->stream));
+// The launch choices a step bakes in: the tile configuration of every GEMM shape of the step at this
+// step's row-count estimates (P rows: layers 0-1; S rows: layer-1 suffix and layers >= 2; logit rows).
+static std::vector<int> shape_key(const focus_ctx* x, int maxP, const Counters& e) {
+  const focus_config& c = x->cfg;
+  std::vector<int> k;
+  if (gemm_backend() != 1) return k;
+  const GemmMode qm = fused_qkv(x) ? GEMM_QKV_ROPE : GEMM_STORE;
+  for (int m : {e.M_P, e.M_S}) {
+    k.push_back(gemm_tc_choice(x->qkv_dim, c.d_model, qm, maxP, m));
+    k.push_back(gemm_tc_choice(c.d_model, x->q_dim, GEMM_ADD, maxP, m));
+    k.push_back(gemm_tc_choice(2 * c.d_ff, c.d_model, GEMM_SWIGLU, maxP, m));
+    k.push_back(gemm_tc_choice(c.d_model, c.d_ff, GEMM_ADD, maxP, m));
   }
-  // capture only in a steady state (the same list as the previous step); otherwise launch eagerly
-  if (!same_list) return enqueue_step(x, ids, n_req);
+  k.push_back(gemm_tc_choice(c.vocab, c.d_model, GEMM_STORE, maxP, e.M_L));
+  return k;
+}
+
+// Capture the step's launch sequence for the row-count estimate e into a new graph of the cache.
+static focus_status capture_graph(focus_ctx* x, const int32_t* ids, int32_t n_req, const Counters& e,
+                                  const std::vector<int>& key) {
+  focus_status rc;
   focus_ctx::StepGraph g;
   g.list.assign(ids, ids + n_req);
-  for (int i = 0; i < 3; ++i) g.bucket[i] = bucket[i];
+  g.key = key;
   if (cudaMallocHost(&g.list_host, (size_t)n_req * 4) != cudaSuccess) return FOCUS_ERR_CUDA;
   std::memcpy(g.list_host, ids, (size_t)n_req * 4);
   cudaGraph_t graph = nullptr;
@@ -804,9 +811,13 @@ static focus_status step_graph(focus_ctx* x, const int32_t* ids, int32_t n_req, 
   // capture on the private stream (capturing the legacy default stream is not allowed); the graph is
   // then launched on the context stream, so stream order is unchanged
   cudaStream_t user = x->stream;
+  const Counters est_saved = x->est;
+  const std::vector<int32_t> last_saved = x->last_list;
+  x->est = e;
   x->stream = x->cap_stream;
   if ((rc = cuda_status(cudaStreamBeginCapture(x->stream, cudaStreamCaptureModeThreadLocal))) != FOCUS_OK) {
     x->stream = user;
+    x->est = est_saved;
     cudaFreeHost(g.list_host);
     return rc;
   }
@@ -815,16 +826,19 @@ static focus_status step_graph(focus_ctx* x, const int32_t* ids, int32_t n_req, 
   x->upload_src = nullptr;
   const cudaError_t ec = cudaStreamEndCapture(x->stream, &graph);
   x->stream = user;
+  x->est = est_saved;
+  x->last_list = last_saved;
   if (rc == FOCUS_OK && ec == cudaSuccess) rc = cuda_status(cudaGraphInstantiate(&g.exec, graph, 0));
   else if (rc == FOCUS_OK) rc = cuda_status(ec);
   if (graph) cudaGraphDestroy(graph);
+  g.launches = x->launches - l0;
+  x->launches = l0;                               // capturing launches nothing
   if (rc != FOCUS_OK) {
     cudaFreeHost(g.list_host);
     return rc;
   }
-  g.launches = x->launches - l0;
   g.last_use = x->graph_clock;
-  if (x->graphs.size() >= 32) {   // keep the 32 most recently used
+  if (x->graphs.size() >= kMaxGraphs) {            // keep the most recently used
     auto lru = std::min_element(x->graphs.begin(), x->graphs.end(),
                                 [](const focus_ctx::StepGraph& a, const focus_ctx::StepGraph& b) { return a.last_use < b.last_use; });
     cudaGraphExecDestroy(lru->exec);
@@ -832,7 +846,57 @@ static focus_status step_graph(focus_ctx* x, const int32_t* ids, int32_t n_req, 
     x->graphs.erase(lru);
   }
   x->graphs.push_back(g);
-  return cuda_status(cudaGraphLaunch(x->graphs.back().exec, x->stream));
+  return FOCUS_OK;
+}
+
+static focus_ctx::StepGraph* find_graph(focus_ctx* x, const int32_t* ids, int32_t n_req, const std::vector<int>* key) {
+  for (auto& g : x->graphs) {
+    if (g.list.size() != (size_t)n_req || !std::equal(ids, ids + n_req, g.list.begin())) continue;
+    if (key == nullptr || g.key == *key) return &g;
+  }
+  return nullptr;
+}
+
+static focus_status step_graph(focus_ctx* x, const int32_t* ids, int32_t n_req, bool same_list) {
+  // graph key: the request list and the GEMM tile configurations the launch sequence bakes in;
+  // device-side row counts keep any replay exact
+  const int maxP = n_req * x->B;
+  const std::vector<int> key = shape_key(x, maxP, x->est);
+  ++x->graph_clock;
+  focus_ctx::StepGraph* g = find_graph(x, ids, n_req, &key);
+  if (g == nullptr) {
+    // capture only in a steady state (the same list as the previous step); otherwise launch eagerly
+    if (!same_list) return enqueue_step(x, ids, n_req);
+    focus_status rc;
+    if (find_graph(x, ids, n_req, nullptr) == nullptr) {
+      // first steady-state step of this list: capture every tile configuration its row counts can
+      // select (estimates of 1 .. maxP/256 pair tiles per row space), so no capture lands in a
+      // later step
+      std::vector<std::vector<int>> seen;
+      const int mp = (maxP + 255) / 256;
+      for (int a = 1; a <= mp; ++a)
+        for (int b = 1; b <= mp; ++b)
+          for (int l = 1; l <= mp; ++l) {
+            Counters e = x->est;
+            e.M_P = std::min(a * 256, maxP);
+            e.M_S = std::min(b * 256, maxP);
+            e.M_L = std::min(l * 256, maxP);
+            const std::vector<int> k = shape_key(x, maxP, e);
+            if (std::find(seen.begin(), seen.end(), k) != seen.end() || seen.size() >= kMaxGraphs / 2) continue;
+            seen.push_back(k);
+            if ((rc = capture_graph(x, ids, n_req, e, k)) != FOCUS_OK) return rc;
+          }
+    }
+    g = find_graph(x, ids, n_req, &key);
+    if (g == nullptr) {
+      if ((rc = capture_graph(x, ids, n_req, x->est, key)) != FOCUS_OK) return rc;
+      g = &x->graphs.back();
+    }
+  }
+  g->last_use = x->graph_clock;
+  x->launches += g->launches;
+  x->last_list = x->pending_list;
+  return cuda_status(cudaGraphLaunch(g->exec, x->stream));
 }
 
 static focus_status enqueue_step(focus_ctx* x, const int32_t* ids, int32_t n_req) {

@@ -1071,66 +1071,88 @@ static bool launch_pair(const bf16* A, int lda, int a_rows, const bf16* W, int N
 
 // m_est: expected live row count (host estimate, e.g. last step's counter) used only to pick the tile
 // width: 128-wide tiles when 256-wide tiles would leave more than ~half of the SMs idle.
+// Tile configuration of a tensor-core GEMM of shape (N, K, mode) at an expected live row count m:
+// the ONLY host decision that depends on the row-count estimate (grids come from M_max).  The
+// whole-step graph cache keys on these choices, so a captured graph is replayed exactly when the
+// eager sequence would launch the same kernels.
+enum { GC_SPLIT = 1, GC_128x2, GC_256x2, GC_128x1, GC_256x1, GC_SINGLE_128, GC_SINGLE_256 };
+static int split_parts(int K) {
+  // ordered split into S k-ranges (at least 8 k-blocks each, S units in one wave): two ranges for deep
+  // K at the C3 shapes.  S up to 4 (FOCUS_GEMM_SPLIT_MAX) was measured slower on the C2 shapes (O
+  // 0.53 -> 0.93 ms/step: the ordered chain of residual adds costs more than the extra SMs give)
+  static int s_cap = -1, s2_env = -1, s2_mink = -1;
+  if (s_cap < 0) {
+    const char* e = getenv("FOCUS_GEMM_SPLIT_MAX");
+    s_cap = e ? std::max(2, std::min(4, atoi(e))) : 2;
+    // GEMM_ADD whose 256-wide units fit one wave twice over: 256-wide tiles with ordered split-K
+    // (FOCUS_GEMM_SPLIT2=0: off) instead of 128-wide tiles, halving the activation re-reads
+    e = getenv("FOCUS_GEMM_SPLIT2");
+    s2_env = (e && e[0] == '0') ? 0 : 1;
+    // (measured at M = 428: down, K = 12288, 57 -> 53 us; O, K = 4096, 29 -> 33 us, so only for deep K)
+    e = getenv("FOCUS_GEMM_SPLIT2_MINK");
+    s2_mink = e ? std::max(256, atoi(e)) : 8192;
+  }
+  if (!s2_env || K < s2_mink) return 1;
+  const int sp = std::min(s_cap, K / tc::BK / 8);
+  return sp >= 2 ? sp : 1;
+}
+
+static int env_flag(const char* name, int& cache) {
+  if (cache < 0) cache = getenv(name) != nullptr ? 1 : 0;
+  return cache;
+}
+
+int gemm_tc_choice(int N, int K, GemmMode mode, int M_max, int m_est) {
+  using namespace tc;
+  const int m = m_est > 0 ? std::min(m_est, M_max) : M_max;
+  static int bn256 = -1, bn128 = -1, pair_env = -1, ka_env = -1;
+  const bool force256 = env_flag("FOCUS_GEMM_BN256", bn256) != 0;
+  if (pair_env < 0) {   // CTA-pair tiles by default; FOCUS_GEMM_PAIR=0: one CTA per tile
+    const char* e = getenv("FOCUS_GEMM_PAIR");
+    pair_env = !(e && e[0] == '0');
+  }
+  if (pair_env) {
+    const long long units256 = (long long)((m + 2 * BM - 1) / (2 * BM)) * ((N + 255) / 256);
+    const bool narrow2 = mode != GEMM_SWIGLU && !force256 &&
+                         (4 * units256 <= (num_sms() * 11) / 10 || env_flag("FOCUS_GEMM_BN128", bn128));
+    // k-atoms per stage (measured at the C3 shapes): 2 for 128-wide tiles (4 stages of 48 KB), 1 for
+    // 256-wide tiles (6 stages of 32 KB); FOCUS_GEMM_KA=1|2 forces one
+    if (ka_env < 0) {
+      const char* e = getenv("FOCUS_GEMM_KA");
+      ka_env = (e && (e[0] == '1' || e[0] == '2')) ? e[0] - '0' : 0;
+    }
+    const int ka = ka_env ? ka_env : (narrow2 ? 2 : 1);
+    // the split decision uses the GEMM's shape only (K), never the row count, so results are batch
+    // invariant
+    if (mode == GEMM_ADD && ka_env == 0 && split_parts(K) >= 2) return GC_SPLIT;
+    if (ka == 2 && K % (2 * BK) == 0) return narrow2 ? GC_128x2 : GC_256x2;
+    return narrow2 ? GC_128x1 : GC_256x1;
+  }
+  const long long tiles256 = (long long)((m + BM - 1) / BM) * ((N + 255) / 256);
+  const bool narrow = mode != GEMM_SWIGLU && 2 * tiles256 <= (num_sms() * 11) / 10 && !force256;
+  return narrow ? GC_SINGLE_128 : GC_SINGLE_256;
+}
+
+// m_est: expected live row count (host estimate, e.g. last step's counter) used only to pick the tile
+// width: 128-wide tiles when 256-wide tiles would leave more than ~half of the SMs idle.
 bool launch_gemm_tc(const bf16* A, int lda, int a_rows, const bf16* W, int N, int K, float* C, int ldc, const int* M_dev,
                     int M_max, GemmMode mode, const GemmWs& ws, cudaStream_t s, const GemmEpi* epi, int m_est) {
   using namespace tc;
   if (M_max <= 0) return true;
   if (K % BK || lda % 8 || a_rows < 1) return false;
   const int m = m_est > 0 ? std::min(m_est, M_max) : M_max;
-  const long long tiles256 = (long long)((m + BM - 1) / BM) * ((N + 255) / 256);
-  const bool narrow = mode != GEMM_SWIGLU && 2 * tiles256 <= (num_sms() * 11) / 10 && getenv("FOCUS_GEMM_BN256") == nullptr;
-  // opt-in (FOCUS_GEMM_MC=1): clusters of 4 CTAs (the 4 m-tiles of a weight tile) share W by TMA
-  // multicast when the live row count fills them.  Measured no faster at the C3 shapes (at cluster
-  // size <= 4 the L2 already serves the duplicate requests once), so one CTA per tile by default.
-  const char* pm_e = getenv("FOCUS_GEMM_PAIR");   // CTA-pair tiles by default; FOCUS_GEMM_PAIR=0: one CTA per tile
-  const bool pair_mode = !(pm_e && pm_e[0] == '0');
-  if (pair_mode) {
-    const long long units256 = (long long)((m + 2 * BM - 1) / (2 * BM)) * ((N + 255) / 256);
-    const bool narrow2 = mode != GEMM_SWIGLU && getenv("FOCUS_GEMM_BN256") == nullptr &&
-                         (4 * units256 <= (num_sms() * 11) / 10 || getenv("FOCUS_GEMM_BN128") != nullptr);
-    // k-atoms per stage (measured at the C3 shapes): 2 for 128-wide tiles (4 stages of 48 KB), 1 for
-    // 256-wide tiles (6 stages of 32 KB); FOCUS_GEMM_KA=1|2 forces one
-    static int ka_env = -1;
-    if (ka_env < 0) {
-      const char* e = getenv("FOCUS_GEMM_KA");
-      ka_env = (e && (e[0] == '1' || e[0] == '2')) ? e[0] - '0' : 0;
-    }
-    const int ka = ka_env ? ka_env : (narrow2 ? 2 : 1);
-    // GEMM_ADD whose 256-wide units fit one wave twice over: 256-wide tiles with ordered split-K
-    // (FOCUS_GEMM_SPLIT2=0: off) instead of 128-wide tiles, halving the activation re-reads
-    static int s2_env = -1;
-    if (s2_env < 0) {
-      const char* e = getenv("FOCUS_GEMM_SPLIT2");
-      s2_env = (e && e[0] == '0') ? 0 : 1;
-    }
-    // (measured at M = 428: down, K = 12288, 57 -> 53 us; O, K = 4096, 29 -> 33 us, so only for deep K)
-    static int s2_mink = -1;
-    if (s2_mink < 0) {
-      const char* e = getenv("FOCUS_GEMM_SPLIT2_MINK");
-      s2_mink = e ? std::max(256, atoi(e)) : 8192;
-    }
-    // ordered split into S k-ranges (at least 8 k-blocks each, S units in one wave): two ranges for deep
-    // K at the C3 shapes.  S up to 4 (FOCUS_GEMM_SPLIT_MAX) was measured slower on the C2 shapes (O
-    // 0.53 -> 0.93 ms/step: the ordered chain of residual adds costs more than the extra SMs give)
-    static int s_cap = -1;
-    if (s_cap < 0) {
-      const char* e = getenv("FOCUS_GEMM_SPLIT_MAX");
-      s_cap = e ? std::max(2, std::min(4, atoi(e))) : 2;
-    }
-    // the decision uses the GEMM's shape only (K >= FOCUS_GEMM_SPLIT2_MINK), never the row count, so
-    // results are batch invariant
-    if (s2_env && mode == GEMM_ADD && ka_env == 0 && K >= s2_mink) {
-      const int ks_n = K / BK;
-      const int sp = std::min(s_cap, ks_n / 8);
-      if (sp >= 2) return launch_pair<256, 1>(A, lda, a_rows, W, N, K, C, ldc, M_dev, M_max, mode, ws, s, epi, m, sp);
-    }
-    if (ka == 2 && K % (2 * BK) == 0) {
-      if (narrow2) return launch_pair<128, 2>(A, lda, a_rows, W, N, K, C, ldc, M_dev, M_max, mode, ws, s, epi, m);
-      return launch_pair<256, 2>(A, lda, a_rows, W, N, K, C, ldc, M_dev, M_max, mode, ws, s, epi, m);
-    }
-    if (narrow2) return launch_pair<128, 1>(A, lda, a_rows, W, N, K, C, ldc, M_dev, M_max, mode, ws, s, epi, m);
-    return launch_pair<256, 1>(A, lda, a_rows, W, N, K, C, ldc, M_dev, M_max, mode, ws, s, epi, m);
+  switch (gemm_tc_choice(N, K, mode, M_max, m_est)) {
+    case GC_SPLIT: return launch_pair<256, 1>(A, lda, a_rows, W, N, K, C, ldc, M_dev, M_max, mode, ws, s, epi, m, split_parts(K));
+    case GC_128x2: return launch_pair<128, 2>(A, lda, a_rows, W, N, K, C, ldc, M_dev, M_max, mode, ws, s, epi, m);
+    case GC_256x2: return launch_pair<256, 2>(A, lda, a_rows, W, N, K, C, ldc, M_dev, M_max, mode, ws, s, epi, m);
+    case GC_128x1: return launch_pair<128, 1>(A, lda, a_rows, W, N, K, C, ldc, M_dev, M_max, mode, ws, s, epi, m);
+    case GC_256x1: return launch_pair<256, 1>(A, lda, a_rows, W, N, K, C, ldc, M_dev, M_max, mode, ws, s, epi, m);
+    default: break;
   }
+  // opt-in (FOCUS_GEMM_PAIR=0): one CTA per tile; (FOCUS_GEMM_MC=1) clusters of 4 CTAs (the 4 m-tiles
+  // of a weight tile) share W by TMA multicast when the live row count fills them.  Measured no
+  // faster at the C3 shapes (at cluster size <= 4 the L2 already serves the duplicate requests once)
+  const bool narrow = gemm_tc_choice(N, K, mode, M_max, m_est) == GC_SINGLE_128;
   const int m_tiles = (m + BM - 1) / BM;
   const bool cluster4 = getenv("FOCUS_GEMM_MC") != nullptr && m_tiles % 4 == 0;
   if (narrow) {

@@ -92,6 +92,8 @@ __global__ void __launch_bounds__(1024) k_step_setup(const int* __restrict__ req
   if (threadIdx.x == 0) {
     offP[n_req] = carry;
     cnt->M_P = carry;
+    cnt->sum_P += carry;
+    cnt->steps += 1;
   }
 }
 

@@ -190,6 +190,8 @@ __global__ void __launch_bounds__(1024) k_select_plan(SelectArgs a) {
     a.offL[a.n_req] = carryL;
     a.cnt->M_S = carryS;
     a.cnt->M_L = carryL;
+    a.cnt->sum_S += carryS;
+    a.cnt->sum_L += carryL;
   }
 }
 

@@ -51,6 +51,16 @@ def reduce_max(value: float, device=None) -> float:
     return float(t.item())
 
 
+def reduce_min(value: float, device=None) -> float:
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()):
+        return value
+    t = torch.tensor([value], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MIN)
+    return float(t.item())
+
+
 def reduce_sum(value: float, device=None) -> float:
     import torch
     import torch.distributed as dist

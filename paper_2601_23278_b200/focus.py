@@ -39,7 +39,7 @@ class focus_config(C.Structure):
                 ("placeholder_mode", C.c_int32), ("strategy", C.c_int32), ("fixed_k", C.c_int32),
                 ("max_requests", C.c_int32), ("max_seq_len", C.c_int32), ("page_size", C.c_int32),
                 ("max_prefill_chunk", C.c_int32), ("kv_pages", C.c_int64), ("weight_seed", C.c_uint64),
-                ("debug_taps", C.c_int32), ("logit_scale", C.c_float)]
+                ("debug_taps", C.c_int32), ("logit_scale", C.c_float), ("batch_invariant", C.c_int32)]
 
 
 class focus_commit_result(C.Structure):
@@ -102,7 +102,8 @@ def _check(rc: int, where: str):
 
 
 def make_config(run, max_requests: Optional[int] = None, max_seq_len: Optional[int] = None,
-                max_prefill_chunk: int = 1024, debug_taps: bool = False, kv_pages: int = 0) -> focus_config:
+                max_prefill_chunk: int = 1024, debug_taps: bool = False, kv_pages: int = 0,
+                batch_invariant: bool = False) -> focus_config:
     """focus_config from a synth.RunConfig (plain data)."""
     m, me = run.model, run.method
     if max_seq_len is None:
@@ -116,7 +117,7 @@ def make_config(run, max_requests: Optional[int] = None, max_seq_len: Optional[i
         placeholder_mode=me.placeholder_mode, strategy=me.strategy, fixed_k=me.fixed_k,
         max_requests=max_requests or run.n_requests, max_seq_len=max_seq_len, page_size=run.page_size,
         max_prefill_chunk=max_prefill_chunk, kv_pages=kv_pages, weight_seed=run.weight_seed,
-        debug_taps=1 if debug_taps else 0, logit_scale=m.logit_scale)
+        debug_taps=1 if debug_taps else 0, logit_scale=m.logit_scale, batch_invariant=1 if batch_invariant else 0)
 
 
 def focus_required_bytes(cfg: focus_config) -> int:
@@ -233,7 +234,13 @@ class FocusContext:
         return list(arr)
 
     def counters(self) -> np.ndarray:
-        return np.frombuffer(self.focus_debug_export("COUNTERS", cap=32), dtype=np.int32).copy()
+        """int32[8]: M_P, M_S, M_logit, invariant, rows per attention chunk, chunks, pad, pad."""
+        return np.frombuffer(self.focus_debug_export("COUNTERS", cap=64)[:32], dtype=np.int32).copy()
+
+    def cumulative_rows(self) -> dict:
+        """Rows processed since focus_init: sum M_P, sum M_S, sum M_logit and the step count."""
+        a = np.frombuffer(self.focus_debug_export("COUNTERS", cap=64)[32:64], dtype=np.int64)
+        return dict(sum_P=int(a[0]), sum_S=int(a[1]), sum_L=int(a[2]), steps=int(a[3]))
 
     def rows(self, which: str) -> np.ndarray:
         return np.frombuffer(self.focus_debug_export("ROWS_" + which), dtype=np.int32).reshape(-1, 4).copy()

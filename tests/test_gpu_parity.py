@@ -298,3 +298,31 @@ def test_committed_kv_slots_never_rewritten(model):
                 for p in range(run.prompt_len):
                     frozen.setdefault((r, l, p), K[p].copy())
         live = [x["req_id"] for x in res if not x["finished"]]
+
+
+@pytest.mark.parametrize("model", [GQA_TC, GQA_TC_DEEPFF], ids=["tc", "tc_splitk"])
+def test_sharding_invariance_batch_invariant(model):
+    """SURVEY 8(e) / tier T5: with batch_invariant = 1, LPT-sharding a mixed-length batch over world
+    sizes 1, 2 and 4 (each shard its own context, as on its own GPU) gives every request exactly the
+    same committed tokens (logit_scale 16: multi-token commits, so block phases differ by request)."""
+    from paper_2601_23278_b200 import dist as D
+    from paper_2601_23278_b200.runner import generate
+    mdl = dataclasses.replace(model, logit_scale=16.0)
+    run = get_config("C1").with_(model=mdl, method=MethodConfig(block_size=16), n_requests=8, prompt_len=20,
+                                 prompt_len_hi=300, gen_len=32, page_size=64)
+    prompts = request_prompts(run)
+    costs = [len(p) + run.gen_len / 2 for p in prompts]
+    outs = {}
+    for world in (1, 2, 4):
+        toks = {}
+        for rank in range(world):
+            mine = D.shard_requests(run.n_requests, world, rank, costs)
+            ctx = _ctx(run, max_requests=len(mine), batch_invariant=True)
+            for slot, g in enumerate(mine):
+                ctx.focus_kv_append(slot, prompts[g], run.gen_len)
+            generate(ctx, list(range(len(mine))), keep_log=False)
+            for slot, g in enumerate(mine):
+                toks[g] = ctx.focus_get_tokens(slot)
+            del ctx
+        outs[world] = toks
+    assert outs[1] == outs[2] == outs[4]
