@@ -2,6 +2,9 @@
 through the tap buffers of the C ABI: the oracle is fed each stage's GPU input and compared with the
 stage's GPU output.  Shapes span several GEMM tiles with ragged M,
 several KV pages, GQA packing and block sizes 4/16."""
+import json
+import os
+
 import numpy as np
 import pytest
 
@@ -30,9 +33,23 @@ MINI_G2 = ModelConfig(n_layers=3, d_model=512, n_q_heads=8, n_kv_heads=4, head_d
                       rope_theta=1e6)
 
 
-# GEMM stage tolerance: fp32 accumulation on the tensor core over K <= 12288 (DESIGN.md §7 "numerics":
-# the MMA's internal accumulation order is not the fp64 reference order; ~sqrt(K) * 2^-23 relative)
-GEMM_TOL = 5e-5
+# GEMM stage tolerance (DESIGN.md §7 "numerics"): the tensor core accumulates the K bf16 products in
+# fp32 in its own order; the rounding errors of the partial sums add up like a random walk, ~sqrt(K) * u
+# relative (u = 2^-24).  Bound: 3 sqrt(K) u (K = 12288: 2.0e-5; K = 4096: 1.1e-5).  Measured on B200
+# (profiles/r2_gemm_errors.jsonl, every stage of this test): max 7.1e-6 at K = 6144 / 12288, 3.5e-6 at
+# K = 4096, i.e. at most half the bound.
+def gemm_tol(K):
+    return 3.0 * np.sqrt(K) * 2.0 ** -24
+
+
+
+def _log_err(stage, K, err):
+    """Append a measured GEMM stage error to $FOCUS_TEST_LOG (JSON lines) when set: the distribution
+    behind gemm_tol (profiles/r2_gemm_errors.jsonl)."""
+    path = os.environ.get("FOCUS_TEST_LOG")
+    if path:
+        with open(path, "a") as f:
+            f.write(json.dumps({"stage": stage, "K": int(K), "rel_l2": float(err)}) + "\n")
 
 
 def _bf16_close(got, want, tag, frac=0.95, tol=4e-3):
@@ -87,6 +104,9 @@ def test_layer_stages(model, B, nreq, prompt, taps, page):
         k_o = bf16_round(rope(f32(y[:, qd:qd + hkv * dh].reshape(Mq, hkv, dh)), pos, model.rope_theta)).reshape(Mq, -1)
         v_o = bf16_round(y[:, qd + hkv * dh:])
         _bf16_close(qkv, np.concatenate([q_o, k_o, v_o], 1), ("qkv+rope", l))
+        # the QKV GEMM before its bf16 rounding is not exported; its fp32 accumulation shows in the
+        # fraction of bf16 outputs identical to the fp64 reference's rounding
+        _log_err("qkv bf16-mismatch-fraction", d, 1.0 - float(np.mean(qkv == np.concatenate([q_o, k_o, v_o], 1))))
         # importance (layers 0, 1) from the GPU's q, k over P
         if l <= 1:
             Iraw = np.frombuffer(ctx.focus_debug_export("I0" if l == 0 else "I1"), np.float32)
@@ -127,14 +147,16 @@ def test_layer_stages(model, B, nreq, prompt, taps, page):
             x_res = x_in
         x_mid = ctx.export_f32("TAP_X_MID", (Ma, d)).astype(np.float64)
         inc = att @ w["o"].T
-        assert rel_l2(x_mid - x_res, inc) < GEMM_TOL, ("o-proj", l, rel_l2(x_mid - x_res, inc))
+        _log_err("o-proj", qd, rel_l2(x_mid - x_res, inc))
+        assert rel_l2(x_mid - x_res, inc) < gemm_tol(qd), ("o-proj", l, rel_l2(x_mid - x_res, inc))
         h2 = ctx.export_bf16("TAP_H2", (Ma, d))
         _bf16_close(h2, bf16_round(rms_norm(x_mid, 1.0, model.rms_eps)), ("rmsnorm2", l), frac=0.99)
         act = ctx.export_bf16("TAP_ACT", (Ma, model.d_ff))
         _bf16_close(act, bf16_round(silu(f32(h2 @ w["gate"].T)) * f32(h2 @ w["up"].T)), ("swiglu", l))
         x_out = ctx.export_f32("TAP_X_OUT", (Ma, d)).astype(np.float64)
         inc = act @ w["down"].T
-        assert rel_l2(x_out - x_mid, inc) < GEMM_TOL, ("down", l, rel_l2(x_out - x_mid, inc))
+        _log_err("down", model.d_ff, rel_l2(x_out - x_mid, inc))
+        assert rel_l2(x_out - x_mid, inc) < gemm_tol(model.d_ff), ("down", l, rel_l2(x_out - x_mid, inc))
         # LM head on S cap M rows (sampled vocab columns) after the last layer
         if l == model.n_layers - 1 and ML:
             hl = ctx.export_bf16("HL", (ML, d))
@@ -143,7 +165,8 @@ def test_layer_stages(model, B, nreq, prompt, taps, page):
             logits = ctx.export_f32("LOGITS", (ML, model.vocab))
             for lo in (0, model.vocab - 2048):
                 wl = weight_matrix(TID_LMHEAD, model.vocab, d, d, run.weight_seed, lo, lo + 2048).astype(np.float64)
-                assert rel_l2(logits[:, lo:lo + 2048], hl @ wl.T) < GEMM_TOL, ("lm-head", lo)
+                _log_err("lm-head", d, rel_l2(logits[:, lo:lo + 2048], hl @ wl.T))
+                assert rel_l2(logits[:, lo:lo + 2048], hl @ wl.T) < gemm_tol(d), ("lm-head", lo)
         ctx.commit_results(live)
     ctx.focus_set_tap(-1)
     ctx.focus_sync()
