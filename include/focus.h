@@ -157,7 +157,9 @@ enum {
   FOCUS_DBG_ROWS_L = 5,     /* int32[M_logit][4] logit rows (S cap M)                        */
   FOCUS_DBG_I0 = 6,         /* float[n_req][n_kv_heads][B] per-kv-head partial importance    */
   FOCUS_DBG_I1 = 7,
-  FOCUS_DBG_LOGITS = 8,     /* float[M_logit][vocab]                                         */
+  FOCUS_DBG_LOGITS = 8,     /* float[M_logit][vocab] (stored only when cfg.debug_taps = 1: the LM
+                               head's epilogue otherwise emits just the per-row confidence
+                               statistics, and the logits never reach HBM)                   */
   FOCUS_DBG_TOKCONF = 9,    /* struct {int32 tok; float conf;}[M_logit]                      */
   FOCUS_DBG_KV_K = 10,      /* bf16[s+B][n_kv_heads][head_dim] of (req_id, layer)            */
   FOCUS_DBG_KV_V = 11,

@@ -148,6 +148,9 @@ struct GemmEpi {
   const AttnUnit* pf_units;            // plan [pf_grid][pf_ucap] (nullptr: off)
   const int* pf_n;                     // [pf_grid] units per attention CTA
   int pf_grid, pf_ucap, pf_tiles;
+  // STORE (LM head): per row and 64-column group, (max, sum exp(z - max), lowest argmax) of the logits
+  // (mask id excluded) -> vpart[row][group] (ld vp_ld); C may then be nullptr (logits never stored)
+  VocabPartial* vpart; int vp_ld; int mask_id;
 };
 // a_rows: allocated rows of A (TMA bounds); M_dev/M_max: live / maximum rows of this call.
 void launch_gemm(const bf16* A, int lda, int a_rows, const bf16* W, int N, int K, float* C, int ldc,
@@ -220,6 +223,9 @@ void launch_select_plan(const SelectArgs& a, cudaStream_t s);
 
 void launch_vocab_reduce(const float* logits, const int* M_dev, int M_max, int V, int mask_id, int nch,
                          VocabPartial* part, cudaStream_t s);
+// combine the LM-head epilogue's per-64-column partials of each logit row (fixed order) -> out[row]
+void launch_vocab_combine(const VocabPartial* tiles, int ngroups, const int* M_dev, int M_max, VocabPartial* out,
+                          cudaStream_t s);
 
 struct CommitArgs {
   const int* req_list; int n_req;

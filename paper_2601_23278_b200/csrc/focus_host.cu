@@ -96,6 +96,8 @@ struct focus_ctx {
   Counters* cnt = nullptr;
   float *I0p = nullptr, *I1p = nullptr;
   VocabPartial* vpart = nullptr;
+  VocabPartial* vtiles = nullptr;  // LM-head epilogue partials [logit row][64-column group]
+  bool vocab_fused = false;        // LM head emits vtiles (tensor-core GEMM); logits stored only with taps
   TokConf* tokconf = nullptr;
   focus_commit_result* res_dev = nullptr;
   GemmWs gws{};
@@ -242,6 +244,7 @@ size_t carve(focus_ctx* x, char* base) {
   x->I0p = (float*)take(c.max_requests * nparts * x->B * 4);
   x->I1p = (float*)take(c.max_requests * nparts * x->B * 4);
   x->vpart = (VocabPartial*)take(RL * x->nch_vocab * sizeof(VocabPartial));
+  x->vtiles = (VocabPartial*)take(RL * ((V + 63) / 64) * sizeof(VocabPartial));
   x->tokconf = (TokConf*)take(RL * sizeof(TokConf));
   x->res_dev = (focus_commit_result*)take(c.max_requests * sizeof(focus_commit_result));
   if (x->attn_tc) {
@@ -289,7 +292,10 @@ void derive(focus_ctx* x) {
   x->split_tiles = 16;                         // 128-key tiles per split (the kernel may enlarge it)
   if (const char* e = getenv("FOCUS_ATTN_SPLIT_TILES")) x->split_tiles = std::max(2, atoi(e));
   x->max_nsplit = std::max(16, ((c.max_seq_len + 127) / 128 + x->split_tiles - 1) / x->split_tiles + 1);
-  x->nch_vocab = std::max(1, std::min(16, c.vocab / 8192));
+  // LM head with the vocab-statistics epilogue (default on the tensor-core GEMM path; FOCUS_VOCAB_FUSED=0:
+  // store the fp32 logits and reduce them in k_vocab_reduce)
+  x->vocab_fused = gemm_backend() == 1 && !(getenv("FOCUS_VOCAB_FUSED") && getenv("FOCUS_VOCAB_FUSED")[0] == '0');
+  x->nch_vocab = x->vocab_fused ? 1 : std::max(1, std::min(16, c.vocab / 8192));
   x->mask_id = c.vocab - 1;
   x->max_gen = c.max_seq_len;
 }
@@ -927,13 +933,19 @@ static focus_status enqueue_step(focus_ctx* x, const int32_t* ids, int32_t n_req
   a1.imp_only = 1;
   a1.out = nullptr;
   if (x->attn_tc && plan_attention(x, a0, 0)) ++x->launches;
-  if (x->attn_tc && plan_attention(x, a1, 1)) ++x->launches;
+  // layer-1 importance (block keys only, O(B^2 H d_h) work): the CUDA-core kernel, one CTA per
+  // (request, chunk, kv head) with the block scores in shared memory, is far cheaper than a persistent
+  // tensor-core launch for it (FOCUS_IMP_TC=1: the tensor-core importance-only mode)
+  static int imp_tc = -1;
+  if (imp_tc < 0) imp_tc = (getenv("FOCUS_IMP_TC") && getenv("FOCUS_IMP_TC")[0] == '1') ? 1 : 0;
+  if (x->attn_tc && imp_tc && plan_attention(x, a1, 1)) ++x->launches;
   qkv_piece(x, 0, 0, x->x, rsP);
   LAUNCH(ATTN, run_attention(x, a0));
   out_mlp_piece(x, 0, 0, x->x, rsP);
   // A3 layer-1 projections on P, K1/V1 stored before eviction, importance-only I1
   qkv_piece(x, 1, 1, x->x, rsP);
-  LAUNCH(IMPORTANCE, run_attention(x, a1));
+  if (x->attn_tc && !imp_tc) LAUNCH(IMPORTANCE, launch_attention(a1, s));
+  else LAUNCH(IMPORTANCE, run_attention(x, a1));
   // A4 selection + compaction plan, A5 gather
   {
     SelectArgs sa{};
@@ -995,9 +1007,24 @@ static focus_status enqueue_step(focus_ctx* x, const int32_t* ids, int32_t n_req
   }
   // A8 final norm + LM head on S cap M, vocab reduction
   LAUNCH(RMSNORM, launch_rmsnorm(x->x2, x->srcL, ML, maxP, c.d_model, c.rms_eps, x->h, s));
-  LAUNCH(GEMM_LM, launch_gemm(x->h, c.d_model, x->max_rows, x->Wlm, c.vocab, c.d_model, x->logits, c.vocab, ML, maxP,
-                              GEMM_STORE, x->gws, s, est.M_L));
-  LAUNCH(VOCAB, launch_vocab_reduce(x->logits, ML, maxP, c.vocab, x->mask_id, x->nch_vocab, x->vpart, s));
+  if (x->vocab_fused) {
+    // the LM head's epilogue emits per-row vocab statistics per 64 columns; the fp32 logits reach HBM
+    // only when debug taps are on (parity tests read them)
+    GemmEpi e{};
+    e.vpart = x->vtiles;
+    e.vp_ld = (c.vocab + 63) / 64;
+    e.mask_id = x->mask_id;
+    bool ok = false;
+    LAUNCH(GEMM_LM, ok = launch_gemm_tc(x->h, c.d_model, x->max_rows, x->Wlm, c.vocab, c.d_model,
+                                        c.debug_taps ? x->logits : nullptr, c.vocab, ML, maxP, GEMM_STORE, x->gws,
+                                        s, &e, est.M_L));
+    if (!ok) return FOCUS_ERR_CUDA;
+    LAUNCH(VOCAB, launch_vocab_combine(x->vtiles, e.vp_ld, ML, maxP, x->vpart, s));
+  } else {
+    LAUNCH(GEMM_LM, launch_gemm(x->h, c.d_model, x->max_rows, x->Wlm, c.vocab, c.d_model, x->logits, c.vocab, ML,
+                                maxP, GEMM_STORE, x->gws, s, est.M_L));
+    LAUNCH(VOCAB, launch_vocab_reduce(x->logits, ML, maxP, c.vocab, x->mask_id, x->nch_vocab, x->vpart, s));
+  }
   return cuda_status(cudaGetLastError());
 }
 

@@ -14,6 +14,15 @@
 
 namespace focus {
 
+__device__ __forceinline__ VocabPartial vp_combine(VocabPartial a, VocabPartial b);
+__device__ __forceinline__ VocabPartial vp_combine(VocabPartial a, float4 b4, int) {   // b as raw 16 bytes
+  VocabPartial b;
+  b.m = b4.x;
+  b.s = b4.y;
+  b.idx = __float_as_int(b4.z);
+  b.pad = 0;
+  return vp_combine(a, b);
+}
 __device__ __forceinline__ VocabPartial vp_combine(VocabPartial a, VocabPartial b) {
   if (b.m == -CUDART_INF_F) return a;
   if (a.m == -CUDART_INF_F) return b;
@@ -81,6 +90,44 @@ void launch_vocab_reduce(const float* logits, const int* M_dev, int M_max, int V
   if (M_max <= 0) return;
   dim3 grid(M_max, nch);
   launch_pdl(k_vocab_reduce, grid, dim3(256), 0, s, logits, M_dev, M_max, V, mask_id, nch, part);
+}
+
+// One CTA per logit row: thread t combines groups t, t + 256, ... in order, then a fixed butterfly per
+// warp and the 8 warps in order (vp_combine is commutative, so the result does not depend on timing);
+// (max, sum exp(z - max), lowest argmax) of the whole row goes to out[row].  The LM-head epilogue wrote
+// the per-64-column partials, so the fp32 logits never reach HBM.
+__global__ void __launch_bounds__(256) k_vocab_combine(const VocabPartial* __restrict__ tiles, int ngroups,
+                                                       const int* __restrict__ M_dev, int M_max,
+                                                       VocabPartial* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
+  const int row = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (row >= min(*M_dev, M_max)) return;
+  const VocabPartial* t = tiles + (size_t)row * ngroups;
+  VocabPartial acc{-CUDART_INF_F, 0.f, 0x7fffffff, 0};
+  for (int g = threadIdx.x; g < ngroups; g += 256) acc = vp_combine(acc, __ldcg(reinterpret_cast<const float4*>(t + g)) , 0);
+  for (int off = 1; off < 32; off <<= 1) {
+    VocabPartial o;
+    o.m = __shfl_xor_sync(0xffffffffu, acc.m, off);
+    o.s = __shfl_xor_sync(0xffffffffu, acc.s, off);
+    o.idx = __shfl_xor_sync(0xffffffffu, acc.idx, off);
+    o.pad = 0;
+    acc = vp_combine(acc, o);
+  }
+  __shared__ VocabPartial red[8];
+  if (lane == 0) red[warp] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    VocabPartial r = red[0];
+    for (int w = 1; w < 8; ++w) r = vp_combine(r, red[w]);
+    out[row] = r;
+  }
+}
+
+void launch_vocab_combine(const VocabPartial* tiles, int ngroups, const int* M_dev, int M_max, VocabPartial* out,
+                          cudaStream_t s) {
+  if (M_max <= 0) return;
+  launch_pdl(k_vocab_combine, dim3(M_max), dim3(256), 0, s, tiles, ngroups, M_dev, M_max, out);
 }
 
 __global__ void __launch_bounds__(1024) k_commit(CommitArgs a) {

@@ -21,6 +21,8 @@
 #include <mutex>
 #include <unordered_map>
 
+#include <math_constants.h>
+
 #include "tc_ptx.cuh"
 
 namespace focus {
@@ -181,10 +183,47 @@ __device__ __forceinline__ void epilogue_tile(Chunk&& chunk, int row0, int M, in
   const int rr = lane >> 3, jj = lane & 7;              // read-back: row 4i + rr, 16-B chunk jj
   if constexpr (MODE == GEMM_STORE || MODE == GEMM_ADD) {
     const bool vec_ok = (ldc % 4) == 0 && (((uintptr_t)C) & 15) == 0;
+    // LM head: the confidence statistics of this thread's row over each 64-column group (columns in
+    // ascending order; ties keep the lowest id).  conf = 1 / sum exp(z - max) (A-CF1), mask id excluded.
+    const bool vocab = MODE == GEMM_STORE && epi.vpart != nullptr;
+    VocabPartial vp{-CUDART_INF_F, 0.f, 0x7fffffff, 0};
 #pragma unroll 1
     for (int c0 = part * (BN / nparts); c0 < (part + 1) * (BN / nparts); c0 += 32) {
       float v[32];
       chunk(c0, v);
+      if (vocab) {
+        const int cb = nt * BN + c0;
+        float m = -CUDART_INF_F;
+        int im = 0x7fffffff;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const bool ok = cb + i < N && cb + i != epi.mask_id;
+          if (ok && v[i] > m) { m = v[i]; im = cb + i; }
+        }
+        float sum = 0.f;
+        if (m != -CUDART_INF_F) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (cb + i < N && cb + i != epi.mask_id) sum += __expf(v[i] - m);
+        }
+        if ((c0 & 32) == 0) {
+          vp = VocabPartial{m, sum, im, 0};
+        } else if (m != -CUDART_INF_F) {            // second half of the 64-column group
+          if (vp.m == -CUDART_INF_F) {
+            vp = VocabPartial{m, sum, im, 0};
+          } else {
+            const float mm = fmaxf(vp.m, m);
+            vp.s = vp.s * __expf(vp.m - mm) + sum * __expf(m - mm);
+            vp.idx = m > vp.m ? im : vp.idx;        // equal maxima: the first group's id is lower
+            vp.m = mm;
+          }
+        }
+        if ((c0 & 32) != 0 || c0 + 32 >= (part + 1) * (BN / nparts)) {
+          const int row = row0 + lane;
+          if (row < M && (cb & ~63) < N) epi.vpart[(size_t)row * epi.vp_ld + (cb >> 6)] = vp;
+        }
+        if (C == nullptr) continue;                    // logits not stored (no debug taps)
+      }
 #pragma unroll
       for (int j = 0; j < 8; ++j) sts128(epi_slot(buf, lane, j), f4_bits(v + 4 * j));
       __syncwarp();

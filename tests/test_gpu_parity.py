@@ -85,7 +85,7 @@ def _resync(run, prompt_lens, max_steps=1 << 30):
     B, m = run.method.block_size, run.model
     tau32 = float(np.float32(run.method.conf_threshold))
     nreq = run.n_requests
-    ctx = _ctx(run)
+    ctx = _ctx(run, debug_taps=True)          # the fp32 logits are stored only with taps (fused vocab stats)
     prompts = request_prompts(run)
     for r in range(nreq):
         ctx.focus_kv_append(r, prompts[r], run.gen_len)
