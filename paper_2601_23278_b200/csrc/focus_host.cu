@@ -933,11 +933,11 @@ static focus_status enqueue_step(focus_ctx* x, const int32_t* ids, int32_t n_req
   a1.imp_only = 1;
   a1.out = nullptr;
   if (x->attn_tc && plan_attention(x, a0, 0)) ++x->launches;
-  // layer-1 importance (block keys only, O(B^2 H d_h) work): the CUDA-core kernel, one CTA per
-  // (request, chunk, kv head) with the block scores in shared memory, is far cheaper than a persistent
-  // tensor-core launch for it (FOCUS_IMP_TC=1: the tensor-core importance-only mode)
+  // layer-1 importance (block keys only, O(B^2 H d_h) work): the persistent tensor-core kernel's
+  // importance-only mode (default; 0.063 ms per C3 step) or, with FOCUS_IMP_TC=0, the CUDA-core kernel
+  // (one CTA per (request, chunk, kv head); measured 0.124 ms)
   static int imp_tc = -1;
-  if (imp_tc < 0) imp_tc = (getenv("FOCUS_IMP_TC") && getenv("FOCUS_IMP_TC")[0] == '1') ? 1 : 0;
+  if (imp_tc < 0) imp_tc = (getenv("FOCUS_IMP_TC") && getenv("FOCUS_IMP_TC")[0] == '0') ? 0 : 1;
   if (x->attn_tc && imp_tc && plan_attention(x, a1, 1)) ++x->launches;
   qkv_piece(x, 0, 0, x->x, rsP);
   LAUNCH(ATTN, run_attention(x, a0));
