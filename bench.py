@@ -338,7 +338,7 @@ def profile_steps(rk, n):
     c.focus_sync()
     prof = c.profile()
     c.focus_set_profile(False)
-    return dict(prof=prof, flops=fl_tot, bytes=by_tot, steps=n)
+    return dict(prof=prof, flops=fl_tot, bytes=by_tot, steps=n, M_S=max(1, int(cnt[1])))
 
 
 def e2e_generation(rk, D, warmup):
@@ -466,6 +466,35 @@ def roofline_report(pd, pk):
     return roof, gemms, kernels, step
 
 
+def cublas_reference(model, M, dev):
+    """cuBLAS (torch.matmul, bf16) at the projection shapes of the profiled step's S rows, weights
+    cold (a 256 MB buffer is rewritten between reps, as the step streams its weights from HBM): the
+    library baseline the hand-written tcgen05 GEMMs are compared with."""
+    import torch
+    d, ff = model.d_model, model.d_ff
+    qd = model.n_q_heads * model.head_dim
+    shapes = {"gemm_qkv": (model.qkv_dim, d), "gemm_o": (d, qd), "gemm_gu": (2 * ff, d), "gemm_down": (d, ff)}
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    out = {}
+    for k, (N, K) in shapes.items():
+        A = torch.randn(M, K, device=dev, dtype=torch.bfloat16)
+        W = torch.randn(N, K, device=dev, dtype=torch.bfloat16)
+        best = 1e9
+        for r in range(6):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+            e0.record()
+            torch.matmul(A, W.t())
+            e1.record()
+            torch.cuda.synchronize()
+            if r:
+                best = min(best, e0.elapsed_time(e1))
+        out[k] = {"M": M, "N": N, "K": K, "us": round(best * 1e3, 1), "tflops": round(2 * M * N * K / (best * 1e-3) / 1e12, 1)}
+    del flush
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_focus(args):
     import torch
     from paper_2601_23278_b200 import dist as D
@@ -543,9 +572,16 @@ def run_focus(args):
             extras["no_eviction"]["focus_speedup_windows"] = round(value / extras["no_eviction"]["value"], 3)
 
     pk = peaks()
-    roof = gemms = kernels = stepr = None
+    roof = gemms = kernels = stepr = cub = None
     if g["prof"] is not None:
         roof, gemms, kernels, stepr = roofline_report(g["prof"], pk)
+        if rank == 0 and not args.no_extras:
+            cub = cublas_reference(run.model, g["prof"]["M_S"], dev)
+            for k, v in cub.items():
+                if k in kernels:
+                    ours = kernels[k]["ms_per_step"] * 1e3 / max(1, kernels[k]["launches"])
+                    v["ours_us_per_launch"] = round(ours, 1)
+                    v["ours_over_cublas"] = round(ours / v["us"], 3)
     stats = D.all_gather_stats([int(g["gen_dec"]), len(gids), int(prefill_s * 1e3)], dev)
     global_batch = int(D.reduce_sum(len(gids), dev))
 
@@ -580,6 +616,10 @@ def run_focus(args):
                "clocks": clk.summary(), "per_rank": stats}
         if roof is not None:
             out.update(roofline=roof, roofline_gemms=gemms, kernels=kernels, step_roofline=stepr)
+        if cub is not None:
+            out["cublas_reference"] = {"note": "torch.matmul bf16 at the profiled step's S-row shapes, cold weights; "
+                                               "ours = CUDA-event time per launch averaged over the step's launches "
+                                               "(layers 0-1 run the P rows)", **cub}
         out.update(extras)
         if cpu is not None:
             out["cpu_baseline"] = cpu

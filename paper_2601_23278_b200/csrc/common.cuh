@@ -124,7 +124,10 @@ struct GemmWs {                 // split-K partials + per-tile semaphores (carve
   size_t bytes;
   int* sem;
   size_t sem_count;
+  int no_swap;                  // 1: never the swap-AB decode GEMM (batch_invariant: the path would
+                                // otherwise depend on the batch's row-count bound)
 };
+constexpr int kSwapSemBase = 4096;   // swap-AB split-K tile counters: sem[kSwapSemBase + tile]
 // One work unit of the tensor-core attention kernel (request i of the call, query-row chunk, kv head,
 // key split; key tiles [t_lo, t_hi) of 128 keys), as planned once per step by k_attn_plan.
 struct AttnUnit {
@@ -158,7 +161,7 @@ void launch_gemm(const bf16* A, int lda, int a_rows, const bf16* W, int N, int K
 int gemm_backend();
 // tile configuration a tensor-core GEMM of this shape takes at m_est expected live rows (the graph
 // cache keys on it; kernels_gemm_tc.cu)
-int gemm_tc_choice(int N, int K, GemmMode mode, int M_max, int m_est);
+int gemm_tc_choice(int N, int K, GemmMode mode, int M_max, int m_est, bool allow_swap = true);
 int num_sms();
 void gemm_set_backend(int b);
 

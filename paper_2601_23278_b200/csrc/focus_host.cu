@@ -12,9 +12,20 @@
 #include <new>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "common.cuh"
 
 using namespace focus;
+
+namespace {
+// NVTX phase ranges: host-side markers around the step's phases, visible in Nsight
+// Systems / ncu --nvtx (header-only NVTX v3; no-ops without an attached tool)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+}  // namespace
 
 namespace focus {
 void launch_gemm_simt(const bf16* A, int lda, const bf16* W, int N, int K, float* C, int ldc, const int* M_dev,
@@ -262,7 +273,8 @@ size_t carve(focus_ctx* x, char* base) {
   }
   x->gws.bytes = (size_t)64 << 20;
   x->gws.ptr = (float*)take(x->gws.bytes);
-  x->gws.sem_count = 4096;
+  x->gws.sem_count = kSwapSemBase + 4096;
+  x->gws.no_swap = c.batch_invariant ? 1 : 0;
   x->gws.sem = (int*)take(x->gws.sem_count * 4);
   if (c.debug_taps) {
     const size_t sz[kTapCount] = {R * d * 4, R * d * 2, R * qkv * 2, R * qd * 2, R * d * 4,
@@ -648,6 +660,7 @@ focus_status focus_destroy(focus_ctx* x) {
 
 focus_status focus_kv_append(focus_ctx* x, int32_t req_id, const int32_t* prompt, int32_t n_tokens, int32_t gen_len) {
   if (!x) return FOCUS_ERR_STATE;
+  NvtxRange nv("focus_kv_append (prefill)");
   const focus_config& c = x->cfg;
   if (x->step_pending) return FOCUS_ERR_STATE;
   if (req_id < 0 || req_id >= c.max_requests || x->slot_used[req_id]) return FOCUS_ERR_STATE;
@@ -748,6 +761,7 @@ static bool graphs_enabled(const focus_ctx* x) {
 
 focus_status focus_step_block(focus_ctx* x, const int32_t* ids, int32_t n_req) {
   if (!x) return FOCUS_ERR_STATE;
+  NvtxRange nv("focus_step_block");
   if (x->step_pending) return FOCUS_ERR_STATE;
   focus_status rc = check_list(x, ids, n_req);
   if (rc != FOCUS_OK) return rc;
@@ -790,12 +804,12 @@ static std::vector<int> shape_key(const focus_ctx* x, int maxP, const Counters& 
   if (gemm_backend() != 1) return k;
   const GemmMode qm = fused_qkv(x) ? GEMM_QKV_ROPE : GEMM_STORE;
   for (int m : {e.M_P, e.M_S}) {
-    k.push_back(gemm_tc_choice(x->qkv_dim, c.d_model, qm, maxP, m));
-    k.push_back(gemm_tc_choice(c.d_model, x->q_dim, GEMM_ADD, maxP, m));
-    k.push_back(gemm_tc_choice(2 * c.d_ff, c.d_model, GEMM_SWIGLU, maxP, m));
-    k.push_back(gemm_tc_choice(c.d_model, c.d_ff, GEMM_ADD, maxP, m));
+    k.push_back(gemm_tc_choice(x->qkv_dim, c.d_model, qm, maxP, m, !x->gws.no_swap));
+    k.push_back(gemm_tc_choice(c.d_model, x->q_dim, GEMM_ADD, maxP, m, !x->gws.no_swap));
+    k.push_back(gemm_tc_choice(2 * c.d_ff, c.d_model, GEMM_SWIGLU, maxP, m, !x->gws.no_swap));
+    k.push_back(gemm_tc_choice(c.d_model, c.d_ff, GEMM_ADD, maxP, m, !x->gws.no_swap));
   }
-  k.push_back(gemm_tc_choice(c.vocab, c.d_model, GEMM_STORE, maxP, e.M_L));
+  k.push_back(gemm_tc_choice(c.vocab, c.d_model, GEMM_STORE, maxP, e.M_L, !x->gws.no_swap));
   return k;
 }
 
@@ -914,6 +928,7 @@ static focus_status enqueue_step(focus_ctx* x, const int32_t* ids, int32_t n_req
   x->last_list = x->pending_list;
   const int maxP = n_req * x->B;
   // A0 setup, A1 embedding
+  nvtxRangePushA("A0-A1 setup, embedding");
   LAUNCH(SETUP, launch_step_setup(x->req_dev, n_req, x->st, x->B, x->rowP, x->offP, x->tokP, x->cnt, s));
   const int* MP = &x->cnt->M_P;
   const int* MS = &x->cnt->M_S;
@@ -924,6 +939,8 @@ static focus_status enqueue_step(focus_ctx* x, const int32_t* ids, int32_t n_req
   RowSpace rsS{MS, maxP, x->rowS, est.M_S, x->ropeT_S};
   if (fused_qkv(x))
     LAUNCH(ROPE_STORE, launch_rope_rows(x->rowP, MP, maxP, x->rope_cos, x->rope_sin, x->ropeT_P, x->max_rows, s));
+  nvtxRangePop();
+  nvtxRangePushA("A2-A3 layer 0, layer-1 prefix, importance");
   // A2 layer 0 fully on P (+ fused importance I0)
   // attention unit tables of the P-row launches (layer 0, layer-1 importance), once per step
   AttnArgs a0 = attn_args(x, 0, x->qkv, x->qkv_dim, n_req, x->offP, 0);
@@ -946,6 +963,8 @@ static focus_status enqueue_step(focus_ctx* x, const int32_t* ids, int32_t n_req
   qkv_piece(x, 1, 1, x->x, rsP);
   if (x->attn_tc && !imp_tc) LAUNCH(IMPORTANCE, launch_attention(a1, s));
   else LAUNCH(IMPORTANCE, run_attention(x, a1));
+  nvtxRangePop();
+  nvtxRangePushA("A4-A5 selection, compaction");
   // A4 selection + compaction plan, A5 gather
   {
     SelectArgs sa{};
@@ -989,6 +1008,8 @@ static focus_status enqueue_step(focus_ctx* x, const int32_t* ids, int32_t n_req
     x->pf_tiles = pf_env;
     x->pf_grid = attn_tc_grid(a3);
   }
+  nvtxRangePop();
+  nvtxRangePushA("A6-A7 layers 1-suffix .. L-1 on S");
   // A6 layer-1 suffix on S: keys = context + whole block
   LAUNCH(ATTN, run_attention(x, a2));
   out_mlp_piece(x, 1, 1, x->x2, rsS);
@@ -1005,6 +1026,8 @@ static focus_status enqueue_step(focus_ctx* x, const int32_t* ids, int32_t n_req
     LAUNCH(ATTN, run_attention(x, a));
     out_mlp_piece(x, l, l, x->x2, rsS);
   }
+  nvtxRangePop();
+  nvtxRangePushA("A8 final norm, LM head, vocab statistics");
   // A8 final norm + LM head on S cap M, vocab reduction
   LAUNCH(RMSNORM, launch_rmsnorm(x->x2, x->srcL, ML, maxP, c.d_model, c.rms_eps, x->h, s));
   if (x->vocab_fused) {
@@ -1018,18 +1041,20 @@ static focus_status enqueue_step(focus_ctx* x, const int32_t* ids, int32_t n_req
     LAUNCH(GEMM_LM, ok = launch_gemm_tc(x->h, c.d_model, x->max_rows, x->Wlm, c.vocab, c.d_model,
                                         c.debug_taps ? x->logits : nullptr, c.vocab, ML, maxP, GEMM_STORE, x->gws,
                                         s, &e, est.M_L));
-    if (!ok) return FOCUS_ERR_CUDA;
+    if (!ok) { nvtxRangePop(); return FOCUS_ERR_CUDA; }
     LAUNCH(VOCAB, launch_vocab_combine(x->vtiles, e.vp_ld, ML, maxP, x->vpart, s));
   } else {
     LAUNCH(GEMM_LM, launch_gemm(x->h, c.d_model, x->max_rows, x->Wlm, c.vocab, c.d_model, x->logits, c.vocab, ML,
                                 maxP, GEMM_STORE, x->gws, s, est.M_L));
     LAUNCH(VOCAB, launch_vocab_reduce(x->logits, ML, maxP, c.vocab, x->mask_id, x->nch_vocab, x->vpart, s));
   }
+  nvtxRangePop();
   return cuda_status(cudaGetLastError());
 }
 
 focus_status focus_commit(focus_ctx* x, const int32_t* ids, int32_t n_req, focus_commit_result* out) {
   if (!x) return FOCUS_ERR_STATE;
+  NvtxRange nv("focus_commit (A9-A10)");
   if (!x->step_pending || n_req != (int)x->pending_list.size()) return FOCUS_ERR_STATE;
   for (int i = 0; i < n_req; ++i)
     if (!ids || ids[i] != x->pending_list[i]) return FOCUS_ERR_STATE;

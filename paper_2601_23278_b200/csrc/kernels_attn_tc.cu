@@ -739,13 +739,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         for (int t = x.t_lo; t < x.t_hi; ++t, ++g) {
           const int slot = g % NS;
           if (pf > 0 && t + NS + pf < x.t_hi) prefetch_tile(x, t + NS + pf);
-          mbar_wait(&emptyb[slot], ((g / NS) & 1) ^ 1);
-          tr.ev(1);
           // only the boxes that hold keys of [kbeg, kend): the tail of a unit's last tile (and the head
           // of an importance-only tile) is not streamed; those smem rows keep finite data (the rings
           // are zeroed at kernel start) and the softmax masks their keys (P = 0)
           const int pc0 = a.page_skip ? max(0, (x.kbeg - t * KT) / pr) : 0;
           const int pc1 = a.page_skip ? min(KT / pr, (x.kend - t * KT + pr - 1) / pr) : KT / pr;
+          // (measured: issuing the page-table lookups before the slot wait doubled the per-tile time of
+          // the C3 layers; the lookups stay after the wait)
+          mbar_wait(&emptyb[slot], ((g / NS) & 1) ^ 1);
+          tr.ev(1);
           mbar_expect_tx(&fullb[slot], (uint32_t)(pc1 - pc0) * pr * 256);
           uint8_t* dst = ring + slot * KV_BYTES;
           for (int pc = pc0; pc < pc1; ++pc) {

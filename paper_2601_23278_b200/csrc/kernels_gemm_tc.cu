@@ -919,6 +919,265 @@ struct MapKeyHash {
   }
 };
 
+
+// ====================================================================================== swap-AB decode GEMM
+// Few live rows (M_max <= 128: the decode shapes of C2 / C5, ...): the weight rows go on the MMA M side
+// and the tokens on N ("swap-AB"),  acc^T[128 features x NT tokens] = W_tile[128 x K] . A^T,  so the
+// tensor core does no work on padding rows, and each CTA computes one 128-feature tile (SWIGLU: the
+// gate and the up tile of 128 features, two accumulators) over one of `split` contiguous K ranges:
+// every SM streams weights even when the GEMM has few feature tiles.  The split partials (fp32,
+// [token][feature]) are reduced by the tile's last-arriving CTA in K-range order (deterministic; the
+// split depends on N and K only), which then runs the mode's epilogue with thread = feature:
+//   ADD       x[t][f] += acc (one writer per element; 32 consecutive features per warp store)
+//   STORE     logits C[t][f] (when C) and per (token, 64-feature group) vocab statistics (epi.vpart)
+//   SWIGLU    act[t][f] = bf16(silu(gate) * up)
+//   QKV_ROPE  tile = one q/k/v head: RoPE pairs (d, d+64) exchanged through shared memory, bf16 q|k|v
+//             rows and the paged KV store
+namespace swp {
+constexpr int THREADS = 256;
+template <int NT, bool GU>
+struct SL {
+  static constexpr int NW = GU ? 2 : 1;                          // weight tiles (accumulators) per CTA
+  static constexpr int W_BYTES = NW * 128 * BK * 2;              // 16 / 32 KB
+  static constexpr int ACT_BYTES = NT * BK * 2;
+  static constexpr int STAGE = W_BYTES + ACT_BYTES;
+  static constexpr int STAGES = (160 * 1024) / STAGE > 8 ? 8 : (160 * 1024) / STAGE;
+  static constexpr int XCH = 32 * 128 * 4;                       // exchange buffer: 32 tokens x 128 features
+  static constexpr int SMEM = STAGES * STAGE + XCH + 1024 + 256;
+  static constexpr int COLS = NW * NT;
+  static constexpr int TCOLS = COLS <= 32 ? 32 : COLS <= 64 ? 64 : COLS <= 128 ? 128 : 256;
+};
+}  // namespace swp
+
+template <int MODE, int NT>
+__global__ void __launch_bounds__(swp::THREADS, 1)
+    k_gemm_swap(const __grid_constant__ CUtensorMap mapW, const __grid_constant__ CUtensorMap mapA, float* __restrict__ C,
+                int ldc, int N, int K, const int* __restrict__ M_dev, int M_max, const GemmEpi epi, int split,
+                float* __restrict__ ws, int* __restrict__ cnt) {
+  constexpr bool GU = MODE == GEMM_SWIGLU;
+  using L = swp::SL<NT, GU>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  float* xch = (float*)(smem + L::STAGES * L::STAGE);
+  uint64_t* bars = (uint64_t*)(smem + L::STAGES * L::STAGE + L::XCH);
+  uint64_t* full = bars;                                // [STAGES]
+  uint64_t* empty = bars + L::STAGES;                   // [STAGES]
+  uint64_t* tfull = bars + 2 * L::STAGES;               // [1]
+  uint32_t* tmem_sh = (uint32_t*)(tfull + 1);
+  int* flag_sh = (int*)(tmem_sh + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tile = blockIdx.x / split, sp = blockIdx.x % split;
+  const int kbt = K / BK, kb0 = sp * kbt / split, kb1 = (sp + 1) * kbt / split;
+  const int wrow0 = tile * 128 * L::NW;                 // first weight row of the tile (SWIGLU: gate, then up)
+  pdl_trigger();
+  if (warp == 0 && lane == 0) {
+    for (int i = 0; i < L::STAGES; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+    mbar_init(&tfull[0], 1);
+    fence_barrier_init();
+    prefetch_map(&mapW);
+    prefetch_map(&mapA);
+  }
+  if (warp == 2) tmem_alloc<L::TCOLS>(tmem_sh);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_sh;
+  if (warp == 0) {
+    if (lane == 0) {
+      // the weight tiles do not depend on earlier kernels: the first stages' weight loads are issued
+      // before the grid dependency wait (they overlap the previous kernel's tail); the activation tiles
+      // after it
+      const uint64_t pol = l2_policy_evict_first();
+      const int pre = min(kb1 - kb0, L::STAGES);
+      for (int i = 0; i < pre; ++i) {
+        uint8_t* st = smem + i * L::STAGE;
+        mbar_expect_tx(&full[i], L::STAGE);
+        tma_load_2d_hint(st, &mapW, &full[i], (kb0 + i) * BK, wrow0, pol);
+        if (GU) tma_load_2d_hint(st + 128 * BK * 2, &mapW, &full[i], (kb0 + i) * BK, wrow0 + 128, pol);
+      }
+      pdl_wait();
+      for (int i = 0; i < pre; ++i)
+        tma_load_2d(smem + i * L::STAGE + L::W_BYTES, &mapA, &full[i], (kb0 + i) * BK, 0);
+      int stage = pre % L::STAGES;
+      uint32_t phase = pre == L::STAGES ? 1u : 0u;
+      for (int kb = kb0 + pre; kb < kb1; ++kb) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        uint8_t* st = smem + stage * L::STAGE;
+        mbar_expect_tx(&full[stage], L::STAGE);
+        tma_load_2d_hint(st, &mapW, &full[stage], kb * BK, wrow0, pol);
+        if (GU) tma_load_2d_hint(st + 128 * BK * 2, &mapW, &full[stage], kb * BK, wrow0 + 128, pol);
+        tma_load_2d(st + L::W_BYTES, &mapA, &full[stage], kb * BK, 0);
+        if (++stage == L::STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_bf16(128, NT, false, false);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int kb = kb0; kb < kb1; ++kb) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        const uint32_t w0 = smem_u32(smem + stage * L::STAGE), a0 = w0 + L::W_BYTES;
+#pragma unroll
+        for (int k = 0; k < BK / 16; ++k) {
+          const uint32_t acc = (kb > kb0 || k > 0) ? 1u : 0u;
+          mma_bf16(tmem, desc_kmajor_sw128(w0 + k * 32), desc_kmajor_sw128(a0 + k * 32), idesc, acc);
+          if (GU) mma_bf16(tmem + NT, desc_kmajor_sw128(w0 + 128 * BK * 2 + k * 32), desc_kmajor_sw128(a0 + k * 32), idesc, acc);
+        }
+        mma_commit(&empty[stage]);
+        if (++stage == L::STAGES) { stage = 0; phase ^= 1; }
+      }
+      mma_commit(&tfull[0]);
+    }
+  } else if (warp >= 4) {
+    pdl_wait();
+    const int f = threadIdx.x - 128, q = warp - 4;
+    const int M = M_dev ? min(*M_dev, M_max) : M_max;
+    const uint32_t tb = tmem + ((uint32_t)(q * 32) << 16);
+    mbar_wait(&tfull[0], 0);
+    tc_fence_after();
+    const size_t slot = (size_t)L::NW * NT * 128;       // partial floats per CTA: [acc][token][feature]
+    bool mine = true;
+    if (split > 1) {
+      float* part = ws + (size_t)blockIdx.x * slot;
+#pragma unroll 1
+      for (int c = 0; c < L::NW * NT; c += 32) {
+        float v[32];
+        tmem_ld32(tb + c, v);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) __stcg(part + (size_t)(c + i) * 128 + f, v[i]);
+      }
+      __threadfence();
+      named_bar(1, 128);
+      if (f == 0) *flag_sh = atomicAdd(&cnt[tile], 1);
+      named_bar(1, 128);
+      mine = *flag_sh == split - 1;                     // the tile's last-arriving range reduces
+      if (mine) __threadfence();
+    }
+    if (mine) {
+      const float* base = ws + (size_t)tile * split * slot;
+      // 32 accumulator columns [c, c+32) of this thread's feature: TMEM, or the K-range partials summed
+      // in range order
+      auto get = [&](int c, float* v) {
+        if (split == 1) {
+          tmem_ld32(tb + c, v);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = 0.f;
+          for (int s2 = 0; s2 < split; ++s2) {
+            const float* p2 = base + (size_t)s2 * slot + (size_t)c * 128 + f;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] += __ldcg(p2 + (size_t)i * 128);
+          }
+        }
+      };
+      const int feat = tile * 128 + f;                  // output feature (SWIGLU: act column)
+#pragma unroll 1
+      for (int t0 = 0; t0 < NT; t0 += 32) {
+        if (t0 >= M) break;                             // warp-uniform: M is the same for every thread
+        float v[32];
+        get(t0, v);
+        if constexpr (MODE == GEMM_ADD) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (t0 + i < M)
+              asm volatile("red.global.add.f32 [%0], %1;" ::"l"(C + (size_t)(t0 + i) * ldc + feat), "f"(v[i]) : "memory");
+        } else if constexpr (MODE == GEMM_SWIGLU) {
+          float u[32];
+          get(NT + t0, u);
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (t0 + i < M) {
+              const float a = __fdividef(v[i] * u[i], 1.0f + exp2f(-1.4426950408889634f * v[i]));
+              epi.out[(size_t)(t0 + i) * epi.ldo + feat] = __float2bfloat16_rn(a);
+            }
+        } else if constexpr (MODE == GEMM_STORE) {
+          if (C != nullptr) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (t0 + i < M && feat < N) C[(size_t)(t0 + i) * ldc + feat] = v[i];
+          }
+          if (epi.vpart != nullptr) {
+            // per token: (max, sum exp(z - max), lowest argmax) over this warp's 32 features, then the
+            // two warps of each 64-feature group combined through shared memory
+            float* xm = xch;                             // [4 warps][32 tokens] max, sum, idx
+            const bool ok = feat < N && feat != epi.mask_id;
+#pragma unroll 1
+            for (int i = 0; i < 32; ++i) {
+              const float z = ok ? v[i] : -CUDART_INF_F;
+              float m = z;
+              for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+              const unsigned hit = __ballot_sync(0xffffffffu, z == m && m != -CUDART_INF_F);
+              float e = (m == -CUDART_INF_F || !ok) ? 0.f : __expf(z - m);
+              for (int o = 16; o; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
+              if (lane == 0) {
+                xm[(q * 32 + i) * 4 + 0] = m;
+                xm[(q * 32 + i) * 4 + 1] = e;
+                xm[(q * 32 + i) * 4 + 2] = __int_as_float(hit ? tile * 128 + q * 32 + __ffs(hit) - 1 : 0x7fffffff);
+              }
+            }
+            named_bar(1, 128);
+            if ((q & 1) == 0) {                          // warps 0 and 2: lane i = token t0 + i
+              const int i = lane, t = t0 + i;
+              const float* a = xm + (q * 32 + i) * 4;
+              const float* b = xm + ((q + 1) * 32 + i) * 4;
+              VocabPartial r;
+              const float ma = a[0], mb = b[0];
+              r.m = fmaxf(ma, mb);
+              if (r.m == -CUDART_INF_F) { r.s = 0.f; r.idx = 0x7fffffff; }
+              else {
+                r.s = (ma == -CUDART_INF_F ? 0.f : a[1] * __expf(ma - r.m)) + (mb == -CUDART_INF_F ? 0.f : b[1] * __expf(mb - r.m));
+                r.idx = ma >= mb ? __float_as_int(a[2]) : __float_as_int(b[2]);   // equal maxima: warp q's ids are lower
+              }
+              r.pad = 0;
+              const int g = (tile * 128 + q * 32) >> 6;
+              if (t < M && g < epi.vp_ld) epi.vpart[(size_t)t * epi.vp_ld + g] = r;
+            }
+            named_bar(1, 128);
+          }
+        } else {   // GEMM_QKV_ROPE: tile = head
+          const int head = tile;
+          const int hkv = epi.kv.n_kv_heads;
+          const bool is_v = head >= epi.n_q_heads + hkv;
+          const bool is_k = !is_v && head >= epi.n_q_heads;
+          const int kvh = head - epi.n_q_heads - (is_v ? hkv : 0);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) xch[i * 128 + f] = v[i];
+          named_bar(1, 128);
+          const int kf = f & 63;
+#pragma unroll 4
+          for (int i = 0; i < 32; ++i) {
+            const int t = t0 + i;
+            if (t >= M) break;
+            float y = v[i];
+            if (!is_v) {
+              const float other = xch[i * 128 + (f ^ 64)];
+              const float cc = __ldg(epi.ropeT + (size_t)kf * epi.rope_ld + t);
+              const float sn = __ldg(epi.ropeT + (size_t)(64 + kf) * epi.rope_ld + t);
+              y = f < 64 ? v[i] * cc - other * sn : v[i] * cc + other * sn;
+            }
+            const __nv_bfloat16 b = __float2bfloat16_rn(y);
+            epi.out[(size_t)t * epi.ldo + head * 128 + f] = b;
+            if (is_k || is_v) {
+              const RowInfo ri = epi.rows[t];
+              if (f == 0 && ri.j >= 0 && ((epi.st[ri.slot].committed >> ri.j) & 1ull)) atomicExch(&epi.cnt->invariant, 1);
+              (is_v ? epi.kv.V : epi.kv.K)[kv_offset(epi.kv, ri.slot, ri.pos, kvh) + f] = b;
+            }
+          }
+          named_bar(1, 128);                             // xch reuse by the next chunk
+        }
+      }
+      if (split > 1 && f == 0) cnt[tile] = 0;           // re-arm for the next launch (every range has arrived)
+    }
+  }
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_free<L::TCOLS>(tmem);
+  }
+}
+
 // ka = 0: 2-D map [rows][cols], box box_rows x 64.  ka >= 1: 3-D view {64, rows, cols / 64} of the same
 // matrix (k-atom stride 128 B), box {64, box_rows, ka} = ka consecutive SW128 K-major tiles.
 bool get_map(const void* ptr, int rows, int cols, int ld, int box_rows, CUtensorMap* out, int ka = 0) {
@@ -1114,7 +1373,78 @@ static bool launch_pair(const bf16* A, int lda, int a_rows, const bf16* W, int N
 // the ONLY host decision that depends on the row-count estimate (grids come from M_max).  The
 // whole-step graph cache keys on these choices, so a captured graph is replayed exactly when the
 // eager sequence would launch the same kernels.
-enum { GC_SPLIT = 1, GC_128x2, GC_256x2, GC_128x1, GC_256x1, GC_SINGLE_128, GC_SINGLE_256 };
+enum { GC_SPLIT = 1, GC_128x2, GC_256x2, GC_128x1, GC_256x1, GC_SINGLE_128, GC_SINGLE_256, GC_SWAP };
+
+// swap-AB decode GEMM (see k_gemm_swap): applicable for M_max <= 128 live rows and 128-aligned feature
+// tiles; opt-in (FOCUS_GEMM_SWAP=1).  Measured at C2 (M <= 64, B200): down projection 0.93 -> 0.68 ms per
+// step, O equal, QKV 0.58 -> 1.13, gate-up 0.67 -> 0.76, LM head 0.14 -> 0.28: the split-K reduction by
+// one CTA and the per-token RoPE-table loads of the epilogue cost more than the idle SMs of the
+// CTA-pair kernel.  The split into K ranges depends on N and K only.
+static bool swap_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("FOCUS_GEMM_SWAP");
+    on = (e && e[0] == '1') ? 1 : 0;
+  }
+  return on == 1;
+}
+static bool swap_shape_ok(int N, int K, GemmMode mode, int M_max) {
+  return swap_enabled() && M_max >= 1 && M_max <= 128 && K % tc::BK == 0 && N % (mode == GEMM_SWIGLU ? 256 : 128) == 0;
+}
+static bool swap_applies(int N, int K, GemmMode mode, int M_max, const GemmEpi* epi) {
+  if (!swap_shape_ok(N, K, mode, M_max)) return false;
+  if ((mode == GEMM_SWIGLU || mode == GEMM_QKV_ROPE) && !epi) return false;
+  if (mode == GEMM_QKV_ROPE && epi->kv.head_dim != 128) return false;
+  return true;
+}
+
+template <int MODE, int NT>
+static void launch_swap_k(int grid, cudaStream_t s, const CUtensorMap& mw, const CUtensorMap& ma, float* C, int ldc,
+                          int N, int K, const int* M_dev, int M_max, const GemmEpi& e, int split, const GemmWs& ws) {
+  using namespace tc;
+  constexpr int SMEM = swp::SL<NT, MODE == GEMM_SWIGLU>::SMEM;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_gemm_swap<MODE, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    attr = true;
+  }
+  launch_pdl(k_gemm_swap<MODE, NT>, dim3(grid), dim3(swp::THREADS), SMEM, s, mw, ma, C, ldc, N, K, M_dev, M_max, e,
+             split, ws.ptr, ws.sem + kSwapSemBase);
+}
+
+template <int NT>
+static bool launch_swap_nt(const bf16* A, int lda, int a_rows, const bf16* W, int N, int K, float* C, int ldc,
+                           const int* M_dev, int M_max, GemmMode mode, const GemmWs& ws, cudaStream_t s,
+                           const GemmEpi* epi) {
+  using namespace tc;
+  CUtensorMap mw, ma;
+  if (!get_map(W, N, K, K, 128, &mw) || !get_map(A, a_rows, K, lda, NT, &ma)) return false;
+  const int nw = mode == GEMM_SWIGLU ? 2 : 1;
+  const int tiles = N / (128 * nw);
+  const int kbt = K / BK;
+  // K ranges of >= 4 k-blocks so that about one CTA per SM streams weights
+  int split = std::max(1, std::min(std::min(16, kbt / 4), num_sms() / std::max(1, tiles)));
+  const size_t slot = (size_t)nw * NT * 128 * sizeof(float);
+  if (split > 1 && ((size_t)tiles * split * slot > ws.bytes || ws.sem_count < (size_t)kSwapSemBase + tiles)) split = 1;
+  const GemmEpi e = epi ? *epi : GemmEpi{};
+  const int grid = tiles * split;
+  switch (mode) {
+    case GEMM_ADD: launch_swap_k<GEMM_ADD, NT>(grid, s, mw, ma, C, ldc, N, K, M_dev, M_max, e, split, ws); break;
+    case GEMM_SWIGLU: launch_swap_k<GEMM_SWIGLU, NT>(grid, s, mw, ma, C, ldc, N, K, M_dev, M_max, e, split, ws); break;
+    case GEMM_QKV_ROPE: launch_swap_k<GEMM_QKV_ROPE, NT>(grid, s, mw, ma, C, ldc, N, K, M_dev, M_max, e, split, ws); break;
+    default: launch_swap_k<GEMM_STORE, NT>(grid, s, mw, ma, C, ldc, N, K, M_dev, M_max, e, split, ws);
+  }
+  return true;
+}
+
+static bool launch_gemm_swap(const bf16* A, int lda, int a_rows, const bf16* W, int N, int K, float* C, int ldc,
+                             const int* M_dev, int M_max, GemmMode mode, const GemmWs& ws, cudaStream_t s,
+                             const GemmEpi* epi) {
+  if (a_rows < (M_max <= 32 ? 32 : M_max <= 64 ? 64 : 128)) return false;   // the A box reads NT rows
+  if (M_max <= 32) return launch_swap_nt<32>(A, lda, a_rows, W, N, K, C, ldc, M_dev, M_max, mode, ws, s, epi);
+  if (M_max <= 64) return launch_swap_nt<64>(A, lda, a_rows, W, N, K, C, ldc, M_dev, M_max, mode, ws, s, epi);
+  return launch_swap_nt<128>(A, lda, a_rows, W, N, K, C, ldc, M_dev, M_max, mode, ws, s, epi);
+}
 static int split_parts(int K) {
   // ordered split into S k-ranges (at least 8 k-blocks each, S units in one wave): two ranges for deep
   // K at the C3 shapes.  S up to 4 (FOCUS_GEMM_SPLIT_MAX) was measured slower on the C2 shapes (O
@@ -1141,8 +1471,9 @@ static int env_flag(const char* name, int& cache) {
   return cache;
 }
 
-int gemm_tc_choice(int N, int K, GemmMode mode, int M_max, int m_est) {
+int gemm_tc_choice(int N, int K, GemmMode mode, int M_max, int m_est, bool allow_swap) {
   using namespace tc;
+  if (allow_swap && swap_shape_ok(N, K, mode, M_max)) return GC_SWAP;
   const int m = m_est > 0 ? std::min(m_est, M_max) : M_max;
   static int bn256 = -1, bn128 = -1, pair_env = -1, ka_env = -1;
   const bool force256 = env_flag("FOCUS_GEMM_BN256", bn256) != 0;
@@ -1180,7 +1511,10 @@ bool launch_gemm_tc(const bf16* A, int lda, int a_rows, const bf16* W, int N, in
   if (M_max <= 0) return true;
   if (K % BK || lda % 8 || a_rows < 1) return false;
   const int m = m_est > 0 ? std::min(m_est, M_max) : M_max;
-  switch (gemm_tc_choice(N, K, mode, M_max, m_est)) {
+  if (!ws.no_swap && swap_applies(N, K, mode, M_max, epi) &&
+      launch_gemm_swap(A, lda, a_rows, W, N, K, C, ldc, M_dev, M_max, mode, ws, s, epi))
+    return true;
+  switch (gemm_tc_choice(N, K, mode, M_max, m_est, false)) {
     case GC_SPLIT: return launch_pair<256, 1>(A, lda, a_rows, W, N, K, C, ldc, M_dev, M_max, mode, ws, s, epi, m, split_parts(K));
     case GC_128x2: return launch_pair<128, 2>(A, lda, a_rows, W, N, K, C, ldc, M_dev, M_max, mode, ws, s, epi, m);
     case GC_256x2: return launch_pair<256, 2>(A, lda, a_rows, W, N, K, C, ldc, M_dev, M_max, mode, ws, s, epi, m);
@@ -1191,7 +1525,7 @@ bool launch_gemm_tc(const bf16* A, int lda, int a_rows, const bf16* W, int N, in
   // opt-in (FOCUS_GEMM_PAIR=0): one CTA per tile; (FOCUS_GEMM_MC=1) clusters of 4 CTAs (the 4 m-tiles
   // of a weight tile) share W by TMA multicast when the live row count fills them.  Measured no
   // faster at the C3 shapes (at cluster size <= 4 the L2 already serves the duplicate requests once)
-  const bool narrow = gemm_tc_choice(N, K, mode, M_max, m_est) == GC_SINGLE_128;
+  const bool narrow = gemm_tc_choice(N, K, mode, M_max, m_est, false) == GC_SINGLE_128;
   const int m_tiles = (m + BM - 1) / BM;
   const bool cluster4 = getenv("FOCUS_GEMM_MC") != nullptr && m_tiles % 4 == 0;
   if (narrow) {
