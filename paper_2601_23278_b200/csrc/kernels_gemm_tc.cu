@@ -1380,13 +1380,9 @@ enum { GC_SPLIT = 1, GC_128x2, GC_256x2, GC_128x1, GC_256x1, GC_SINGLE_128, GC_S
 // step, O equal, QKV 0.58 -> 1.13, gate-up 0.67 -> 0.76, LM head 0.14 -> 0.28: the split-K reduction by
 // one CTA and the per-token RoPE-table loads of the epilogue cost more than the idle SMs of the
 // CTA-pair kernel.  The split into K ranges depends on N and K only.
-static bool swap_enabled() {
-  static int on = -1;
-  if (on < 0) {
-    const char* e = getenv("FOCUS_GEMM_SWAP");
-    on = (e && e[0] == '1') ? 1 : 0;
-  }
-  return on == 1;
+static bool swap_enabled() {   // read per call (the tests switch it per context)
+  const char* e = getenv("FOCUS_GEMM_SWAP");
+  return e && e[0] == '1';
 }
 static bool swap_shape_ok(int N, int K, GemmMode mode, int M_max) {
   return swap_enabled() && M_max >= 1 && M_max <= 128 && K % tc::BK == 0 && N % (mode == GEMM_SWIGLU ? 256 : 128) == 0;

@@ -213,3 +213,12 @@ def test_layer_stages_unplanned_attention(monkeypatch):
     """Stage-wise parity with the attention unit table built in the kernel prologue (no plan kernel)."""
     monkeypatch.setenv("FOCUS_ATTN_NOPLAN", "1")
     test_layer_stages(MINI_G2, 8, 3, 2900, (0, 1, 2), 256)
+
+
+def test_layer_stages_swap_ab_gemm(monkeypatch):
+    """Stage-wise parity with the opt-in swap-AB split-K decode GEMM (M <= 128 live rows: weights on
+    the MMA M side, K ranges reduced in order by the tile's last CTA) for every projection and the LM
+    head (vocab statistics), at the 8B and 1.7B layer shapes."""
+    monkeypatch.setenv("FOCUS_GEMM_SWAP", "1")
+    test_layer_stages(M8B4, 16, 3, 100, (0, 1, 3), 64)
+    test_layer_stages(M1P7B3, 4, 5, 70, (0, 1, 2), 64)

@@ -326,3 +326,14 @@ def test_sharding_invariance_batch_invariant(model):
             del ctx
         outs[world] = toks
     assert outs[1] == outs[2] == outs[4]
+
+
+def test_resynced_swap_ab_gemm(monkeypatch):
+    """The whole step with the opt-in swap-AB decode GEMM (48 rows): rules bit-exact in the resynced
+    protocol, including the threshold regime."""
+    monkeypatch.setenv("FOCUS_GEMM_SWAP", "1")
+    mdl = dataclasses.replace(GQA_TC, logit_scale=16.0)
+    run = get_config("C1").with_(model=mdl, method=MethodConfig(block_size=8), n_requests=6, prompt_len=13,
+                                 gen_len=16, page_size=16)
+    st = _resync(run, [13] * 6)
+    assert st["above_tau"] > 0, st
