@@ -47,6 +47,7 @@ UNIT = "tokens/s"
 CALIBRATED_SCALE = {"C2": 16.0, "C3": 16.0, "C4": 16.0, "C5": 16.0}
 MODEL_NAME = {"C2": "SDAR-1.7B-shaped (random init)", "C3": "SDAR-8B-shaped (random init)",
               "C4": "SDAR-8B-shaped (random init)", "C5": "SDAR-8B-shaped (random init)",
+              "C3B64": "SDAR-8B-shaped (random init)",
               "C1": "tiny block-diffusion model (random init)"}
 
 

@@ -197,6 +197,8 @@ struct AttnArgs {
   int nch_fixed;                // 1: every non-causal unit runs the 64-row softmax variant (one hot copy)
   void* plan_units;             // unit table [grid][UCAP] precomputed by k_attn_plan, or nullptr
   int* plan_n;                  // [grid] units per CTA (nullptr: the kernel builds its table itself)
+  int pre_pf_tiles;             // key tiles of the first unit prefetched into L2 before the PDL wait
+  int max_slots;                // request slots (rows of the page table)
 };
 void launch_attention(const AttnArgs& a, cudaStream_t s);
 bool attn_tc_supported(int head_dim, int page_size, int group);

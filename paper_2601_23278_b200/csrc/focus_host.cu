@@ -497,6 +497,13 @@ AttnArgs attn_args(focus_ctx* x, int l, const bf16* q, int ldq, int n_req, const
   a.page_skip = (getenv("FOCUS_ATTN_PAGESKIP") && getenv("FOCUS_ATTN_PAGESKIP")[0] == '0') ? 0 : 1;
   a.kv_hint = (getenv("FOCUS_ATTN_L2HINT") && getenv("FOCUS_ATTN_L2HINT")[0] == '0') ? 0 : 1;
   a.imp_scratch = x->attn_scratch;
+  static int pre_pf = -1;
+  if (pre_pf < 0) {                              // FOCUS_ATTN_PRE_PF=n: first-unit tiles prefetched pre-wait
+    const char* e = getenv("FOCUS_ATTN_PRE_PF");
+    pre_pf = e ? std::max(0, atoi(e)) : 2;
+  }
+  a.pre_pf_tiles = pre_pf;
+  a.max_slots = x->cfg.max_requests;
   a.trace = (l == x->trace_layer && x->cfg.debug_taps >= 0) ? x->attn_trace : nullptr;
   return a;
 }

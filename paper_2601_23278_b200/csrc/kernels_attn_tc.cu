@@ -688,6 +688,34 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if (warp == 0 && lane == 0 && a.plan_n != nullptr && a.pre_pf_tiles > 0 && !IMP_ONLY) {
+    // Start-up: the first K/V tiles of this CTA's first unit are prefetched into L2 BEFORE the grid
+    // dependency wait, so they stream while the previous kernel (the QKV GEMM) drains; the TMA loads
+    // after the wait then hit L2 instead of paying the full loaded-HBM latency (~4 us for the first
+    // tile when every CTA starts at once).  The plan / page-table reads here may see data of an
+    // unfinished earlier kernel; a prefetch is only a hint, so a stale address costs a wasted fetch and
+    // never a wrong result (everything that is consumed is read after pdl_wait below).
+    const int n0 = a.plan_n[blockIdx.x];
+    if (n0 > 0) {
+      const Unit& x0 = static_cast<const Unit*>(a.plan_units)[(size_t)blockIdx.x * UCAP];
+      const int H = a.kv.n_kv_heads, ps = a.kv.page_size, pr = min(ps, KT);
+      const size_t layer_rows = (size_t)a.kv_pages * H * ps;
+      const int t_end = min(x0.t_hi, x0.t_lo + a.pre_pf_tiles);
+      if (x0.slot >= 0 && x0.slot < a.max_slots && x0.kvh >= 0 && x0.kvh < H && x0.t_hi - x0.t_lo < (1 << 16))
+        for (int t = max(x0.t_lo, 0); t < t_end; ++t)
+          for (int pc = 0; pc < KT / pr; ++pc) {
+            const int pos = t * KT + pc * pr;
+            if (pos >= x0.s0) break;                     // context keys only (the block's are being written)
+            const int pidx = max(0, min(pos / ps, a.kv.max_pages - 1));
+            const int page = a.kv.page_table[(size_t)x0.slot * a.kv.max_pages + pidx];
+            const int row = (int)((size_t)a.layer * layer_rows + ((size_t)page * H + x0.kvh) * ps + pos % ps);
+            tma_prefetch_2d(&mapK, 0, row);
+            tma_prefetch_2d(&mapK, 64, row);
+            tma_prefetch_2d(&mapV, 0, row);
+            tma_prefetch_2d(&mapV, 64, row);
+          }
+    }
+  }
   pdl_wait();                                       // plan tables, q rows, KV pages come from earlier kernels
   __shared__ int n_my_sh;
   __shared__ int merge_flag;

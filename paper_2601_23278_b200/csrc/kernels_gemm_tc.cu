@@ -1063,12 +1063,24 @@ __global__ void __launch_bounds__(swp::THREADS, 1)
         if (split == 1) {
           tmem_ld32(tb + c, v);
         } else {
+          // partials of range 0 -> v, then range s2 + 1's loads are in flight while range s2's are added
+          float nx[32];
+          const float* p0 = base + (size_t)c * 128 + f;
 #pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = 0.f;
-          for (int s2 = 0; s2 < split; ++s2) {
-            const float* p2 = base + (size_t)s2 * slot + (size_t)c * 128 + f;
+          for (int i = 0; i < 32; ++i) v[i] = __ldcg(p0 + (size_t)i * 128);
 #pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] += __ldcg(p2 + (size_t)i * 128);
+          for (int i = 0; i < 32; ++i) nx[i] = __ldcg(p0 + slot + (size_t)i * 128);
+          for (int s2 = 1; s2 < split; ++s2) {
+            float cur[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) cur[i] = nx[i];
+            if (s2 + 1 < split) {
+              const float* pn = p0 + (size_t)(s2 + 1) * slot;
+#pragma unroll
+              for (int i = 0; i < 32; ++i) nx[i] = __ldcg(pn + (size_t)i * 128);
+            }
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] += cur[i];
           }
         }
       };
@@ -1146,23 +1158,38 @@ __global__ void __launch_bounds__(swp::THREADS, 1)
           for (int i = 0; i < 32; ++i) xch[i * 128 + f] = v[i];
           named_bar(1, 128);
           const int kf = f & 63;
-#pragma unroll 4
+          // the chunk's RoPE factors and KV slots are loaded up front (independent loads in flight)
+          float cc[32], sn[32];
+          if (!is_v) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              const int t = min(t0 + i, M - 1);
+              cc[i] = __ldg(epi.ropeT + (size_t)kf * epi.rope_ld + t);
+              sn[i] = __ldg(epi.ropeT + (size_t)(64 + kf) * epi.rope_ld + t);
+            }
+          }
+          size_t kvo[32];
+          if (is_k || is_v) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              const RowInfo ri = epi.rows[min(t0 + i, M - 1)];
+              kvo[i] = kv_offset(epi.kv, ri.slot, ri.pos, kvh);
+              if (f == i && t0 + i < M && ri.j >= 0 && ((epi.st[ri.slot].committed >> ri.j) & 1ull))
+                atomicExch(&epi.cnt->invariant, 1);
+            }
+          }
+#pragma unroll
           for (int i = 0; i < 32; ++i) {
             const int t = t0 + i;
-            if (t >= M) break;
-            float y = v[i];
-            if (!is_v) {
-              const float other = xch[i * 128 + (f ^ 64)];
-              const float cc = __ldg(epi.ropeT + (size_t)kf * epi.rope_ld + t);
-              const float sn = __ldg(epi.ropeT + (size_t)(64 + kf) * epi.rope_ld + t);
-              y = f < 64 ? v[i] * cc - other * sn : v[i] * cc + other * sn;
-            }
-            const __nv_bfloat16 b = __float2bfloat16_rn(y);
-            epi.out[(size_t)t * epi.ldo + head * 128 + f] = b;
-            if (is_k || is_v) {
-              const RowInfo ri = epi.rows[t];
-              if (f == 0 && ri.j >= 0 && ((epi.st[ri.slot].committed >> ri.j) & 1ull)) atomicExch(&epi.cnt->invariant, 1);
-              (is_v ? epi.kv.V : epi.kv.K)[kv_offset(epi.kv, ri.slot, ri.pos, kvh) + f] = b;
+            if (t < M) {
+              float y = v[i];
+              if (!is_v) {
+                const float other = xch[i * 128 + (f ^ 64)];
+                y = f < 64 ? v[i] * cc[i] - other * sn[i] : v[i] * cc[i] + other * sn[i];
+              }
+              const __nv_bfloat16 b = __float2bfloat16_rn(y);
+              epi.out[(size_t)t * epi.ldo + head * 128 + f] = b;
+              if (is_k || is_v) (is_v ? epi.kv.V : epi.kv.K)[kvo[i] + f] = b;
             }
           }
           named_bar(1, 128);                             // xch reuse by the next chunk

@@ -89,6 +89,9 @@ CONFIGS = {
                     gen_len=512, description="SDAR-8B-shaped, block 16, batch 256 request-sharded, mixed prompts"),
     "C5": RunConfig("C5", SDAR_8B, MethodConfig(block_size=32), n_requests=32, prompt_len=16384, gen_len=1024,
                     description="SDAR-8B-shaped, block 32, long context"),
+    # the paper's large-block regime (fig:throughput_blocks P:506-511, 3.52x at B = 64)
+    "C3B64": RunConfig("C3B64", SDAR_8B, MethodConfig(block_size=64), n_requests=64, prompt_len=1024, gen_len=512,
+                       description="SDAR-8B-shaped, block 64, batch 64 (f3)"),
 }
 
 
