@@ -22,8 +22,9 @@ from __future__ import annotations
 import numpy as np
 
 from synth.configs import ModelConfig
-from synth.gen import (TID_EMBED, TID_LMHEAD, layer_tid, logit_scale_log2, weight_matrix)
+from synth.gen import (TID_EMBED, TID_LMHEAD, expert_tid, layer_tid, logit_scale_log2, weight_matrix)
 
+from . import moe as MOE
 from .numerics import attend, bf16_round, f32, rms_norm, rope, silu
 
 
@@ -54,11 +55,24 @@ class OracleWeights:
             "k": weight_matrix(layer_tid(l, "k"), hkv * dh, d, d, self.seed),
             "v": weight_matrix(layer_tid(l, "v"), hkv * dh, d, d, self.seed),
             "o": weight_matrix(layer_tid(l, "o"), d, hq * dh, hq * dh, self.seed),
-            "gate": weight_matrix(layer_tid(l, "gate"), ff, d, d, self.seed),
-            "up": weight_matrix(layer_tid(l, "up"), ff, d, d, self.seed),
-            "down": weight_matrix(layer_tid(l, "down"), d, ff, ff, self.seed),
         }
-        w = {k: v.astype(np.float64) for k, v in w.items()}
+        if c.is_moe_layer(l):
+            # MoE FFN (reading A-M5): router [E][d], routed experts e: gate/up [de][d], down [d][de];
+            # shared experts: gate/up [ns*de][d], down [d][ns*de]
+            de, E, ns = c.d_expert, c.n_experts, c.n_shared_experts
+            w["router"] = weight_matrix(layer_tid(l, "router"), E, d, d, self.seed)
+            w["experts"] = [{k: weight_matrix(expert_tid(l, k, e), *(shape + (fan,)), self.seed).astype(np.float64)
+                             for k, shape, fan in (("gate", (de, d), d), ("up", (de, d), d), ("down", (d, de), de))}
+                            for e in range(E)]
+            if ns:
+                w["sgate"] = weight_matrix(layer_tid(l, "sgate"), ns * de, d, d, self.seed)
+                w["sup"] = weight_matrix(layer_tid(l, "sup"), ns * de, d, d, self.seed)
+                w["sdown"] = weight_matrix(layer_tid(l, "sdown"), d, ns * de, ns * de, self.seed)
+        else:
+            w["gate"] = weight_matrix(layer_tid(l, "gate"), ff, d, d, self.seed)
+            w["up"] = weight_matrix(layer_tid(l, "up"), ff, d, d, self.seed)
+            w["down"] = weight_matrix(layer_tid(l, "down"), d, ff, ff, self.seed)
+        w = {k: (v.astype(np.float64) if k != "experts" else v) for k, v in w.items()}
         if self.cache:
             self._layers[l] = w
         return w
@@ -135,13 +149,44 @@ class Backbone:
         return self._f32(x + self._f32(o @ w["o"].T))
 
     def mlp(self, l: int, x: np.ndarray) -> np.ndarray:
-        """x + (silu(h Wg^T) * h Wu^T) Wd^T with h = RMSNorm(x)."""
+        """x + (silu(h Wg^T) * h Wu^T) Wd^T with h = RMSNorm(x); MoE layers: oracle/moe.py."""
         c, w = self.cfg, self.w.layer(l)
+        if c.is_moe_layer(l):
+            return self.moe(l, x)
         h = self._bf(rms_norm(x, 1.0, c.rms_eps))
         g = self._f32(h @ w["gate"].T)
         u = self._f32(h @ w["up"].T)
         a = self._bf(silu(g) * u)
         return self._f32(x + self._f32(a @ w["down"].T))
+
+    def moe_route(self, l: int, x: np.ndarray):
+        """Router of an MoE layer (A-M6): z = RMSNorm(x) W_r^T (fp32 in gpu mode) and each row's
+        [(expert, weight)] selection."""
+        c, w = self.cfg, self.w.layer(l)
+        h = self._bf(rms_norm(x, 1.0, c.rms_eps))
+        z = self._f32(h @ w["router"].T)
+        return h, z, [MOE.route(z[n], c.top_k) for n in range(z.shape[0])]
+
+    def moe(self, l: int, x: np.ndarray) -> np.ndarray:
+        """x + shared(h) + sum_k w_k expert_{e_k}(h) (A-M5).  gpu mode rounding points: router logits,
+        expert projections and outputs fp32, silu*mul bf16; the shared expert's output is added to the
+        residual first, then the routed experts' weighted sum (selection order, fp32)."""
+        c, w = self.cfg, self.w.layer(l)
+        f = self._f32 if self.mode == "gpu" else None
+        b = self._bf if self.mode == "gpu" else None
+        h, z, sel = self.moe_route(l, x)
+        x = np.asarray(x, dtype=np.float64)
+        if c.n_shared_experts:
+            x = self._f32(x + MOE.swiglu(h, w["sgate"], w["sup"], w["sdown"], f, b))
+        out = np.empty_like(x)
+        for n in range(x.shape[0]):
+            acc = np.zeros(x.shape[1])
+            for e, wt in sel[n]:
+                ex = w["experts"][e]
+                y = MOE.swiglu(h[n:n + 1], ex["gate"], ex["up"], ex["down"], f, b)[0]
+                acc = self._f32(acc + self._f32(self._f32(wt) * y))
+            out[n] = x[n] + acc
+        return self._f32(out)
 
     def logits(self, x: np.ndarray) -> np.ndarray:
         """z = RMSNorm(x) W_lm^T; z[mask id] = -inf (A-CF1)."""

@@ -27,6 +27,17 @@ class ModelConfig:
     rope_theta: float
     rms_eps: float = 1e-6
     logit_scale: float = 1.0             # W_lm scale, a power of two (focus_config::logit_scale)
+    # Mixture-of-Experts FFN (LLaDA2.0-mini-shaped workload; reading A-M5): layers
+    # >= n_dense_layers replace the dense SwiGLU by n_experts routed experts (top_k per token,
+    # d_expert wide) plus n_shared_experts shared experts; n_experts = 0: dense model
+    n_experts: int = 0
+    top_k: int = 0
+    d_expert: int = 0
+    n_shared_experts: int = 0
+    n_dense_layers: int = 1
+
+    def is_moe_layer(self, layer: int) -> bool:
+        return self.n_experts > 0 and layer >= self.n_dense_layers
 
     @property
     def mask_token_id(self) -> int:
@@ -77,6 +88,12 @@ SDAR_1P7B = ModelConfig(n_layers=28, d_model=2048, n_q_heads=16, n_kv_heads=8, h
                         d_ff=6144, vocab=151936, rope_theta=1e6)
 SDAR_8B = ModelConfig(n_layers=36, d_model=4096, n_q_heads=32, n_kv_heads=8, head_dim=128,
                       d_ff=12288, vocab=151936, rope_theta=1e6)
+# LLaDA2.0-mini-shaped MoE (16B total, ~1.4B active; PAPER.md P:426 gives only the totals -- the
+# layout is reading A-M5): 20 layers, d 2048, GQA 16/4 x 128, vocab 157184, layer 0 dense (d_ff 5120),
+# layers 1.. with 256 routed experts of width 512 (top-8) + 1 shared expert of width 512
+LLADA2_MINI = ModelConfig(n_layers=20, d_model=2048, n_q_heads=16, n_kv_heads=4, head_dim=128, d_ff=5120,
+                          vocab=157184, rope_theta=6e5, n_experts=256, top_k=8, d_expert=512,
+                          n_shared_experts=1, n_dense_layers=1)
 
 CONFIGS = {
     "C1": RunConfig("C1", TINY, MethodConfig(block_size=4), n_requests=1, prompt_len=16, gen_len=16,
@@ -89,6 +106,9 @@ CONFIGS = {
                     gen_len=512, description="SDAR-8B-shaped, block 16, batch 256 request-sharded, mixed prompts"),
     "C5": RunConfig("C5", SDAR_8B, MethodConfig(block_size=32), n_requests=32, prompt_len=16384, gen_len=1024,
                     description="SDAR-8B-shaped, block 32, long context"),
+    # the paper's second model family, LLaDA2.0-mini (MoE), at its default block 32
+    "C6": RunConfig("C6", LLADA2_MINI, MethodConfig(block_size=32), n_requests=64, prompt_len=1024, gen_len=512,
+                    description="LLaDA2.0-mini-shaped MoE, block 32, batch 64 (f4)"),
     # the paper's large-block regime (fig:throughput_blocks P:506-511, 3.52x at B = 64)
     "C3B64": RunConfig("C3B64", SDAR_8B, MethodConfig(block_size=64), n_requests=64, prompt_len=1024, gen_len=512,
                        description="SDAR-8B-shaped, block 64, batch 64 (f3)"),

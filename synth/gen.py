@@ -16,7 +16,8 @@ a rounding boundary: 255^2 * fan_in / 3 = 3*5^2*17^2*fan_in is never a power
 of 4, so log2(.) is never an integer.
 
 Tensor ids: embedding E = 1, LM head W_lm = 2, prompt tokens = 3, prompt
-lengths = 4; layer l: 16*(l+1) + {q:0, k:1, v:2, o:3, gate:4, up:5, down:6}.
+lengths = 4; layer l: 16*(l+1) + {q:0, k:1, v:2, o:3, gate:4, up:5, down:6, router:7, shared
+gate:8, shared up:9, shared down:10}; routed expert e of layer l: expert_tid(l, kind, e).
 """
 from __future__ import annotations
 
@@ -32,11 +33,19 @@ TID_EMBED = 1
 TID_LMHEAD = 2
 TID_PROMPT = 3
 TID_PROMPT_LEN = 4
-KIND = {"q": 0, "k": 1, "v": 2, "o": 3, "gate": 4, "up": 5, "down": 6}
+KIND = {"q": 0, "k": 1, "v": 2, "o": 3, "gate": 4, "up": 5, "down": 6, "router": 7, "sgate": 8, "sup": 9,
+        "sdown": 10}
+EXPERT_KIND = {"gate": 0, "up": 1, "down": 2}
 
 
 def layer_tid(layer: int, kind: str) -> int:
     return 16 * (layer + 1) + KIND[kind]
+
+
+def expert_tid(layer: int, kind: str, expert: int) -> int:
+    """Tensor id of routed expert `expert` of MoE layer `layer` (kind gate / up / down): a separate id
+    range 2^20 + (3 layer + kind) 2^12 + expert (tid < 2^24, so tid << 40 fits in 64 bits)."""
+    return (1 << 20) + ((3 * layer + EXPERT_KIND[kind]) << 12) + expert
 
 
 def mix64(z: np.ndarray) -> np.ndarray:
