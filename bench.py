@@ -47,7 +47,7 @@ UNIT = "tokens/s"
 CALIBRATED_SCALE = {"C2": 16.0, "C3": 16.0, "C4": 16.0, "C5": 16.0}
 MODEL_NAME = {"C2": "SDAR-1.7B-shaped (random init)", "C3": "SDAR-8B-shaped (random init)",
               "C4": "SDAR-8B-shaped (random init)", "C5": "SDAR-8B-shaped (random init)",
-              "C3B64": "SDAR-8B-shaped (random init)",
+              "C3B64": "SDAR-8B-shaped (random init)", "C6": "LLaDA2.0-mini-shaped MoE (random init)",
               "C1": "tiny block-diffusion model (random init)"}
 
 
@@ -169,17 +169,29 @@ def step_work(model, B, counters, states, rids):
     qkv = model.qkv_dim
     qd = model.n_q_heads * model.head_dim
     MP, MS, ML = counters
+    # dense FFN layers (rows: layer 0 on P, layers >= 1 on S); MoE models replace layers >= n_dense_layers
+    moe_layers = [l for l in range(L) if model.is_moe_layer(l)]
+    dense_parts = [(MP if l == 0 else MS, 1) for l in range(L) if not model.is_moe_layer(l)]
     shapes = {  # family: (N, K, rows per step [(rows, launches)], out bytes per element read+written)
         "gemm_qkv": (qkv, d, [(MP, 2), (MS, L - 2)], 2),
         "gemm_o": (d, qd, [(MP, 1), (MS, L - 1)], 8),
-        "gemm_gu": (2 * ff, d, [(MP, 1), (MS, L - 1)], 1),
-        "gemm_down": (d, ff, [(MP, 1), (MS, L - 1)], 8),
+        "gemm_gu": (2 * ff, d, dense_parts, 1),
+        "gemm_down": (d, ff, dense_parts, 8),
         "gemm_lm": (V, d, [(ML, 1)], 4),
     }
     fl, by = {}, {}
     for k, (N, K, parts, ob) in shapes.items():
         fl[k] = sum(2 * r * N * K * n for r, n in parts)
         by[k] = sum((2 * N * K + 2 * r * K + ob * r * N) * n for r, n in parts)
+    if moe_layers:
+        # MoE (A-M5): router GEMM; routed + shared experts (each row runs top_k + n_shared SwiGLU experts);
+        # weight bytes: every routed expert (all are touched at these row counts) and the shared ones
+        E, de, act = model.n_experts, model.d_expert, model.top_k + model.n_shared_experts
+        rows = [MP if l == 0 else MS for l in moe_layers]
+        fl["moe_route"] = sum(2 * r * d * E for r in rows)
+        by["moe_route"] = sum(2 * E * d + 2 * r * d + 4 * r * E for r in rows)
+        fl["moe_experts"] = sum(2 * r * act * 3 * d * de for r in rows)
+        by["moe_experts"] = sum(2 * (E + model.n_shared_experts) * 3 * d * de + r * act * (2 * d + 4 * d) for r in rows)
     kvb = 4 * model.n_kv_heads * model.head_dim          # K+V bf16 bytes per token per layer
     attn_bytes = attn_flops = 0
     for r in rids:
@@ -435,7 +447,7 @@ def roofline_report(pd, pk):
                      tflops=round(fl[k] / (v["total_ms"] / 1e3) / 1e12, 2),
                      gbs=round(by[k] / (v["total_ms"] / 1e3) / 1e9, 1))
         kernels[k] = e
-    cands = [k for k in kernels if k in fl]
+    cands = [k for k in kernels if k in fl and prof[k]["launches"]]
     dom = max(cands, key=lambda k: prof[k]["total_ms"])
     n_l = prof[dom]["launches"]
     ms_l = prof[dom]["total_ms"] / n_l
@@ -454,7 +466,7 @@ def roofline_report(pd, pk):
     roof.update(kernel=names.get(dom, f"k_gemm_pair ({dom}) per layer"), traffic=traffic.get(dom),
                 launch_ms=round(ms_l, 4), launches_per_step=n_l // n, share_of_step=e["share"],
                 timing="CUDA events around every launch on the library stream, 2 profiled steps after the middle window")
-    proj = ["gemm_qkv", "gemm_o", "gemm_gu", "gemm_down"]
+    proj = [k for k in ("gemm_qkv", "gemm_o", "gemm_gu", "gemm_down", "moe_experts") if prof.get(k, {}).get("launches")]
     g_ms = sum(prof[k]["total_ms"] for k in proj)
     g_fl = sum(fl[k] for k in proj)
     ach_all = g_fl / (g_ms / 1e3) / 1e12

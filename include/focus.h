@@ -87,6 +87,12 @@ typedef struct {
                               partial softmaxes (equal up to fp32 rounding).  Set it when requests
                               are sharded across GPUs and per-request outputs must be identical at
                               every world size.  0 = fastest (default).        */
+  /* Mixture-of-Experts FFN (LLaDA2.0-mini-shaped workload; readings A-M5, A-M6): with
+     n_experts > 0 the layers l >= n_dense_layers replace the dense SwiGLU by a router (top_k of
+     n_experts by logit, softmax over the selected logits), n_experts routed SwiGLU experts of width
+     d_expert and n_shared_experts shared ones; run on the compacted rows like every layer.
+     n_experts <= 1024, 1 <= top_k <= min(16, n_experts), d_expert % 128 == 0; 0 = dense model. */
+  int32_t n_experts, top_k, d_expert, n_shared_experts, n_dense_layers;
 } focus_config;
 
 typedef struct focus_ctx focus_ctx;
@@ -176,9 +182,16 @@ enum {
   FOCUS_DBG_LAUNCHES = 30,  /* uint64: kernels launched by this context so far                */
   FOCUS_DBG_PROFILE = 31,   /* focus_prof_entry[FOCUS_PROF_KINDS] accumulated since the last
                                focus_set_profile(ctx, 1)                                       */
-  FOCUS_DBG_ATTN_TRACE = 32 /* uint64[grid][8 roles][512]: clock64 event trace of the last
+  FOCUS_DBG_ATTN_TRACE = 32, /* uint64[grid][8 roles][512]: clock64 event trace of the last
                                tensor-core attention launch of layer FOCUS_ATTN_TRACE_LAYER
                                (env var read at focus_init; empty otherwise)                   */
+  FOCUS_DBG_MOE_SEL = 33,   /* int32[M_S][top_k]: experts selected for the rows of the last MoE
+                               layer of the last step (selection order)                        */
+  FOCUS_DBG_MOE_WT = 34,    /* float[M_S][top_k]: their routing weights                        */
+  FOCUS_DBG_MOE_ROWS = 35,  /* int32[M_S * top_k] token row of each gathered (expert-contiguous)
+                               row, then int32[n_experts + 1] expert offsets                   */
+  FOCUS_DBG_MOE_Y = 36,     /* float[M_S * top_k][d] expert outputs of the gathered rows        */
+  FOCUS_DBG_MOE_AG = 37     /* bf16[M_S * top_k][d] gathered expert inputs                      */
 };
 
 /* Per-kernel-kind device time measured with CUDA events on the context stream around every launch
@@ -187,7 +200,8 @@ enum {
   FOCUS_PROF_SETUP = 0, FOCUS_PROF_EMBED, FOCUS_PROF_RMSNORM, FOCUS_PROF_GEMM_QKV, FOCUS_PROF_ROPE_STORE /* RoPE: unfused store, or the per-row factor tables */,
   FOCUS_PROF_ATTN, FOCUS_PROF_IMPORTANCE, FOCUS_PROF_GEMM_O, FOCUS_PROF_GEMM_GU, FOCUS_PROF_SILU,
   FOCUS_PROF_GEMM_DOWN, FOCUS_PROF_SELECT, FOCUS_PROF_GATHER, FOCUS_PROF_GEMM_LM, FOCUS_PROF_VOCAB,
-  FOCUS_PROF_COMMIT, FOCUS_PROF_KINDS
+  FOCUS_PROF_COMMIT, FOCUS_PROF_MOE_ROUTE /* router GEMM, top-k, placement, gather */,
+  FOCUS_PROF_MOE_EXPERTS /* grouped expert GEMMs + shared expert */, FOCUS_PROF_MOE_COMBINE, FOCUS_PROF_KINDS
 };
 typedef struct {
   int32_t kind, launches;

@@ -228,6 +228,17 @@ void launch_select_plan(const SelectArgs& a, cudaStream_t s);
 
 void launch_vocab_reduce(const float* logits, const int* M_dev, int M_max, int V, int mask_id, int nch,
                          VocabPartial* part, cudaStream_t s);
+// MoE FFN (kernels_moe.cu, grouped expert GEMM in kernels_gemm_tc.cu)
+void launch_moe_route(const float* z, int ldz, const int* M_dev, int M_max, int E, int K, int* sel, float* wt, int* cnt,
+                      cudaStream_t s);
+void launch_moe_place(const int* sel, const int* cnt, const int* M_dev, int M_max, int E, int K, int* off, int* tok_of,
+                      int* slot_of, cudaStream_t s);
+void launch_moe_gather(const bf16* h, const int* tok_of, const int* M_dev, int M_max, int K, int d, bf16* Ag,
+                       cudaStream_t s);
+void launch_moe_combine(const float* y, const int* slot_of, const float* wt, const int* M_dev, int M_max, int K, int d,
+                        float* x, int* cnt, int E, cudaStream_t s);
+bool launch_gemm_grouped(const bf16* A, int a_rows, const bf16* W, int n_experts, int wrows, int K, float* C, int ldc,
+                         const int* off, int M_max_rows, GemmMode mode, const GemmEpi* epi, cudaStream_t s);
 // combine the LM-head epilogue's per-64-column partials of each logit row (fixed order) -> out[row]
 void launch_vocab_combine(const VocabPartial* tiles, int ngroups, const int* M_dev, int M_max, VocabPartial* out,
                           cudaStream_t s);

@@ -61,6 +61,11 @@ int weight_exp(int fan_in) {
   return -(int)std::ceil(std::log2(255.0 * std::sqrt((double)fan_in / 3.0)));
 }
 
+bool is_moe(const focus_config& c, int layer) { return c.n_experts > 0 && layer >= c.n_dense_layers; }
+
+// synth/gen.py expert_tid: routed expert e of layer l, kind 0 gate / 1 up / 2 down
+uint64_t expert_tid(int layer, int kind, int e) { return (1ull << 20) + ((uint64_t)(3 * layer + kind) << 12) + e; }
+
 }  // namespace
 
 struct focus_ctx {
@@ -88,6 +93,18 @@ struct focus_ctx {
   bf16* E = nullptr;
   bf16* Wlm = nullptr;
   std::vector<bf16*> Wqkv, Wo, Wgu, Wd;
+  // MoE layers (A-M5): router [E][d], routed experts gate/up [E][2 de][d] (interleaved by 128 rows per
+  // expert) and down [E][d][de], shared experts gate/up [2 ns de][d] and down [d][ns de]
+  std::vector<bf16*> Wr, Wxgu, Wxd, Wsgu, Wsd;
+  int* moe_sel = nullptr;          // [rows][top_k] selected experts (selection order)
+  float* moe_wt = nullptr;         // [rows][top_k] routing weights
+  int* moe_cnt = nullptr;          // [E] tokens per expert
+  int* moe_off = nullptr;          // [E + 1] expert offsets into the gathered rows
+  int* moe_tok = nullptr;          // [rows * top_k] gathered row -> token row
+  int* moe_slot = nullptr;         // [rows][top_k] token row, k -> gathered row
+  bf16* moe_Ag = nullptr;          // [rows * top_k + 64][d] gathered expert inputs
+  bf16* moe_act = nullptr;         // [rows * top_k + 64][de] expert SwiGLU activations
+  float* moe_y = nullptr;          // [rows * top_k][d] expert outputs
   // KV pool
   bf16* Kpool = nullptr;
   bf16* Vpool = nullptr;
@@ -107,6 +124,7 @@ struct focus_ctx {
   Counters* cnt = nullptr;
   float *I0p = nullptr, *I1p = nullptr;
   VocabPartial* vpart = nullptr;
+  focus_status sticky = FOCUS_OK;  // launch-time failure reported by the next focus_sync
   VocabPartial* vtiles = nullptr;  // LM-head epilogue partials [logit row][64-column group]
   bool vocab_fused = false;        // LM head emits vtiles (tensor-core GEMM); logits stored only with taps
   TokConf* tokconf = nullptr;
@@ -182,6 +200,12 @@ bool valid_config(const focus_config& c) {
   if (G > kAttnQRows) return false;
   if ((c.n_q_heads * c.head_dim) % 64) return false;
   if (c.batch_invariant < 0 || c.batch_invariant > 1) return false;
+  if (c.n_experts < 0 || c.n_experts > 1024) return false;
+  if (c.n_experts > 0) {
+    if (c.top_k < 1 || c.top_k > 16 || c.top_k > c.n_experts) return false;
+    if (c.d_expert <= 0 || c.d_expert % 128 || c.n_shared_experts < 0 || c.n_shared_experts > 8) return false;
+    if (c.n_dense_layers < 0 || c.n_dense_layers > c.n_layers) return false;
+  }
   if (c.logit_scale != 0.f) {                     // a power of two in [2^-16, 2^16] (W_lm stays exact)
     int e = 0;
     const float m = std::frexp(c.logit_scale, &e);
@@ -213,11 +237,24 @@ size_t carve(focus_ctx* x, char* base) {
   x->E = (bf16*)take(V * d * 2);
   x->Wlm = (bf16*)take(V * d * 2);
   x->Wqkv.assign(L, nullptr); x->Wo.assign(L, nullptr); x->Wgu.assign(L, nullptr); x->Wd.assign(L, nullptr);
+  x->Wr.assign(L, nullptr); x->Wxgu.assign(L, nullptr); x->Wxd.assign(L, nullptr);
+  x->Wsgu.assign(L, nullptr); x->Wsd.assign(L, nullptr);
+  const size_t E = c.n_experts, de = c.d_expert, ns = c.n_shared_experts;
   for (size_t l = 0; l < L; ++l) {
     x->Wqkv[l] = (bf16*)take(qkv * d * 2);
     x->Wo[l] = (bf16*)take(d * qd * 2);
-    x->Wgu[l] = (bf16*)take(2 * ff * d * 2);
-    x->Wd[l] = (bf16*)take(d * ff * 2);
+    if (is_moe(c, (int)l)) {
+      x->Wr[l] = (bf16*)take(E * d * 2);
+      x->Wxgu[l] = (bf16*)take(E * 2 * de * d * 2);
+      x->Wxd[l] = (bf16*)take(E * d * de * 2);
+      if (ns) {
+        x->Wsgu[l] = (bf16*)take(2 * ns * de * d * 2);
+        x->Wsd[l] = (bf16*)take(d * ns * de * 2);
+      }
+    } else {
+      x->Wgu[l] = (bf16*)take(2 * ff * d * 2);
+      x->Wd[l] = (bf16*)take(d * ff * 2);
+    }
   }
   x->Kpool = (bf16*)take(L * x->kv_layer_elems * 2);
   x->Vpool = (bf16*)take(L * x->kv_layer_elems * 2);
@@ -258,6 +295,18 @@ size_t carve(focus_ctx* x, char* base) {
   x->vtiles = (VocabPartial*)take(RL * ((V + 63) / 64) * sizeof(VocabPartial));
   x->tokconf = (TokConf*)take(RL * sizeof(TokConf));
   x->res_dev = (focus_commit_result*)take(c.max_requests * sizeof(focus_commit_result));
+  if (E) {
+    const size_t RK = R * c.top_k;
+    x->moe_sel = (int*)take(RK * 4);
+    x->moe_wt = (float*)take(RK * 4);
+    x->moe_cnt = (int*)take(E * 4);
+    x->moe_off = (int*)take((E + 1) * 4);
+    x->moe_tok = (int*)take(RK * 4);
+    x->moe_slot = (int*)take(RK * 4);
+    x->moe_Ag = (bf16*)take((RK + 64) * d * 2);
+    x->moe_act = (bf16*)take((RK + 64) * de * 2);
+    x->moe_y = (float*)take(RK * d * 4);
+  }
   if (x->attn_tc) {
     const size_t pairs = (size_t)c.max_requests * x->n_chunks * c.n_kv_heads;
     x->attn_part = (float*)take(pairs * x->max_nsplit * ((size_t)128 * c.head_dim + 256) * 4);
@@ -437,6 +486,48 @@ void qkv_piece(focus_ctx* x, int l, int tl, float* xr, const RowSpace& rs) {
   tap(x, tl, TAP_ROWS, rs.rows, (size_t)rs.M_max * sizeof(RowInfo));
 }
 
+// MoE FFN of layer l on the rows `rs` (A-M5, A-M6): h = RMSNorm(x) is in x->h.  Router GEMM -> top-k
+// routing -> expert-contiguous placement -> gathered rows -> grouped expert GEMMs (gate/up + SwiGLU,
+// down) -> shared expert (x += shared(h)) -> x += sum_k w_k y_k (selection order).
+void moe_piece(focus_ctx* x, int l, int tl, float* xr, const RowSpace& rs) {
+  const focus_config& c = x->cfg;
+  cudaStream_t s = x->stream;
+  const int E = c.n_experts, K = c.top_k, d = c.d_model, de = c.d_expert;
+  const int RK = x->max_rows * K;
+  LAUNCH(MOE_ROUTE, {
+    launch_gemm(x->h, d, x->max_rows, x->Wr[l], E, d, x->f32tmp, E, rs.M_dev, rs.M_max, GEMM_STORE, x->gws, s, rs.M_est);
+    launch_moe_route(x->f32tmp, E, rs.M_dev, rs.M_max, E, K, x->moe_sel, x->moe_wt, x->moe_cnt, s);
+    launch_moe_place(x->moe_sel, x->moe_cnt, rs.M_dev, rs.M_max, E, K, x->moe_off, x->moe_tok, x->moe_slot, s);
+    launch_moe_gather(x->h, x->moe_tok, rs.M_dev, rs.M_max, K, d, x->moe_Ag, s);
+  });
+  x->launches += 3;                               // the group above launched 4 kernels
+  bool ok = true;
+  LAUNCH(MOE_EXPERTS, {
+    GemmEpi e{};
+    e.out = x->moe_act;
+    e.ldo = de;
+    ok = launch_gemm_grouped(x->moe_Ag, RK + 64, x->Wxgu[l], E, 2 * de, d, nullptr, 0, x->moe_off,
+                             rs.M_max, GEMM_SWIGLU, &e, s) &&
+         launch_gemm_grouped(x->moe_act, RK + 64, x->Wxd[l], E, d, de, x->moe_y, d, x->moe_off, rs.M_max,
+                             GEMM_STORE, nullptr, s);
+    if (c.n_shared_experts) {                     // shared experts: dense SwiGLU on every row, residual add
+      GemmEpi es{};
+      es.out = x->act;
+      es.ldo = c.n_shared_experts * de;
+      const int nsd = c.n_shared_experts * de;
+      ok = ok && launch_gemm_tc(x->h, d, x->max_rows, x->Wsgu[l], 2 * nsd, d, nullptr, 0, rs.M_dev, rs.M_max,
+                                GEMM_SWIGLU, x->gws, s, &es, rs.M_est);
+      launch_gemm(x->act, nsd, x->max_rows, x->Wsd[l], d, nsd, xr, d, rs.M_dev, rs.M_max, GEMM_ADD, x->gws, s,
+                  rs.M_est);
+    }
+  });
+  x->launches += c.n_shared_experts ? 3 : 1;
+  if (!ok) x->sticky = FOCUS_ERR_CUDA;
+  tap(x, tl, TAP_ACT, x->moe_act, (size_t)rs.M_max * de * 2);
+  LAUNCH(MOE_COMBINE, launch_moe_combine(x->moe_y, x->moe_slot, x->moe_wt, rs.M_dev, rs.M_max, K, d, xr, x->moe_cnt, E, s));
+  tap(x, tl, TAP_X_OUT, xr, (size_t)rs.M_max * d * 4);
+}
+
 void out_mlp_piece(focus_ctx* x, int l, int tl, float* xr, const RowSpace& rs) {
   const focus_config& c = x->cfg;
   cudaStream_t s = x->stream;
@@ -446,6 +537,10 @@ void out_mlp_piece(focus_ctx* x, int l, int tl, float* xr, const RowSpace& rs) {
   tap(x, tl, TAP_X_MID, xr, (size_t)rs.M_max * c.d_model * 4);
   LAUNCH(RMSNORM, launch_rmsnorm(xr, nullptr, rs.M_dev, rs.M_max, c.d_model, c.rms_eps, x->h, s));
   tap(x, tl, TAP_H2, x->h, (size_t)rs.M_max * c.d_model * 2);
+  if (is_moe(c, l)) {
+    moe_piece(x, l, tl, xr, rs);
+    return;
+  }
   // tensor-core GEMM with the SwiGLU epilogue; otherwise GEMM -> fp32 -> k_silu_mul
   GemmEpi e{};
   e.out = x->act; e.ldo = c.d_ff;
@@ -589,9 +684,25 @@ focus_status focus_init(const focus_config* cfg, void* dev_arena, size_t arena_b
     launch_init_weights(x->Wqkv[l] + (size_t)qd * d, kd, d, t0 + 1, seed, weight_exp(d), 0, 0, s);
     launch_init_weights(x->Wqkv[l] + (size_t)(qd + kd) * d, kd, d, t0 + 2, seed, weight_exp(d), 0, 0, s);
     launch_init_weights(x->Wo[l], d, qd, t0 + 3, seed, weight_exp(qd), 0, 0, s);
-    launch_init_weights(x->Wgu[l], ff, d, t0 + 4, seed, weight_exp(d), kGuGroup, 0, s);
-    launch_init_weights(x->Wgu[l], ff, d, t0 + 5, seed, weight_exp(d), kGuGroup, 1, s);
-    launch_init_weights(x->Wd[l], d, ff, t0 + 6, seed, weight_exp(ff), 0, 0, s);
+    if (is_moe(c, l)) {
+      const int E = c.n_experts, de = c.d_expert, nsd = c.n_shared_experts * c.d_expert;
+      launch_init_weights(x->Wr[l], E, d, t0 + 7, seed, weight_exp(d), 0, 0, s);
+      for (int e = 0; e < E; ++e) {
+        bf16* gu = x->Wxgu[l] + (size_t)e * 2 * de * d;
+        launch_init_weights(gu, de, d, expert_tid(l, 0, e), seed, weight_exp(d), kGuGroup, 0, s);
+        launch_init_weights(gu, de, d, expert_tid(l, 1, e), seed, weight_exp(d), kGuGroup, 1, s);
+        launch_init_weights(x->Wxd[l] + (size_t)e * d * de, d, de, expert_tid(l, 2, e), seed, weight_exp(de), 0, 0, s);
+      }
+      if (nsd) {
+        launch_init_weights(x->Wsgu[l], nsd, d, t0 + 8, seed, weight_exp(d), kGuGroup, 0, s);
+        launch_init_weights(x->Wsgu[l], nsd, d, t0 + 9, seed, weight_exp(d), kGuGroup, 1, s);
+        launch_init_weights(x->Wsd[l], d, nsd, t0 + 10, seed, weight_exp(nsd), 0, 0, s);
+      }
+    } else {
+      launch_init_weights(x->Wgu[l], ff, d, t0 + 4, seed, weight_exp(d), kGuGroup, 0, s);
+      launch_init_weights(x->Wgu[l], ff, d, t0 + 5, seed, weight_exp(d), kGuGroup, 1, s);
+      launch_init_weights(x->Wd[l], d, ff, t0 + 6, seed, weight_exp(ff), 0, 0, s);
+    }
   }
   // RoPE table in binary64 on the host (angle pos * theta^(-2k/dh), rotate-half pairs)
   {
@@ -630,6 +741,7 @@ focus_status focus_init(const focus_config* cfg, void* dev_arena, size_t arena_b
     }
   }
   cudaMemsetAsync(x->gws.sem, 0, x->gws.sem_count * 4, s);
+  if (x->moe_cnt) cudaMemsetAsync(x->moe_cnt, 0, (size_t)c.n_experts * 4, s);
   cudaMemsetAsync(x->page_table, 0, (size_t)c.max_requests * x->max_pages_per_req * 4, s);
   cudaMemsetAsync(x->out_tokens, 0, (size_t)c.max_requests * x->max_gen * 4, s);
   for (int k = 0; k < FOCUS_PROF_KINDS; ++k) x->prof_acc[k] = focus_prof_entry{k, 0, 0.f, 0.f};
@@ -817,6 +929,14 @@ static std::vector<int> shape_key(const focus_ctx* x, int maxP, const Counters& 
     k.push_back(gemm_tc_choice(c.d_model, c.d_ff, GEMM_ADD, maxP, m, !x->gws.no_swap));
   }
   k.push_back(gemm_tc_choice(c.vocab, c.d_model, GEMM_STORE, maxP, e.M_L, !x->gws.no_swap));
+  if (c.n_experts > 0) {                          // MoE: router and shared-expert GEMMs (S rows)
+    const int nsd = c.n_shared_experts * c.d_expert;
+    k.push_back(gemm_tc_choice(c.n_experts, c.d_model, GEMM_STORE, maxP, e.M_S, !x->gws.no_swap));
+    if (nsd) {
+      k.push_back(gemm_tc_choice(2 * nsd, c.d_model, GEMM_SWIGLU, maxP, e.M_S, !x->gws.no_swap));
+      k.push_back(gemm_tc_choice(c.d_model, nsd, GEMM_ADD, maxP, e.M_S, !x->gws.no_swap));
+    }
+  }
   return k;
 }
 
@@ -1092,6 +1212,7 @@ focus_status focus_commit(focus_ctx* x, const int32_t* ids, int32_t n_req, focus
 
 focus_status focus_sync(focus_ctx* x) {
   if (!x) return FOCUS_ERR_STATE;
+  if (x->sticky != FOCUS_OK) return x->sticky;
   focus_status rc = cuda_status(cudaStreamSynchronize(x->stream));
   if (rc != FOCUS_OK) return rc;
   int inv = 0;
@@ -1156,6 +1277,19 @@ focus_status focus_debug_export(focus_ctx* x, int32_t what, int32_t req_id, int3
     case FOCUS_DBG_LOGITS: src = x->logits; bytes = (size_t)cnt.M_L * c.vocab * 4; break;
     case FOCUS_DBG_TOKCONF: src = x->tokconf; bytes = (size_t)cnt.M_L * sizeof(TokConf); break;
     case FOCUS_DBG_HL: src = x->h; bytes = (size_t)cnt.M_L * c.d_model * 2; break;
+    case FOCUS_DBG_MOE_SEL: src = x->moe_sel; bytes = x->moe_sel ? (size_t)cnt.M_S * c.top_k * 4 : 0; break;
+    case FOCUS_DBG_MOE_WT: src = x->moe_wt; bytes = x->moe_wt ? (size_t)cnt.M_S * c.top_k * 4 : 0; break;
+    case FOCUS_DBG_MOE_AG: src = x->moe_Ag; bytes = x->moe_Ag ? (size_t)cnt.M_S * c.top_k * c.d_model * 2 : 0; break;
+    case FOCUS_DBG_MOE_Y: src = x->moe_y; bytes = x->moe_y ? (size_t)cnt.M_S * c.top_k * c.d_model * 4 : 0; break;
+    case FOCUS_DBG_MOE_ROWS: {
+      if (!x->moe_tok) { *n_written = 0; return FOCUS_OK; }
+      const size_t a = (size_t)cnt.M_S * c.top_k * 4, b = (size_t)(c.n_experts + 1) * 4;
+      if (cap < a + b) return FOCUS_ERR_IO;
+      cudaMemcpy(dst, x->moe_tok, a, cudaMemcpyDeviceToHost);
+      cudaMemcpy((char*)dst + a, x->moe_off, b, cudaMemcpyDeviceToHost);
+      *n_written = a + b;
+      return cuda_status(cudaGetLastError());
+    }
     case FOCUS_DBG_ATTN_TRACE: src = x->attn_trace; bytes = x->attn_trace ? (size_t)num_sms() * 8 * kTraceEv * 8 : 0; break;
     case FOCUS_DBG_LAUNCHES:
       if (cap < 8) return FOCUS_ERR_IO;

@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(1024) k_commit(CommitArgs a) {
       if (res && lane == 0) { res->req_id = slot; res->n_new = 0; res->block_done = 0; res->finished = st.finished; res->n_committed = 0; }
       continue;
     }
-    const int lo = a.offL[i], nL = a.offL[i + 1] - lo;
+    const int lo = __ldcg(a.offL + i), nL = __ldcg(a.offL + i + 1) - lo;   // written by the selection, kernels back
     // per logit row: combine chunk partials (fixed order)
     float cf[2] = {-1.f, -1.f};
     int tk[2] = {0, 0}, jp[2] = {-1, -1};
@@ -157,7 +157,7 @@ __global__ void __launch_bounds__(1024) k_commit(CommitArgs a) {
         for (int c = 1; c < a.nch; ++c) p = vp_combine(p, a.part[(size_t)(lo + k) * a.nch + c]);
         cf[t] = 1.0f / p.s;
         tk[t] = p.idx;
-        jp[t] = a.rowL[lo + k].j;
+        jp[t] = __ldcg(&a.rowL[lo + k].j);
         a.tokconf[lo + k] = TokConf{p.idx, cf[t]};
       }
     }

@@ -1205,6 +1205,133 @@ __global__ void __launch_bounds__(swp::THREADS, 1)
   }
 }
 
+
+// Grouped swap-AB GEMM over experts (MoE FFN, readings A-M5/A-M6): expert e owns the rows
+// [off[e], off[e+1]) of the gathered activations A (the tokens routed to e, in row order) and the
+// weight rows [e * wrows, (e + 1) * wrows) of W; CTA (e, tile) computes the features
+// [tile * 128, tile * 128 + 128) of expert e (SWIGLU: its gate and up tiles, 256 weight rows) for all
+// of e's rows, NT at a time (one TMEM accumulator, handed between the MMA issuer and the epilogue per
+// chunk).  An expert with no tokens costs its CTAs one barrier setup and no weight traffic.
+//   SWIGLU  act[p][f] = bf16(silu(gate) * up)   (p = gathered row)
+//   STORE   C[p][f] = acc (fp32)
+template <int MODE, int NT>
+__global__ void __launch_bounds__(swp::THREADS, 1)
+    k_gemm_grouped(const __grid_constant__ CUtensorMap mapW, const __grid_constant__ CUtensorMap mapA,
+                   float* __restrict__ C, int ldc, int K, const int* __restrict__ off, int wrows, int tiles,
+                   const GemmEpi epi) {
+  constexpr bool GU = MODE == GEMM_SWIGLU;
+  using L = swp::SL<NT, GU>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* bars = (uint64_t*)(smem + L::STAGES * L::STAGE + L::XCH);
+  uint64_t* full = bars;                                // [STAGES]
+  uint64_t* empty = bars + L::STAGES;                   // [STAGES]
+  uint64_t* tfull = bars + 2 * L::STAGES;               // [1]
+  uint64_t* tempty = tfull + 1;                         // [1] (4 epilogue warps)
+  uint32_t* tmem_sh = (uint32_t*)(tempty + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int e = blockIdx.x / tiles, tile = blockIdx.x % tiles;
+  pdl_trigger();
+  if (warp == 0 && lane == 0) {
+    for (int i = 0; i < L::STAGES; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+    mbar_init(&tfull[0], 1);
+    mbar_init(&tempty[0], 4);
+    fence_barrier_init();
+    prefetch_map(&mapW);
+    prefetch_map(&mapA);
+  }
+  if (warp == 2) tmem_alloc<L::TCOLS>(tmem_sh);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_sh;
+  pdl_wait();                                           // the expert offsets and rows come from earlier kernels
+  // (L2 loads: the offsets were written two kernels back, and under programmatic dependent launch an L1
+  // line of an earlier co-resident grid may still hold the previous layer's values)
+  const int r0 = __ldcg(off + e), n = __ldcg(off + e + 1) - r0;
+  const int chunks = n > 0 ? (n + NT - 1) / NT : 0;
+  const int kbt = K / BK;
+  const int wrow0 = e * wrows + tile * 128 * L::NW;
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint64_t pol = l2_policy_evict_first();
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int c = 0; c < chunks; ++c)
+        for (int kb = 0; kb < kbt; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* st = smem + stage * L::STAGE;
+          mbar_expect_tx(&full[stage], L::STAGE);
+          tma_load_2d_hint(st, &mapW, &full[stage], kb * BK, wrow0, pol);
+          if (GU) tma_load_2d_hint(st + 128 * BK * 2, &mapW, &full[stage], kb * BK, wrow0 + 128, pol);
+          tma_load_2d(st + L::W_BYTES, &mapA, &full[stage], kb * BK, r0 + c * NT);
+          if (++stage == L::STAGES) { stage = 0; phase ^= 1; }
+        }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_bf16(128, NT, false, false);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int c = 0; c < chunks; ++c) {
+        mbar_wait(&tempty[0], (c & 1) ^ 1);             // the epilogue has read the previous chunk
+        tc_fence_after();
+        for (int kb = 0; kb < kbt; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t w0 = smem_u32(smem + stage * L::STAGE), a0 = w0 + L::W_BYTES;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint32_t acc = (kb > 0 || k > 0) ? 1u : 0u;
+            mma_bf16(tmem, desc_kmajor_sw128(w0 + k * 32), desc_kmajor_sw128(a0 + k * 32), idesc, acc);
+            if (GU) mma_bf16(tmem + NT, desc_kmajor_sw128(w0 + 128 * BK * 2 + k * 32), desc_kmajor_sw128(a0 + k * 32), idesc, acc);
+          }
+          mma_commit(&empty[stage]);
+          if (++stage == L::STAGES) { stage = 0; phase ^= 1; }
+        }
+        mma_commit(&tfull[0]);
+      }
+    }
+  } else if (warp >= 4) {
+    const int f = threadIdx.x - 128, q = warp - 4;
+    const uint32_t tb = tmem + ((uint32_t)(q * 32) << 16);
+    const int feat = tile * 128 + f;
+    for (int c = 0; c < chunks; ++c) {
+      mbar_wait(&tfull[0], c & 1);
+      tc_fence_after();
+      const int nc = min(NT, n - c * NT);               // rows of this chunk
+#pragma unroll 1
+      for (int t0 = 0; t0 < NT; t0 += 32) {
+        if (t0 >= nc) break;
+        float v[32];
+        tmem_ld32(tb + t0, v);
+        if constexpr (GU) {
+          float u[32];
+          tmem_ld32(tb + NT + t0, u);
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (t0 + i < nc) {
+              const float a = __fdividef(v[i] * u[i], 1.0f + exp2f(-1.4426950408889634f * v[i]));
+              epi.out[(size_t)(r0 + c * NT + t0 + i) * epi.ldo + feat] = __float2bfloat16_rn(a);
+            }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (t0 + i < nc) __stcg(C + (size_t)(r0 + c * NT + t0 + i) * ldc + feat, v[i]);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[0]);
+    }
+  }
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_free<L::TCOLS>(tmem);
+  }
+}
+
 // ka = 0: 2-D map [rows][cols], box box_rows x 64.  ka >= 1: 3-D view {64, rows, cols / 64} of the same
 // matrix (k-atom stride 128 B), box {64, box_rows, ka} = ka consecutive SW128 K-major tiles.
 bool get_map(const void* ptr, int rows, int cols, int ld, int box_rows, CUtensorMap* out, int ka = 0) {
@@ -1492,6 +1619,38 @@ static int split_parts(int K) {
 static int env_flag(const char* name, int& cache) {
   if (cache < 0) cache = getenv(name) != nullptr ? 1 : 0;
   return cache;
+}
+
+
+// Grouped expert GEMM of an MoE layer (k_gemm_grouped): A = gathered rows [a_rows][K] (tokens routed to
+// each expert, expert-contiguous, offsets off[E + 1] on the device), W = E experts x wrows rows of K.
+// SWIGLU: wrows = 2 d_expert (gate/up interleaved by 128 rows), out act [rows][d_expert] bf16;
+// STORE: wrows = N (feature rows per expert), out C [rows][ldc] fp32.
+bool launch_gemm_grouped(const bf16* A, int a_rows, const bf16* W, int n_experts, int wrows, int K, float* C, int ldc,
+                         const int* off, int M_max_rows, GemmMode mode, const GemmEpi* epi, cudaStream_t s) {
+  using namespace tc;
+  if (K % BK || wrows % 128 || (mode == GEMM_SWIGLU && (wrows % 256 || !epi))) return false;
+  const int NT = M_max_rows <= 32 ? 32 : 64;            // rows per chunk (an expert's rows loop in chunks)
+  CUtensorMap mw, ma;
+  if (!get_map(W, n_experts * wrows, K, K, 128, &mw) || !get_map(A, a_rows, K, K, NT, &ma)) return false;
+  const int tiles = mode == GEMM_SWIGLU ? wrows / 256 : wrows / 128;
+  const GemmEpi e = epi ? *epi : GemmEpi{};
+  const int grid = n_experts * tiles;
+  auto go = [&](auto kern, int smem) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    const char* np_ = getenv("FOCUS_MOE_NOPDL");
+    const bool nopdl = np_ && (np_[0] == '3' || (np_[0] == '1' && mode == GEMM_SWIGLU) || (np_[0] == '2' && mode != GEMM_SWIGLU));
+    if (nopdl) kern<<<grid, swp::THREADS, smem, s>>>(mw, ma, C, ldc, K, off, wrows, tiles, e);
+    else launch_pdl(kern, dim3(grid), dim3(swp::THREADS), smem, s, mw, ma, C, ldc, K, off, wrows, tiles, e);
+  };
+  if (mode == GEMM_SWIGLU) {
+    if (NT == 32) go(k_gemm_grouped<GEMM_SWIGLU, 32>, swp::SL<32, true>::SMEM);
+    else go(k_gemm_grouped<GEMM_SWIGLU, 64>, swp::SL<64, true>::SMEM);
+  } else {
+    if (NT == 32) go(k_gemm_grouped<GEMM_STORE, 32>, swp::SL<32, false>::SMEM);
+    else go(k_gemm_grouped<GEMM_STORE, 64>, swp::SL<64, false>::SMEM);
+  }
+  return true;
 }
 
 int gemm_tc_choice(int N, int K, GemmMode mode, int M_max, int m_est, bool allow_swap) {

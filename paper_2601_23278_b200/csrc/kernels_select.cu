@@ -41,8 +41,10 @@ __global__ void __launch_bounds__(1024) k_select_plan(SelectArgs a) {
           const int n_parts = ((__popcll(P) + a.attn_rpc - 1) / a.attn_rpc) * a.n_kv_heads;
           const size_t base = (size_t)i * a.n_chunks * a.n_kv_heads;
           for (int p = 0; p < n_parts; ++p) {
-            i0 = __fadd_rn(i0, a.I0p[(base + p) * B + j]);
-            i1 = __fadd_rn(i1, a.I1p[(base + p) * B + j]);
+            // L2 loads: I0 was written several kernels back (layer-0 attention); under programmatic
+            // dependent launch only the immediate predecessor's writes are guaranteed through L1
+            i0 = __fadd_rn(i0, __ldcg(a.I0p + (base + p) * B + j));
+            i1 = __fadd_rn(i1, __ldcg(a.I1p + (base + p) * B + j));
           }
         }
         d[t] = __fsub_rn(i1, i0);

@@ -21,9 +21,11 @@ FOCUS_ERR_NOMEM, FOCUS_ERR_STATE, FOCUS_ERR_CUDA = 5, 6, 7
 
 DBG = dict(STATE=1, COUNTERS=2, ROWS_P=3, ROWS_S=4, ROWS_L=5, I0=6, I1=7, LOGITS=8, TOKCONF=9, KV_K=10, KV_V=11,
            TAP_X_IN=20, TAP_H=21, TAP_QKV=22, TAP_ATTN=23, TAP_X_MID=24, TAP_H2=25, TAP_ACT=26, TAP_X_OUT=27,
-           TAP_QS=28, HL=29, LAUNCHES=30, PROFILE=31, ATTN_TRACE=32)
+           TAP_QS=28, HL=29, LAUNCHES=30, PROFILE=31, ATTN_TRACE=32, MOE_SEL=33, MOE_WT=34,
+           MOE_ROWS=35, MOE_Y=36, MOE_AG=37)
 PROF_KINDS = ["setup", "embed", "rmsnorm", "gemm_qkv", "rope_store", "attention", "importance", "gemm_o",
-              "gemm_gu", "silu_mul", "gemm_down", "select", "gather", "gemm_lm", "vocab_reduce", "commit"]
+              "gemm_gu", "silu_mul", "gemm_down", "select", "gather", "gemm_lm", "vocab_reduce", "commit",
+              "moe_route", "moe_experts", "moe_combine"]
 
 EXPORTED = ["focus_required_bytes", "focus_init", "focus_destroy", "focus_kv_append", "focus_step_block",
             "focus_commit", "focus_sync", "focus_get_tokens", "focus_release", "focus_set_tap",
@@ -39,7 +41,9 @@ class focus_config(C.Structure):
                 ("placeholder_mode", C.c_int32), ("strategy", C.c_int32), ("fixed_k", C.c_int32),
                 ("max_requests", C.c_int32), ("max_seq_len", C.c_int32), ("page_size", C.c_int32),
                 ("max_prefill_chunk", C.c_int32), ("kv_pages", C.c_int64), ("weight_seed", C.c_uint64),
-                ("debug_taps", C.c_int32), ("logit_scale", C.c_float), ("batch_invariant", C.c_int32)]
+                ("debug_taps", C.c_int32), ("logit_scale", C.c_float), ("batch_invariant", C.c_int32),
+                ("n_experts", C.c_int32), ("top_k", C.c_int32), ("d_expert", C.c_int32),
+                ("n_shared_experts", C.c_int32), ("n_dense_layers", C.c_int32)]
 
 
 class focus_commit_result(C.Structure):
@@ -117,7 +121,9 @@ def make_config(run, max_requests: Optional[int] = None, max_seq_len: Optional[i
         placeholder_mode=me.placeholder_mode, strategy=me.strategy, fixed_k=me.fixed_k,
         max_requests=max_requests or run.n_requests, max_seq_len=max_seq_len, page_size=run.page_size,
         max_prefill_chunk=max_prefill_chunk, kv_pages=kv_pages, weight_seed=run.weight_seed,
-        debug_taps=1 if debug_taps else 0, logit_scale=m.logit_scale, batch_invariant=1 if batch_invariant else 0)
+        debug_taps=1 if debug_taps else 0, logit_scale=m.logit_scale, batch_invariant=1 if batch_invariant else 0,
+        n_experts=m.n_experts, top_k=m.top_k, d_expert=m.d_expert, n_shared_experts=m.n_shared_experts,
+        n_dense_layers=m.n_dense_layers)
 
 
 def focus_required_bytes(cfg: focus_config) -> int:

@@ -37,7 +37,8 @@ def test_exports_every_declared_symbol(lib):
 def test_struct_layouts_match_header():
     from paper_2601_23278_b200.focus import focus_commit_result, focus_config, focus_req_state
     # sizes computed from include/focus.h field lists (natural alignment)
-    assert C.sizeof(focus_config) == 22 * 4 + 8 + 8 + 3 * 4 + 4   # ... debug_taps, logit_scale, batch_invariant, pad
+    # 22 x 4-byte fields, kv_pages, weight_seed, debug_taps, logit_scale, batch_invariant, 5 MoE fields
+    assert C.sizeof(focus_config) == 22 * 4 + 8 + 8 + 3 * 4 + 5 * 4
     assert C.sizeof(focus_commit_result) == 5 * 4 + 64 * 4 * 2
     assert C.sizeof(focus_req_state) == 8 * 4 + 2 * 8 + 5 * 8 + 8 * 4 + 64 * 4 * 2
 
