@@ -214,6 +214,12 @@ class Rank:
         from paper_2601_23278_b200 import FocusContext, make_config
         self.run, self.gids, self.lens, self.dev = run, gids, lens, dev
         hi = max(lens.values()) if lens else run.prompt_len
+        # the KV page pool holds exactly this rank's requests (prompt + generation), not max_requests x
+        # max_seq_len: the mixed-length C4 batch (256 requests, prompts 256-4096) would otherwise reserve
+        # 183 GiB of pages for ~90 GiB of tokens
+        ps = run.page_size
+        pages = sum((lens[g] + run.gen_len + ps - 1) // ps for g in gids) if gids else 0
+        cfg_kw.setdefault("kv_pages", pages)
         self.ctx = FocusContext(make_config(run, max_requests=max(1, len(gids)), max_seq_len=hi + run.gen_len,
                                             **cfg_kw))
         self.rids = list(range(len(gids)))
@@ -422,7 +428,7 @@ def _agg_windows(win_lists, D, dev):
     return out
 
 
-def roofline_report(pd, pk):
+def roofline_report(pd, pk, workload):
     """Per kernel family: T_roof = max(FLOPs / tensor peak, bytes / HBM peak) against the CUDA-event
     time of its launches (SURVEY 8(d) reporting); the dominant kernel's object for the JSON line."""
     prof, fl, by, n = pd["prof"], pd["flops"], pd["bytes"], pd["steps"]
@@ -430,7 +436,7 @@ def roofline_report(pd, pk):
     traffic = {}
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
-        traffic = json.load(open(tp)).get("dram_bytes_per_launch", {})
+        traffic = json.load(open(tp)).get("workloads", {}).get(workload, {})   # ncu capture of THIS workload only
     kernels, troof_sum = {}, 0.0
     for k, v in prof.items():
         if not v["launches"]:
@@ -587,7 +593,7 @@ def run_focus(args):
     pk = peaks()
     roof = gemms = kernels = stepr = cub = None
     if g["prof"] is not None:
-        roof, gemms, kernels, stepr = roofline_report(g["prof"], pk)
+        roof, gemms, kernels, stepr = roofline_report(g["prof"], pk, run.name)
         if rank == 0 and not args.no_extras:
             cub = cublas_reference(run.model, g["prof"]["M_S"], dev)
             for k, v in cub.items():

@@ -1638,10 +1638,7 @@ bool launch_gemm_grouped(const bf16* A, int a_rows, const bf16* W, int n_experts
   const int grid = n_experts * tiles;
   auto go = [&](auto kern, int smem) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    const char* np_ = getenv("FOCUS_MOE_NOPDL");
-    const bool nopdl = np_ && (np_[0] == '3' || (np_[0] == '1' && mode == GEMM_SWIGLU) || (np_[0] == '2' && mode != GEMM_SWIGLU));
-    if (nopdl) kern<<<grid, swp::THREADS, smem, s>>>(mw, ma, C, ldc, K, off, wrows, tiles, e);
-    else launch_pdl(kern, dim3(grid), dim3(swp::THREADS), smem, s, mw, ma, C, ldc, K, off, wrows, tiles, e);
+    launch_pdl(kern, dim3(grid), dim3(swp::THREADS), smem, s, mw, ma, C, ldc, K, off, wrows, tiles, e);
   };
   if (mode == GEMM_SWIGLU) {
     if (NT == 32) go(k_gemm_grouped<GEMM_SWIGLU, 32>, swp::SL<32, true>::SMEM);
