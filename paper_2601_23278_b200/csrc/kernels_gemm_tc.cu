@@ -921,20 +921,26 @@ struct MapKeyHash {
 
 
 // ====================================================================================== swap-AB decode GEMM
-// Few live rows (M_max <= 128: the decode shapes of C2 / C5, ...): the weight rows go on the MMA M side
-// and the tokens on N ("swap-AB"),  acc^T[128 features x NT tokens] = W_tile[128 x K] . A^T,  so the
-// tensor core does no work on padding rows, and each CTA computes one 128-feature tile (SWIGLU: the
-// gate and the up tile of 128 features, two accumulators) over one of `split` contiguous K ranges:
-// every SM streams weights even when the GEMM has few feature tiles.  The split partials (fp32,
-// [token][feature]) are reduced by the tile's last-arriving CTA in K-range order (deterministic; the
-// split depends on N and K only), which then runs the mode's epilogue with thread = feature:
+// Few live rows (M_max <= 256, SWIGLU <= 64: the decode shapes of C2, ...): the weight rows go on the MMA M
+// side and the tokens on N ("swap-AB"),  acc^T[128 features x M tokens] = W_tile[128 x K] . A^T.  The MMA
+// N and the activation boxes follow the LIVE row count (32-row TMA boxes), so no tensor-core work or L2
+// traffic is spent on padding rows.  Each CTA computes one 128-feature tile (SWIGLU: the gate and the up
+// tile of the same 128 features, two accumulators) over one of CS contiguous K ranges, so every SM
+// streams weights even when the GEMM has few feature tiles.  The CS CTAs of a tile form a thread-block
+// cluster and reduce through distributed shared memory: after its last MMA each CTA parks its fp32
+// partial [acc][token][feature] in its own drained pipeline buffers; after a cluster barrier CTA r sums,
+// for its slice [r M / CS, (r + 1) M / CS) of the tokens, the CS partials in K-range order (deterministic:
+// CS depends on N, K and the SM count only, never on M) and runs the mode's epilogue, thread = feature:
 //   ADD       x[t][f] += acc (one writer per element; 32 consecutive features per warp store)
 //   STORE     logits C[t][f] (when C) and per (token, 64-feature group) vocab statistics (epi.vpart)
 //   SWIGLU    act[t][f] = bf16(silu(gate) * up)
 //   QKV_ROPE  tile = one q/k/v head: RoPE pairs (d, d+64) exchanged through shared memory, bf16 q|k|v
 //             rows and the paged KV store
+// so the reduction and the epilogue are spread over the cluster instead of trailing on one CTA.
 namespace swp {
 constexpr int THREADS = 256;
+constexpr int ABOX = 32;                                         // activation rows per TMA box
+// layout of the grouped expert GEMM (k_gemm_grouped)
 template <int NT, bool GU>
 struct SL {
   static constexpr int NW = GU ? 2 : 1;                          // weight tiles (accumulators) per CTA
@@ -947,28 +953,59 @@ struct SL {
   static constexpr int COLS = NW * NT;
   static constexpr int TCOLS = COLS <= 32 ? 32 : COLS <= 64 ? 64 : COLS <= 128 ? 128 : 256;
 };
+// layout of the cluster-reduced swap-AB GEMM (k_gemm_swap): NT = token capacity (>= M_max)
+template <int NT, bool GU>
+struct SC {
+  static constexpr int NW = GU ? 2 : 1;
+  static constexpr int W_BYTES = NW * 128 * BK * 2;
+  static constexpr int ACT_BYTES = NT * BK * 2;
+  static constexpr int STAGE = W_BYTES + ACT_BYTES;
+  static constexpr int STAGES = (180 * 1024) / STAGE > 8 ? 8 : (180 * 1024) / STAGE;
+  static constexpr int RED = NW * NT * 128 * 4;                  // parked partial, aliases the drained stages
+  // + the epilogue's chunk buffer [NW][32][128] fp32 (also in the drained stages)
+  static_assert(RED + NW * 32 * 128 * 4 <= STAGES * STAGE, "the partial fits the pipeline buffers");
+  static constexpr int XCH = 32 * 128 * 4;
+  static constexpr int RS = 128 * 33 * 4 + 32 * 8;               // QKV: RoPE rows [128][33] + 32 KV offsets
+  static constexpr int SMEM = STAGES * STAGE + XCH + RS + 1024 + 256;
+  static_assert(SMEM <= 227 * 1024, "shared memory");
+  static constexpr int COLS = NW * NT;
+  static constexpr int TCOLS = COLS <= 32 ? 32 : COLS <= 64 ? 64 : COLS <= 128 ? 128 : 256;
+};
 }  // namespace swp
 
 template <int MODE, int NT>
 __global__ void __launch_bounds__(swp::THREADS, 1)
     k_gemm_swap(const __grid_constant__ CUtensorMap mapW, const __grid_constant__ CUtensorMap mapA, float* __restrict__ C,
-                int ldc, int N, int K, const int* __restrict__ M_dev, int M_max, const GemmEpi epi, int split,
-                float* __restrict__ ws, int* __restrict__ cnt) {
+                int ldc, int N, int K, const int* __restrict__ M_dev, int M_max, const GemmEpi epi) {
   constexpr bool GU = MODE == GEMM_SWIGLU;
-  using L = swp::SL<NT, GU>;
+  using L = swp::SC<NT, GU>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  float* red = (float*)smem;                            // after the last MMA: this CTA's partial
   float* xch = (float*)(smem + L::STAGES * L::STAGE);
-  uint64_t* bars = (uint64_t*)(smem + L::STAGES * L::STAGE + L::XCH);
+  float* rs = (float*)(smem + L::STAGES * L::STAGE + L::XCH);     // QKV: RoPE rows [128][33] of a chunk
+  size_t* kvs = reinterpret_cast<size_t*>(rs + 128 * 33);         // QKV: KV element offsets of a chunk
+  uint64_t* bars = (uint64_t*)(smem + L::STAGES * L::STAGE + L::XCH + L::RS);
   uint64_t* full = bars;                                // [STAGES]
   uint64_t* empty = bars + L::STAGES;                   // [STAGES]
   uint64_t* tfull = bars + 2 * L::STAGES;               // [1]
   uint32_t* tmem_sh = (uint32_t*)(tfull + 1);
-  int* flag_sh = (int*)(tmem_sh + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tile = blockIdx.x / split, sp = blockIdx.x % split;
-  const int kbt = K / BK, kb0 = sp * kbt / split, kb1 = (sp + 1) * kbt / split;
+  const int CS = (int)cluster_nctarank();
+  const int rank = (int)cluster_ctarank();              // = K range
+  const int tile = blockIdx.x / CS;
+  const int kbt = K / BK, kb0 = rank * kbt / CS, kb1 = (rank + 1) * kbt / CS;
   const int wrow0 = tile * 128 * L::NW;                 // first weight row of the tile (SWIGLU: gate, then up)
+  // development trace (gemm_set_trace): global-timer stamps per CTA
+  long long* trace = g_gemm_trace ? g_gemm_trace + (size_t)blockIdx.x * 3 * kGemmTraceEv : nullptr;
+  auto stamp = [&](int e) {
+    if (trace) {
+      unsigned long long gt;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+      trace[e] = (long long)gt;
+    }
+  };
+  if (threadIdx.x == 0) stamp(0);
   pdl_trigger();
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < L::STAGES; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
@@ -982,33 +1019,44 @@ __global__ void __launch_bounds__(swp::THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_sh;
+  if (threadIdx.x == 0) stamp(1);
   if (warp == 0) {
     if (lane == 0) {
       // the weight tiles do not depend on earlier kernels: the first stages' weight loads are issued
-      // before the grid dependency wait (they overlap the previous kernel's tail); the activation tiles
-      // after it
+      // before the grid dependency wait (they overlap the previous kernel's tail); the NT activation rows
+      // after it (a fixed count: waiting for the live row count here would put a global load behind the
+      // weight stream, ~2 us)
       const uint64_t pol = l2_policy_evict_first();
       const int pre = min(kb1 - kb0, L::STAGES);
       for (int i = 0; i < pre; ++i) {
         uint8_t* st = smem + i * L::STAGE;
-        mbar_expect_tx(&full[i], L::STAGE);
+        mbar_expect_tx_only(&full[i], L::W_BYTES);
         tma_load_2d_hint(st, &mapW, &full[i], (kb0 + i) * BK, wrow0, pol);
         if (GU) tma_load_2d_hint(st + 128 * BK * 2, &mapW, &full[i], (kb0 + i) * BK, wrow0 + 128, pol);
       }
+      stamp(8);
       pdl_wait();
-      for (int i = 0; i < pre; ++i)
-        tma_load_2d(smem + i * L::STAGE + L::W_BYTES, &mapA, &full[i], (kb0 + i) * BK, 0);
+      stamp(9);
+      constexpr int nb = NT / swp::ABOX;
+      constexpr uint32_t a_bytes = (uint32_t)L::ACT_BYTES;
+      for (int i = 0; i < pre; ++i) {
+        uint8_t* sa = smem + i * L::STAGE + L::W_BYTES;
+        mbar_expect_tx(&full[i], a_bytes);
+        for (int b = 0; b < nb; ++b) tma_load_2d(sa + b * swp::ABOX * 128, &mapA, &full[i], (kb0 + i) * BK, b * swp::ABOX);
+      }
       int stage = pre % L::STAGES;
       uint32_t phase = pre == L::STAGES ? 1u : 0u;
       for (int kb = kb0 + pre; kb < kb1; ++kb) {
         mbar_wait(&empty[stage], phase ^ 1);
         uint8_t* st = smem + stage * L::STAGE;
-        mbar_expect_tx(&full[stage], L::STAGE);
+        mbar_expect_tx(&full[stage], L::W_BYTES + a_bytes);
         tma_load_2d_hint(st, &mapW, &full[stage], kb * BK, wrow0, pol);
         if (GU) tma_load_2d_hint(st + 128 * BK * 2, &mapW, &full[stage], kb * BK, wrow0 + 128, pol);
-        tma_load_2d(st + L::W_BYTES, &mapA, &full[stage], kb * BK, 0);
+        for (int b = 0; b < nb; ++b)
+          tma_load_2d(st + L::W_BYTES + b * swp::ABOX * 128, &mapA, &full[stage], kb * BK, b * swp::ABOX);
         if (++stage == L::STAGES) { stage = 0; phase ^= 1; }
       }
+      stamp(7);
     }
   } else if (warp == 1) {
     if (lane == 0) {
@@ -1030,181 +1078,247 @@ __global__ void __launch_bounds__(swp::THREADS, 1)
       }
       mma_commit(&tfull[0]);
     }
-  } else if (warp >= 4) {
+  }
+  // QKV: stage the RoPE rows (lane = token, rows r0 .. r0 + nr of ropeT, coalesced) and, with kv, the
+  // KV element offsets and committed-slot check of the 32-token chunk at t0 (one warp per call)
+  const bool qkv_v = MODE == GEMM_QKV_ROPE && tile >= epi.n_q_heads + epi.kv.n_kv_heads;
+  const bool qkv_kv = MODE == GEMM_QKV_ROPE && tile >= epi.n_q_heads;
+  auto stage_qkv = [&](int t0, int te, int r0, int nr, bool kv) {
+    const int t = min(t0 + lane, te - 1);
+    if (!qkv_v) {
+      float tmp[64];
+#pragma unroll
+      for (int i = 0; i < 64; ++i)
+        if (i < nr) tmp[i] = __ldcg(epi.ropeT + (size_t)(r0 + i) * epi.rope_ld + t);
+#pragma unroll
+      for (int i = 0; i < 64; ++i)
+        if (i < nr) rs[(r0 + i) * 33 + lane] = tmp[i];
+    }
+    if (kv && qkv_kv) {
+      const int kvh = tile - epi.n_q_heads - (qkv_v ? epi.kv.n_kv_heads : 0);
+      const RowInfo ri = epi.rows[t];
+      kvs[lane] = kv_offset(epi.kv, ri.slot, ri.pos, kvh);
+      if (t0 + lane < te && ri.j >= 0 && ((epi.st[ri.slot].committed >> ri.j) & 1ull))
+        atomicExch(&epi.cnt->invariant, 1);
+    }
+  };
+  if (MODE == GEMM_QKV_ROPE && (warp == 2 || warp == 3)) {
+    // idle during the main loop: stage the epilogue's first chunk (barrier 2 hands it over)
     pdl_wait();
-    const int f = threadIdx.x - 128, q = warp - 4;
-    const int M = M_dev ? min(*M_dev, M_max) : M_max;
-    const uint32_t tb = tmem + ((uint32_t)(q * 32) << 16);
+    const int Ms = M_dev ? min(__ldcg(M_dev), M_max) : M_max;
+    const int lo = rank * Ms / CS, hi = (rank + 1) * Ms / CS;
+    if (lo < hi) {
+      stage_qkv(lo, hi, (warp - 2) * 64, 64, warp == 2);
+      asm volatile("bar.arrive 2, 192;" ::: "memory");
+    }
+  }
+  const int f = threadIdx.x - 128, q = warp - 4;        // epilogue warps 4..7: thread = feature f of the tile
+  const uint32_t tb = tmem + ((uint32_t)(q * 32) << 16);
+  int M = 0, t_lo = 0, t_hi = 0;
+  if (warp >= 4) {
+    pdl_wait();
+    M = M_dev ? min(__ldcg(M_dev), M_max) : M_max;
+    t_lo = rank * M / CS;
+    t_hi = (rank + 1) * M / CS;
     mbar_wait(&tfull[0], 0);
     tc_fence_after();
-    const size_t slot = (size_t)L::NW * NT * 128;       // partial floats per CTA: [acc][token][feature]
-    bool mine = true;
-    if (split > 1) {
-      float* part = ws + (size_t)blockIdx.x * slot;
+    if (threadIdx.x == 128) stamp(2);
+    if (CS > 1) {                                       // park the partial (every MMA has drained the stages)
+      const int mp = (M + 31) & ~31;
 #pragma unroll 1
       for (int c = 0; c < L::NW * NT; c += 32) {
+        const int acc = c / NT, t0 = c % NT;
+        if (t0 >= mp) continue;
         float v[32];
         tmem_ld32(tb + c, v);
 #pragma unroll
-        for (int i = 0; i < 32; ++i) __stcg(part + (size_t)(c + i) * 128 + f, v[i]);
+        for (int i = 0; i < 32; ++i) red[(size_t)(acc * NT + t0 + i) * 128 + f] = v[i];
       }
-      __threadfence();
-      named_bar(1, 128);
-      if (f == 0) *flag_sh = atomicAdd(&cnt[tile], 1);
-      named_bar(1, 128);
-      mine = *flag_sh == split - 1;                     // the tile's last-arriving range reduces
-      if (mine) __threadfence();
-    }
-    if (mine) {
-      const float* base = ws + (size_t)tile * split * slot;
-      // 32 accumulator columns [c, c+32) of this thread's feature: TMEM, or the K-range partials summed
-      // in range order
-      auto get = [&](int c, float* v) {
-        if (split == 1) {
-          tmem_ld32(tb + c, v);
-        } else {
-          // partials of range 0 -> v, then range s2 + 1's loads are in flight while range s2's are added
-          float nx[32];
-          const float* p0 = base + (size_t)c * 128 + f;
-#pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = __ldcg(p0 + (size_t)i * 128);
-#pragma unroll
-          for (int i = 0; i < 32; ++i) nx[i] = __ldcg(p0 + slot + (size_t)i * 128);
-          for (int s2 = 1; s2 < split; ++s2) {
-            float cur[32];
-#pragma unroll
-            for (int i = 0; i < 32; ++i) cur[i] = nx[i];
-            if (s2 + 1 < split) {
-              const float* pn = p0 + (size_t)(s2 + 1) * slot;
-#pragma unroll
-              for (int i = 0; i < 32; ++i) nx[i] = __ldcg(pn + (size_t)i * 128);
-            }
-#pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] += cur[i];
-          }
-        }
-      };
-      const int feat = tile * 128 + f;                  // output feature (SWIGLU: act column)
-#pragma unroll 1
-      for (int t0 = 0; t0 < NT; t0 += 32) {
-        if (t0 >= M) break;                             // warp-uniform: M is the same for every thread
-        float v[32];
-        get(t0, v);
-        if constexpr (MODE == GEMM_ADD) {
-#pragma unroll
-          for (int i = 0; i < 32; ++i)
-            if (t0 + i < M)
-              asm volatile("red.global.add.f32 [%0], %1;" ::"l"(C + (size_t)(t0 + i) * ldc + feat), "f"(v[i]) : "memory");
-        } else if constexpr (MODE == GEMM_SWIGLU) {
-          float u[32];
-          get(NT + t0, u);
-#pragma unroll
-          for (int i = 0; i < 32; ++i)
-            if (t0 + i < M) {
-              const float a = __fdividef(v[i] * u[i], 1.0f + exp2f(-1.4426950408889634f * v[i]));
-              epi.out[(size_t)(t0 + i) * epi.ldo + feat] = __float2bfloat16_rn(a);
-            }
-        } else if constexpr (MODE == GEMM_STORE) {
-          if (C != nullptr) {
-#pragma unroll
-            for (int i = 0; i < 32; ++i)
-              if (t0 + i < M && feat < N) C[(size_t)(t0 + i) * ldc + feat] = v[i];
-          }
-          if (epi.vpart != nullptr) {
-            // per token: (max, sum exp(z - max), lowest argmax) over this warp's 32 features, then the
-            // two warps of each 64-feature group combined through shared memory
-            float* xm = xch;                             // [4 warps][32 tokens] max, sum, idx
-            const bool ok = feat < N && feat != epi.mask_id;
-#pragma unroll 1
-            for (int i = 0; i < 32; ++i) {
-              const float z = ok ? v[i] : -CUDART_INF_F;
-              float m = z;
-              for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-              const unsigned hit = __ballot_sync(0xffffffffu, z == m && m != -CUDART_INF_F);
-              float e = (m == -CUDART_INF_F || !ok) ? 0.f : __expf(z - m);
-              for (int o = 16; o; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
-              if (lane == 0) {
-                xm[(q * 32 + i) * 4 + 0] = m;
-                xm[(q * 32 + i) * 4 + 1] = e;
-                xm[(q * 32 + i) * 4 + 2] = __int_as_float(hit ? tile * 128 + q * 32 + __ffs(hit) - 1 : 0x7fffffff);
-              }
-            }
-            named_bar(1, 128);
-            if ((q & 1) == 0) {                          // warps 0 and 2: lane i = token t0 + i
-              const int i = lane, t = t0 + i;
-              const float* a = xm + (q * 32 + i) * 4;
-              const float* b = xm + ((q + 1) * 32 + i) * 4;
-              VocabPartial r;
-              const float ma = a[0], mb = b[0];
-              r.m = fmaxf(ma, mb);
-              if (r.m == -CUDART_INF_F) { r.s = 0.f; r.idx = 0x7fffffff; }
-              else {
-                r.s = (ma == -CUDART_INF_F ? 0.f : a[1] * __expf(ma - r.m)) + (mb == -CUDART_INF_F ? 0.f : b[1] * __expf(mb - r.m));
-                r.idx = ma >= mb ? __float_as_int(a[2]) : __float_as_int(b[2]);   // equal maxima: warp q's ids are lower
-              }
-              r.pad = 0;
-              const int g = (tile * 128 + q * 32) >> 6;
-              if (t < M && g < epi.vp_ld) epi.vpart[(size_t)t * epi.vp_ld + g] = r;
-            }
-            named_bar(1, 128);
-          }
-        } else {   // GEMM_QKV_ROPE: tile = head
-          const int head = tile;
-          const int hkv = epi.kv.n_kv_heads;
-          const bool is_v = head >= epi.n_q_heads + hkv;
-          const bool is_k = !is_v && head >= epi.n_q_heads;
-          const int kvh = head - epi.n_q_heads - (is_v ? hkv : 0);
-#pragma unroll
-          for (int i = 0; i < 32; ++i) xch[i * 128 + f] = v[i];
-          named_bar(1, 128);
-          const int kf = f & 63;
-          // the chunk's RoPE factors and KV slots are loaded up front (independent loads in flight)
-          float cc[32], sn[32];
-          if (!is_v) {
-#pragma unroll
-            for (int i = 0; i < 32; ++i) {
-              const int t = min(t0 + i, M - 1);
-              cc[i] = __ldg(epi.ropeT + (size_t)kf * epi.rope_ld + t);
-              sn[i] = __ldg(epi.ropeT + (size_t)(64 + kf) * epi.rope_ld + t);
-            }
-          }
-          size_t kvo[32];
-          if (is_k || is_v) {
-#pragma unroll
-            for (int i = 0; i < 32; ++i) {
-              const RowInfo ri = epi.rows[min(t0 + i, M - 1)];
-              kvo[i] = kv_offset(epi.kv, ri.slot, ri.pos, kvh);
-              if (f == i && t0 + i < M && ri.j >= 0 && ((epi.st[ri.slot].committed >> ri.j) & 1ull))
-                atomicExch(&epi.cnt->invariant, 1);
-            }
-          }
-#pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const int t = t0 + i;
-            if (t < M) {
-              float y = v[i];
-              if (!is_v) {
-                const float other = xch[i * 128 + (f ^ 64)];
-                y = f < 64 ? v[i] * cc[i] - other * sn[i] : v[i] * cc[i] + other * sn[i];
-              }
-              const __nv_bfloat16 b = __float2bfloat16_rn(y);
-              epi.out[(size_t)t * epi.ldo + head * 128 + f] = b;
-              if (is_k || is_v) (is_v ? epi.kv.V : epi.kv.K)[kvo[i] + f] = b;
-            }
-          }
-          named_bar(1, 128);                             // xch reuse by the next chunk
-        }
-      }
-      if (split > 1 && f == 0) cnt[tile] = 0;           // re-arm for the next launch (every range has arrived)
     }
   }
+  if (threadIdx.x == 128) stamp(3);
+  if (CS > 1) {                                         // every partial of the cluster is parked
+    __syncwarp();
+    cluster_sync();
+  }
+  if (threadIdx.x == 128) stamp(4);
+  if (warp >= 4) {
+    // Per 32-token chunk [t0, t0 + 32) of the slice: the CS parked partials are summed in K-range order
+    // by all 128 threads (thread = 4 features of every 4th token: 16-B DSMEM loads, all of one peer in
+    // flight at once) into this CTA's chunk buffer red2 [acc][32][128]; get() then hands thread f its
+    // 32 token values (CS = 1: straight from TMEM)
+    float* red2 = (float*)(smem + L::RED);
+    auto reduce_chunk = [&](int t0) {
+      named_bar(1, 128);                                // the previous chunk's readers of red2 are done
+      const int r = f >> 5, c4 = f & 31;
+      float4 acc4[L::NW][8];
+#pragma unroll
+      for (int a = 0; a < L::NW; ++a)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc4[a][j] = make_float4(0.f, 0.f, 0.f, 0.f);
+      const uint32_t mine = smem_u32(red + 4 * c4);
+      constexpr int PU = GU ? 2 : 4;                    // peers whose loads are in flight together
+#pragma unroll 1
+      for (int p0 = 0; p0 < CS; p0 += PU) {
+        float4 w[PU][L::NW][8];
+#pragma unroll
+        for (int pp = 0; pp < PU; ++pp) {
+          const uint32_t base = mapa_shared(mine, (uint32_t)min(p0 + pp, CS - 1));
+#pragma unroll
+          for (int a = 0; a < L::NW; ++a)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const int t = t0 + r + 4 * j;
+              w[pp][a][j] = (t < t_hi && p0 + pp < CS) ? ld_dsmem_f32x4(base + (uint32_t)((a * NT + t) * 128) * 4u)
+                                                       : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+        }
+#pragma unroll
+        for (int pp = 0; pp < PU; ++pp)                 // in K-range order
+#pragma unroll
+          for (int a = 0; a < L::NW; ++a)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              acc4[a][j].x += w[pp][a][j].x; acc4[a][j].y += w[pp][a][j].y;
+              acc4[a][j].z += w[pp][a][j].z; acc4[a][j].w += w[pp][a][j].w;
+            }
+      }
+#pragma unroll
+      for (int a = 0; a < L::NW; ++a)
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          *reinterpret_cast<float4*>(red2 + (size_t)(a * 32 + r + 4 * j) * 128 + 4 * c4) = acc4[a][j];
+      named_bar(1, 128);
+    };
+    auto get = [&](int acc, int t0, float* v) {
+      if (CS == 1) {
+        tmem_ld32(tb + acc * NT + t0, v);
+        return;
+      }
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = red2[(size_t)(acc * 32 + i) * 128 + f];
+    };
+    const int feat = tile * 128 + f;                    // output feature (SWIGLU: act column)
+    const int te = t_hi;
+#pragma unroll 1
+    for (int t0 = t_lo; t0 < te; t0 += 32) {            // warp-uniform bounds
+      float v[32];
+      if (CS > 1) reduce_chunk(t0);
+      if (threadIdx.x == 128 && t0 == t_lo) stamp(11);
+      get(0, t0, v);
+      if constexpr (MODE == GEMM_ADD) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (t0 + i < te)
+            asm volatile("red.global.add.f32 [%0], %1;" ::"l"(C + (size_t)(t0 + i) * ldc + feat), "f"(v[i]) : "memory");
+      } else if constexpr (MODE == GEMM_SWIGLU) {
+        float u[32];
+        get(1, t0, u);
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (t0 + i < te) {
+            const float a = __fdividef(v[i] * u[i], 1.0f + exp2f(-1.4426950408889634f * v[i]));
+            epi.out[(size_t)(t0 + i) * epi.ldo + feat] = __float2bfloat16_rn(a);
+          }
+      } else if constexpr (MODE == GEMM_STORE) {
+        if (C != nullptr) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (t0 + i < te && feat < N) C[(size_t)(t0 + i) * ldc + feat] = v[i];
+        }
+        if (epi.vpart != nullptr) {
+          // per token: (max, sum exp(z - max), lowest argmax) over this warp's 32 features, then the
+          // two warps of each 64-feature group combined through shared memory
+          float* xm = xch;                               // [4 warps][32 tokens] max, sum, idx
+          const bool ok = feat < N && feat != epi.mask_id;
+#pragma unroll 1
+          for (int i = 0; i < 32; ++i) {
+            const float z = ok ? v[i] : -CUDART_INF_F;
+            float m = z;
+            for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+            const unsigned hit = __ballot_sync(0xffffffffu, z == m && m != -CUDART_INF_F);
+            float e = (m == -CUDART_INF_F || !ok) ? 0.f : __expf(z - m);
+            for (int o = 16; o; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
+            if (lane == 0) {
+              xm[(q * 32 + i) * 4 + 0] = m;
+              xm[(q * 32 + i) * 4 + 1] = e;
+              xm[(q * 32 + i) * 4 + 2] = __int_as_float(hit ? tile * 128 + q * 32 + __ffs(hit) - 1 : 0x7fffffff);
+            }
+          }
+          named_bar(1, 128);
+          if ((q & 1) == 0) {                            // warps 0 and 2: lane i = token t0 + i
+            const int i = lane, t = t0 + i;
+            const float* a = xm + (q * 32 + i) * 4;
+            const float* b = xm + ((q + 1) * 32 + i) * 4;
+            VocabPartial r;
+            const float ma = a[0], mb = b[0];
+            r.m = fmaxf(ma, mb);
+            if (r.m == -CUDART_INF_F) { r.s = 0.f; r.idx = 0x7fffffff; }
+            else {
+              r.s = (ma == -CUDART_INF_F ? 0.f : a[1] * __expf(ma - r.m)) + (mb == -CUDART_INF_F ? 0.f : b[1] * __expf(mb - r.m));
+              r.idx = ma >= mb ? __float_as_int(a[2]) : __float_as_int(b[2]);   // equal maxima: warp q's ids are lower
+            }
+            r.pad = 0;
+            const int g = (tile * 128 + q * 32) >> 6;
+            if (t < te && g < epi.vp_ld) epi.vpart[(size_t)t * epi.vp_ld + g] = r;
+          }
+          named_bar(1, 128);
+        }
+      } else {   // GEMM_QKV_ROPE: tile = head
+        const int head = tile;
+        const int hkv = epi.kv.n_kv_heads;
+        const bool is_v = head >= epi.n_q_heads + hkv;
+        const bool is_k = !is_v && head >= epi.n_q_heads;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) xch[i * 128 + f] = v[i];
+        named_bar(1, 128);
+        const int kf = f & 63;
+        // the chunk's RoPE rows and KV offsets: the first chunk was staged by warps 2-3 during the main
+        // loop (barrier 2), later chunks are staged here (32 rows per warp)
+        if (t0 == t_lo) {
+          named_bar(2, 192);
+        } else {
+          stage_qkv(t0, te, q * 32, 32, q == 0);
+          named_bar(1, 128);
+        }
+        float cc[32], sn[32];
+        if (!is_v) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            cc[i] = rs[kf * 33 + i];
+            sn[i] = rs[(64 + kf) * 33 + i];
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const int t = t0 + i;
+          if (t < te) {
+            float y = v[i];
+            if (!is_v) {
+              const float other = xch[i * 128 + (f ^ 64)];
+              y = f < 64 ? v[i] * cc[i] - other * sn[i] : v[i] * cc[i] + other * sn[i];
+            }
+            const __nv_bfloat16 b = __float2bfloat16_rn(y);
+            epi.out[(size_t)t * epi.ldo + head * 128 + f] = b;
+            if (is_k || is_v) (is_v ? epi.kv.V : epi.kv.K)[kvs[i] + f] = b;
+          }
+        }
+        named_bar(1, 128);                               // xch reuse by the next chunk
+      }
+    }
+  }
+  if (threadIdx.x == 128) stamp(5);
+  if (CS > 1) {                                         // the peers have read this CTA's partial
+    __syncwarp();
+    cluster_sync();
+  }
+  if (threadIdx.x == 128) stamp(6);
   __syncthreads();
   if (warp == 2) {
     tc_fence_after();
     tmem_free<L::TCOLS>(tmem);
   }
 }
-
 
 // Grouped swap-AB GEMM over experts (MoE FFN, readings A-M5/A-M6): expert e owns the rows
 // [off[e], off[e+1]) of the gathered activations A (the tokens routed to e, in row order) and the
@@ -1529,17 +1643,29 @@ static bool launch_pair(const bf16* A, int lda, int a_rows, const bf16* W, int N
 // eager sequence would launch the same kernels.
 enum { GC_SPLIT = 1, GC_128x2, GC_256x2, GC_128x1, GC_256x1, GC_SINGLE_128, GC_SINGLE_256, GC_SWAP };
 
-// swap-AB decode GEMM (see k_gemm_swap): applicable for M_max <= 128 live rows and 128-aligned feature
-// tiles; opt-in (FOCUS_GEMM_SWAP=1).  Measured at C2 (M <= 64, B200): down projection 0.93 -> 0.68 ms per
-// step, O equal, QKV 0.58 -> 1.13, gate-up 0.67 -> 0.76, LM head 0.14 -> 0.28: the split-K reduction by
-// one CTA and the per-token RoPE-table loads of the epilogue cost more than the idle SMs of the
-// CTA-pair kernel.  The split into K ranges depends on N and K only.
-static bool swap_enabled() {   // read per call (the tests switch it per context)
+// swap-AB decode GEMM (see k_gemm_swap): M_max <= 256 (SWIGLU: 64) live rows, 128-aligned feature tiles,
+// and few enough tiles that a cluster of >= 2 K ranges per tile fits one wave (the LM head's ~1 200
+// tiles stay on the CTA-pair kernel).  Default on (FOCUS_GEMM_SWAP=0: off; read per call, the tests
+// switch it per context).  The cluster size depends on N, K and the SM count only.
+static bool swap_enabled() {
   const char* e = getenv("FOCUS_GEMM_SWAP");
-  return e && e[0] == '1';
+  return !(e && e[0] == '0');
+}
+static int swap_nt(int M_max) { return M_max <= 32 ? 32 : M_max <= 64 ? 64 : M_max <= 128 ? 128 : 256; }
+// K ranges per tile: as many as fill the SMs with one CTA each, >= 2 k-blocks per range, <= 16 (the
+// non-portable cluster limit)
+static int swap_cs(int tiles, int kbt) {
+  static int cap = -1;
+  if (cap < 0) {   // FOCUS_GEMM_SWAP_CS: cap on the cluster size (development: 1 = no K split)
+    const char* e = getenv("FOCUS_GEMM_SWAP_CS");
+    cap = e ? std::max(1, std::min(16, atoi(e))) : 16;
+  }
+  return std::max(1, std::min(std::min(cap, kbt / 2), num_sms() / std::max(1, tiles)));
 }
 static bool swap_shape_ok(int N, int K, GemmMode mode, int M_max) {
-  return swap_enabled() && M_max >= 1 && M_max <= 128 && K % tc::BK == 0 && N % (mode == GEMM_SWIGLU ? 256 : 128) == 0;
+  const int nw = mode == GEMM_SWIGLU ? 2 : 1;
+  if (!swap_enabled() || M_max < 1 || M_max > (nw == 2 ? 64 : 256) || K % tc::BK || N % (128 * nw)) return false;
+  return N / (128 * nw) <= num_sms() / 2;
 }
 static bool swap_applies(int N, int K, GemmMode mode, int M_max, const GemmEpi* epi) {
   if (!swap_shape_ok(N, K, mode, M_max)) return false;
@@ -1549,51 +1675,80 @@ static bool swap_applies(int N, int K, GemmMode mode, int M_max, const GemmEpi* 
 }
 
 template <int MODE, int NT>
-static void launch_swap_k(int grid, cudaStream_t s, const CUtensorMap& mw, const CUtensorMap& ma, float* C, int ldc,
-                          int N, int K, const int* M_dev, int M_max, const GemmEpi& e, int split, const GemmWs& ws) {
+static void launch_swap_k(int tiles, int cs, cudaStream_t s, const CUtensorMap& mw, const CUtensorMap& ma, float* C,
+                          int ldc, int N, int K, const int* M_dev, int M_max, const GemmEpi& e) {
   using namespace tc;
-  constexpr int SMEM = swp::SL<NT, MODE == GEMM_SWIGLU>::SMEM;
+  constexpr int SMEM = swp::SC<NT, MODE == GEMM_SWIGLU>::SMEM;
+  auto kern = k_gemm_swap<MODE, NT>;
   static bool attr = false;
+  static int fits[17];                                  // largest co-resident cluster count per size (0: unknown)
   if (!attr) {
-    cudaFuncSetAttribute(k_gemm_swap<MODE, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     attr = true;
   }
-  launch_pdl(k_gemm_swap<MODE, NT>, dim3(grid), dim3(swp::THREADS), SMEM, s, mw, ma, C, ldc, N, K, M_dev, M_max, e,
-             split, ws.ptr, ws.sem + kSwapSemBase);
+  cudaLaunchConfig_t cfg{};
+  cfg.blockDim = dim3(swp::THREADS);
+  cfg.dynamicSmemBytes = SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  // the largest cluster size <= cs whose `tiles` clusters are co-resident (clusters live inside one GPC)
+  for (; cs > 1; --cs) {
+    if (fits[cs] == 0) {
+      at[0].val.clusterDim.x = cs;
+      cfg.gridDim = dim3(tiles * cs);
+      cfg.numAttrs = 1;
+      int n = 0;
+      if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess) {
+        (void)cudaGetLastError();
+        n = -1;                                         // unknown: trust the SM count
+      }
+      fits[cs] = n == 0 ? -2 : n;
+    }
+    if (fits[cs] == -1 || fits[cs] >= tiles) break;
+  }
+  at[0].val.clusterDim.x = cs;
+  cfg.gridDim = dim3(tiles * cs);
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  cudaLaunchKernelEx(&cfg, kern, mw, ma, C, ldc, N, K, M_dev, M_max, e);
 }
 
 template <int NT>
 static bool launch_swap_nt(const bf16* A, int lda, int a_rows, const bf16* W, int N, int K, float* C, int ldc,
-                           const int* M_dev, int M_max, GemmMode mode, const GemmWs& ws, cudaStream_t s,
-                           const GemmEpi* epi) {
+                           const int* M_dev, int M_max, GemmMode mode, cudaStream_t s, const GemmEpi* epi) {
   using namespace tc;
   CUtensorMap mw, ma;
-  if (!get_map(W, N, K, K, 128, &mw) || !get_map(A, a_rows, K, lda, NT, &ma)) return false;
+  if (!get_map(W, N, K, K, 128, &mw) || !get_map(A, a_rows, K, lda, swp::ABOX, &ma)) return false;
   const int nw = mode == GEMM_SWIGLU ? 2 : 1;
   const int tiles = N / (128 * nw);
-  const int kbt = K / BK;
-  // K ranges of >= 4 k-blocks so that about one CTA per SM streams weights
-  int split = std::max(1, std::min(std::min(16, kbt / 4), num_sms() / std::max(1, tiles)));
-  const size_t slot = (size_t)nw * NT * 128 * sizeof(float);
-  if (split > 1 && ((size_t)tiles * split * slot > ws.bytes || ws.sem_count < (size_t)kSwapSemBase + tiles)) split = 1;
+  const int cs = swap_cs(tiles, K / BK);
   const GemmEpi e = epi ? *epi : GemmEpi{};
-  const int grid = tiles * split;
   switch (mode) {
-    case GEMM_ADD: launch_swap_k<GEMM_ADD, NT>(grid, s, mw, ma, C, ldc, N, K, M_dev, M_max, e, split, ws); break;
-    case GEMM_SWIGLU: launch_swap_k<GEMM_SWIGLU, NT>(grid, s, mw, ma, C, ldc, N, K, M_dev, M_max, e, split, ws); break;
-    case GEMM_QKV_ROPE: launch_swap_k<GEMM_QKV_ROPE, NT>(grid, s, mw, ma, C, ldc, N, K, M_dev, M_max, e, split, ws); break;
-    default: launch_swap_k<GEMM_STORE, NT>(grid, s, mw, ma, C, ldc, N, K, M_dev, M_max, e, split, ws);
+    case GEMM_ADD: launch_swap_k<GEMM_ADD, NT>(tiles, cs, s, mw, ma, C, ldc, N, K, M_dev, M_max, e); break;
+    case GEMM_SWIGLU:
+      if constexpr (NT <= 64) launch_swap_k<GEMM_SWIGLU, NT>(tiles, cs, s, mw, ma, C, ldc, N, K, M_dev, M_max, e);
+      break;
+    case GEMM_QKV_ROPE: launch_swap_k<GEMM_QKV_ROPE, NT>(tiles, cs, s, mw, ma, C, ldc, N, K, M_dev, M_max, e); break;
+    default: launch_swap_k<GEMM_STORE, NT>(tiles, cs, s, mw, ma, C, ldc, N, K, M_dev, M_max, e);
   }
   return true;
 }
 
 static bool launch_gemm_swap(const bf16* A, int lda, int a_rows, const bf16* W, int N, int K, float* C, int ldc,
-                             const int* M_dev, int M_max, GemmMode mode, const GemmWs& ws, cudaStream_t s,
+                             const int* M_dev, int M_max, GemmMode mode, const GemmWs&, cudaStream_t s,
                              const GemmEpi* epi) {
-  if (a_rows < (M_max <= 32 ? 32 : M_max <= 64 ? 64 : 128)) return false;   // the A box reads NT rows
-  if (M_max <= 32) return launch_swap_nt<32>(A, lda, a_rows, W, N, K, C, ldc, M_dev, M_max, mode, ws, s, epi);
-  if (M_max <= 64) return launch_swap_nt<64>(A, lda, a_rows, W, N, K, C, ldc, M_dev, M_max, mode, ws, s, epi);
-  return launch_swap_nt<128>(A, lda, a_rows, W, N, K, C, ldc, M_dev, M_max, mode, ws, s, epi);
+  switch (swap_nt(M_max)) {
+    case 32: return launch_swap_nt<32>(A, lda, a_rows, W, N, K, C, ldc, M_dev, M_max, mode, s, epi);
+    case 64: return launch_swap_nt<64>(A, lda, a_rows, W, N, K, C, ldc, M_dev, M_max, mode, s, epi);
+    case 128: return launch_swap_nt<128>(A, lda, a_rows, W, N, K, C, ldc, M_dev, M_max, mode, s, epi);
+    default: return launch_swap_nt<256>(A, lda, a_rows, W, N, K, C, ldc, M_dev, M_max, mode, s, epi);
+  }
 }
 static int split_parts(int K) {
   // ordered split into S k-ranges (at least 8 k-blocks each, S units in one wave): two ranges for deep

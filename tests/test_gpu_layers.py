@@ -216,9 +216,19 @@ def test_layer_stages_unplanned_attention(monkeypatch):
 
 
 def test_layer_stages_swap_ab_gemm(monkeypatch):
-    """Stage-wise parity with the opt-in swap-AB split-K decode GEMM (M <= 128 live rows: weights on
-    the MMA M side, K ranges reduced in order by the tile's last CTA) for every projection and the LM
-    head (vocab statistics), at the 8B and 1.7B layer shapes."""
+    """Stage-wise parity with the swap-AB decode GEMM (default for M_max <= 256 live rows: weights on
+    the MMA M side, K ranges of a tile in one thread-block cluster, reduced in order through distributed
+    shared memory) for every projection, at the 8B and 1.7B layer shapes, including a ragged live row
+    count that is not a multiple of the 32-row activation box."""
     monkeypatch.setenv("FOCUS_GEMM_SWAP", "1")
+    test_layer_stages(M8B4, 16, 3, 100, (0, 1, 3), 64)
+    test_layer_stages(M1P7B3, 4, 5, 70, (0, 1, 2), 64)
+    test_layer_stages(M1P7B3, 4, 13, 70, (0, 2), 64)
+
+
+def test_layer_stages_pair_gemm_small_m(monkeypatch):
+    """The same small-M stages on the CTA-pair GEMM (FOCUS_GEMM_SWAP=0), which the swap-AB kernel
+    replaces by default at these row counts."""
+    monkeypatch.setenv("FOCUS_GEMM_SWAP", "0")
     test_layer_stages(M8B4, 16, 3, 100, (0, 1, 3), 64)
     test_layer_stages(M1P7B3, 4, 5, 70, (0, 1, 2), 64)

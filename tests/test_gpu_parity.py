@@ -328,10 +328,11 @@ def test_sharding_invariance_batch_invariant(model):
     assert outs[1] == outs[2] == outs[4]
 
 
-def test_resynced_swap_ab_gemm(monkeypatch):
-    """The whole step with the opt-in swap-AB decode GEMM (48 rows): rules bit-exact in the resynced
-    protocol, including the threshold regime."""
-    monkeypatch.setenv("FOCUS_GEMM_SWAP", "1")
+@pytest.mark.parametrize("swap", ["1", "0"], ids=["swap_ab", "cta_pair"])
+def test_resynced_swap_ab_gemm(monkeypatch, swap):
+    """The whole step with the swap-AB decode GEMM (48 rows; the default at this row count) and with
+    the CTA-pair GEMM: rules bit-exact in the resynced protocol, including the threshold regime."""
+    monkeypatch.setenv("FOCUS_GEMM_SWAP", swap)
     mdl = dataclasses.replace(GQA_TC, logit_scale=16.0)
     run = get_config("C1").with_(model=mdl, method=MethodConfig(block_size=8), n_requests=6, prompt_len=13,
                                  gen_len=16, page_size=16)
