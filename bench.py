@@ -471,7 +471,9 @@ def roofline_report(pd, pk, workload):
     names = {"attention": "k_attn_tc (block-diffusion paged attention, tcgen05) per layer"}
     roof.update(kernel=names.get(dom, f"k_gemm_pair ({dom}) per layer"), traffic=traffic.get(dom),
                 launch_ms=round(ms_l, 4), launches_per_step=n_l // n, share_of_step=e["share"],
-                timing="CUDA events around every launch on the library stream, 2 profiled steps after the middle window")
+                timing="CUDA events around every launch on the library stream, 2 profiled (eager) steps after the middle "
+                       "window, each held on the device until the host has enqueued it (k_hold), so the intervals "
+                       "are device time, not host launch latency")
     proj = [k for k in ("gemm_qkv", "gemm_o", "gemm_gu", "gemm_down", "moe_experts") if prof.get(k, {}).get("launches")]
     g_ms = sum(prof[k]["total_ms"] for k in proj)
     g_fl = sum(fl[k] for k in proj)

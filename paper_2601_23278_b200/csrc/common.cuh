@@ -101,6 +101,7 @@ void launch_init_weights(bf16* dst, int rows, int cols, uint64_t tid, uint64_t s
 
 void launch_step_setup(const int* req_list, int n_req, focus_req_state* st, int B, RowInfo* rowP,
                        int* offP, int* tokP, Counters* cnt, cudaStream_t s);
+void launch_hold(long long ns, cudaStream_t s);
 void launch_embed(const int* tok, const int* M_dev, int M_max, const bf16* E, int d, float* x,
                   cudaStream_t s);
 void launch_rmsnorm(const float* x, const int* src_map, const int* M_dev, int M_max, int d, float eps,

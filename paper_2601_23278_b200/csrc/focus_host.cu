@@ -904,6 +904,11 @@ focus_status focus_step_block(focus_ctx* x, const int32_t* ids, int32_t n_req) {
     x->est = e;
   }
   focus_status st = FOCUS_OK;
+  if (x->prof_on) {   // profiled (eager) step: the device starts it only once the host has enqueued it
+    static long long hold_us = -1;
+    if (hold_us < 0) hold_us = getenv("FOCUS_PROF_HOLD_US") ? std::max(0, atoi(getenv("FOCUS_PROF_HOLD_US"))) : 30000;
+    if (hold_us > 0) launch_hold(hold_us * 1000, x->stream);
+  }
   if (!graphs_enabled(x)) st = enqueue_step(x, ids, n_req);
   else st = step_graph(x, ids, n_req, same_list);
   if (st != FOCUS_OK) return st;

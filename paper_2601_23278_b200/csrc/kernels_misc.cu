@@ -33,6 +33,19 @@ void launch_init_weights(bf16* dst, int rows, int cols, uint64_t tid, uint64_t s
 // Per request (Alg.1 input; App.E state P:797-821): P = uncommitted, M = masked & P; t += 1;
 // exclusive scan of |P| over the call's request list -> P-row offsets; row maps in
 // (list order, j ascending) (SURVEY c.4 COMPACT rule applied to P).  One CTA.
+// Profiling only: hold the stream for `ns` of device time so the host enqueues the whole profiled step
+// (launches and their timing events) before the device reaches it -- the per-launch event intervals then
+// measure device time, not the host's eager launch latency.
+__global__ void k_hold(long long ns) {
+  unsigned long long t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  do {
+    __nanosleep(1000);
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  } while ((long long)(t - t0) < ns);
+}
+void launch_hold(long long ns, cudaStream_t s) { k_hold<<<1, 1, 0, s>>>(ns); }
+
 __global__ void __launch_bounds__(1024) k_step_setup(const int* __restrict__ req_list, int n_req,
                                                      focus_req_state* __restrict__ st, int B,
                                                      RowInfo* __restrict__ rowP, int* __restrict__ offP,
