@@ -224,6 +224,9 @@ def test_layer_stages_swap_ab_gemm(monkeypatch):
     test_layer_stages(M8B4, 16, 3, 100, (0, 1, 3), 64)
     test_layer_stages(M1P7B3, 4, 5, 70, (0, 1, 2), 64)
     test_layer_stages(M1P7B3, 4, 13, 70, (0, 2), 64)
+    # 128- and 256-token capacities (M_max 80, 192; gate-up stays on the CTA-pair kernel above 64 rows)
+    test_layer_stages(M8B4, 16, 5, 100, (0, 2), 64)
+    test_layer_stages(M8B4, 16, 12, 60, (0, 2), 64)
 
 
 def test_layer_stages_pair_gemm_small_m(monkeypatch):
