@@ -24,15 +24,19 @@
 // Persistent CTA (one per SM), 384 threads, warp-specialised:
 //   warp 0 / 2  TMA producers: K tiles / V tiles (128 keys x 128, 128-B swizzle), 2-slot rings each
 //               (K is freed when QK^T completes, V when PV completes)
-//   warp 1      MMA issuer (one thread): S^T into a double-buffered TMEM tile, O^T += V^T P^T into a
-//               double-buffered TMEM accumulator (one per unit in flight)
-//   warp 3      TMEM allocator + Q loader (one 3-D TMA box per 64-column half: rows n = r*G + g)
+//   warp 1      QK^T issuer (one thread) + Q loader (one 3-D TMA box per 64-column half: rows n = r*G + g):
+//               S^T into one of three TMEM tiles
+//   warp 3      TMEM allocator + PV^T issuer (one thread): O^T += V^T P^T into a double-buffered TMEM
+//               accumulator (one per unit in flight) and the row sums L^T += ONES P^T.  Two issuing threads,
+//               so a QK^T never waits behind a PV^T's dependencies (FOCUS_ATTN_SPLIT_ISSUE=0: one thread,
+//               warp 3 then loads Q)
 //   warps 4-7   softmax, thread = key: online softmax in the log2 domain with a lazy running max
 //               (the max only moves when a score exceeds it by > 2^8; then a cross-warp max, O^T
 //               column rescale and sum rescale), P^T -> double-buffered smem as bf16; block-column
 //               scores -> per-CTA scratch and the Eq.2 epilogue
 //   warps 8-11  epilogue, thread = d_h lane of O^T: O/l -> bf16 rows (or split partials + merge)
 #include <math_constants.h>
+#include <cstdio>
 
 #include "tc_ptx.cuh"
 
@@ -57,6 +61,7 @@ constexpr int HALF_KV = KT * 128;               // 16 KB: one 64-column half of 
 constexpr int KV_BYTES = 2 * HALF_KV;           // 32 KB
 constexpr int P_CHUNK = (KT / 8) * 128;         // 2 KB: 8 query rows x 128 keys of P^T
 constexpr int P_BYTES = (NQM / 8) * P_CHUNK;    // 16 KB
+constexpr int NPB = 2;                          // P^T buffers (measured: one buffer stalls the softmax on PV(g-1))
 constexpr int TMEM_COLS = 512;
 constexpr int O_COL = 0;                        // O^T buffers [0, 64), [64, 128)
 constexpr int NSB = 3;                          // S^T buffers: QK^T runs up to NSB tiles ahead of PV
@@ -67,8 +72,8 @@ constexpr int OFF_Q = 0;
 constexpr int OFF_K = OFF_Q + 2 * Q_BYTES;
 constexpr int OFF_V = OFF_K + SK * KV_BYTES;
 constexpr int OFF_P = OFF_V + SV * KV_BYTES;
-constexpr int OFF_BAR = OFF_P + 2 * P_BYTES;
-constexpr int N_BARS = 2 * SK + 2 * SV + 2 * 9 + 2 * (NSB - 2);
+constexpr int OFF_BAR = OFF_P + NPB * P_BYTES;
+constexpr int N_BARS = 2 * SK + 2 * SV + 4 + 2 * NSB + 2 * NPB + 6;
 constexpr int OFF_MISC = OFF_BAR + 8 * N_BARS + 16;
 constexpr int OFF_M = OFF_MISC;                 // float [NQM] running max (log2 units)
 constexpr int OFF_ALPHA = OFF_M + NQM * 4;      // float [NQM]
@@ -222,7 +227,7 @@ __device__ __forceinline__ void softmax_unit(const AttnArgs& a, const Unit& xr, 
   }
   named_bar(1, 128);
   for (int t = xr.t_lo; t < xr.t_hi; ++t, ++g) {
-    const uint32_t sb = g % NSB, pb = g & 1;
+    const uint32_t sb = g % NSB, pb = g % NPB;
     mbar_wait(&ss.sfull[sb], (g / NSB) & 1);
     tr.ev(1);
     tc_fence_after();
@@ -233,6 +238,7 @@ __device__ __forceinline__ void softmax_unit(const AttnArgs& a, const Unit& xr, 
 #pragma unroll
     for (int c = 0; c < NCH; ++c) tmem_ld32x16(sbase + 16 * c, r[c]);
     tmem_wait_ld();
+    tr.ev(6);
     tc_fence_before();                             // S^T is in registers: the tile may be overwritten
     __syncwarp();
     if (lane == 0) mbar_arrive(&ss.sfree[sb]);
@@ -261,11 +267,14 @@ __device__ __forceinline__ void softmax_unit(const AttnArgs& a, const Unit& xr, 
           if (16 * c + e < nq) th.scr[(16 * c + e) * kMaxB + (k - xr.s0)] = __uint_as_float(r[c][e]) * a.scale;
     }
     if (IMP_ONLY) continue;
+    tr.ev(7);
     const int anyw = __any_sync(0xffffffffu, need);
     if (lane == 0) ss.flags[(g & 1) * 4 + th.q4] = anyw;
     named_bar(1, 128);
+    tr.ev(8);
     const int* fl = ss.flags + (g & 1) * 4;
     if (fl[0] | fl[1] | fl[2] | fl[3]) {
+      tr.ev(9);
       // ---- slow path: exact tile max per row (transposed butterfly + 4-warp combine)
 #pragma unroll
       for (int rd = 0; rd < (NCH + 1) / 2; ++rd) {
@@ -300,7 +309,8 @@ __device__ __forceinline__ void softmax_unit(const AttnArgs& a, const Unit& xr, 
       }
       named_bar(1, 128);
       if (t > xr.t_lo) {                           // O^T and L^T columns *= alpha (PV of tile g-1 done)
-        mbar_wait(&ss.pvdone[(g - 1) & 1], ((g - 1) >> 1) & 1);
+        mbar_wait(&ss.pvdone[(g - 1) % NPB], ((g - 1) / NPB) & 1);
+        tr.ev(10);
         tc_fence_after();
 #pragma unroll
         for (int buf = 0; buf < 2; ++buf) {
@@ -320,7 +330,7 @@ __device__ __forceinline__ void softmax_unit(const AttnArgs& a, const Unit& xr, 
     }
     // ---- (2) P^T = exp2(s * scale*log2e - m) as bf16 into the MN-major P^T buffer
     tr.ev(2);
-    if (g >= 2) mbar_wait(&ss.pvdone[pb], ((g >> 1) & 1) ^ 1);   // PV of tile g-2 done: buffer free
+    if (g >= NPB) mbar_wait(&ss.pvdone[pb], ((g / NPB) & 1) ^ 1);   // PV of tile g-NPB done: buffer free
     tr.ev(3);
     const uint32_t pdst = smem_u32(ss.sP + pb * P_BYTES) + (L >> 3) * 128 + (L & 7) * 16;
     if (kvalid) {
@@ -628,9 +638,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   uint64_t* qempty = qfull + 2;            // [2]
   uint64_t* sfull = qempty + 2;            // [NSB]
   uint64_t* sfree = sfull + NSB;           // [NSB]  (4 softmax warps)
-  uint64_t* pfull = sfree + NSB;           // [2]  (4 softmax warps)
-  uint64_t* pvdone = pfull + 2;            // [2]
-  uint64_t* ofull = pvdone + 2;            // [2]
+  uint64_t* pfull = sfree + NSB;           // [NPB]  (4 softmax warps)
+  uint64_t* pvdone = pfull + NPB;          // [NPB]
+  uint64_t* ofull = pvdone + NPB;          // [2]
   uint64_t* ofree = ofull + 2;             // [2]  (4 epilogue warps)
   uint64_t* statfull = ofree + 2;          // [2]  (4 softmax warps)
   uint32_t* tmem_sh = (uint32_t*)(bars + N_BARS);
@@ -646,7 +656,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   ss.sfull = sfull; ss.sfree = sfree; ss.pfull = pfull; ss.pvdone = pvdone; ss.ofree = ofree; ss.statfull = statfull;
   uint16_t* ones = (uint16_t*)(smem + OFF_ONES);
   Unit* utab = (Unit*)(smem + OFF_UTAB);
-  int* pre = (int*)sP;                     // setup only (aliases the P^T buffers)
+  int* pre = (int*)sQ;                     // setup only (aliases the Q buffers: 17 KB of scan scratch)
   int* nsp = pre + 1028;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -670,9 +680,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     for (int i = 0; i < SK; ++i) { mbar_init(&kfull[i], 1); mbar_init(&kempty[i], 1); }
     for (int i = 0; i < SV; ++i) { mbar_init(&vfull[i], 1); mbar_init(&vempty[i], 1); }
     for (int i = 0; i < NSB; ++i) { mbar_init(&sfull[i], 1); mbar_init(&sfree[i], 4); }
+    for (int i = 0; i < NPB; ++i) { mbar_init(&pfull[i], 4); mbar_init(&pvdone[i], 1); }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&qfull[i], 1); mbar_init(&qempty[i], 1);
-      mbar_init(&pfull[i], 4); mbar_init(&pvdone[i], 1);
       mbar_init(&ofull[i], 1); mbar_init(&ofree[i], 4);
       mbar_init(&statfull[i], 4);
     }
@@ -730,6 +740,21 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     n_my = build_units(a, blockIdx.x, gridDim.x, pre, utab);
   }
   __syncthreads();
+  if (a.debug_check && threadIdx.x == 0 && a.ext_mode != 2) {
+    const int rows = a.row_off[a.n_req];
+    for (int k = 0; k < n_my; ++k) {
+      const Unit& x = utab[k];
+      const bool bad = x.i < 0 || x.i >= a.n_req || x.kvh < 0 || x.kvh >= H || x.nq <= 0 || x.nq > NQM ||
+                       x.sp < 0 || x.sp >= x.nsplit || x.nsplit > a.max_nsplit || x.nsplit > MAXS || x.t_lo >= x.t_hi ||
+                       x.pair < 0 || x.pair >= a.n_req * a.n_chunks * H || x.r0 < 0 || x.r0 + x.nr > rows ||
+                       x.t_lo < x.kbeg / KT || x.t_hi > (x.kend + KT - 1) / KT;
+      if (bad) {
+        printf("attn unit check: cta %d unit %d/%d i %d kvh %d nq %d nr %d r0 %d rows %d sp %d/%d t %d-%d keys %d-%d pair %d\n",
+               blockIdx.x, k, n_my, x.i, x.kvh, x.nq, x.nr, x.r0, rows, x.sp, x.nsplit, x.t_lo, x.t_hi, x.kbeg, x.kend, x.pair);
+        __trap();
+      }
+    }
+  }
   if (threadIdx.x == 0 && a.trace) a.trace[((size_t)blockIdx.x * 8 + 7) * kTraceEv] = clock64();
   const uint32_t tmem = *tmem_sh;
 
@@ -839,12 +864,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       };
       auto issue_pv = [&]() {
         const Unit& x = utab[pu];
-        const uint32_t ob = pu & 1, pb = pg & 1;
+        const uint32_t ob = pu & 1, pb = pg % NPB;
         const bool first = pt == x.t_lo, last = pt + 1 == x.t_hi;
         const int NQ = (x.nq + 15) & ~15;
         const uint32_t idesc_pv = idesc_bf16(DH, NQ, true, true);
         const uint32_t idesc_l = idesc_bf16(128, NQ, false, true);
-        mbar_wait(&pfull[pb], (pg >> 1) & 1);
+        mbar_wait(&pfull[pb], (pg / NPB) & 1);
         tr.ev(5);
         if (first) mbar_wait(&ofree[ob], ((pu >> 1) & 1) ^ 1);
         const uint32_t vs = pg % SV;
@@ -871,13 +896,79 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         if (++pt == x.t_hi && ++pu < n_my) pt = utab[pu].t_lo;
       };
       tr.ev(0);
-      if (!IMP_ONLY) {
+      if (a.split_issue) {
+        // QK^T issuer only (PV^T is issued by warp 3), and the Q loader: the Q tile of unit u goes into
+        // buffer u & 1 once the QK^T MMAs of unit u - 2 have completed (probed after every issue, waited
+        // for only when unit u is about to start), so a QK^T never waits behind a PV^T's dependencies
+        // and the K ring slot is released as soon as its tile has landed and an S^T buffer is free.
+        int q_next = 0;
+        auto load_q = [&](bool block) {
+          while (q_next < n_my && q_next <= qu + 1) {
+            const uint32_t b = q_next & 1;
+            if (q_next >= 2) {
+              const uint32_t par = ((q_next >> 1) & 1) ^ 1;
+              if (block) mbar_wait(&qempty[b], par);
+              else if (!mbar_test(&qempty[b], par)) return;
+            }
+            const Unit& x = utab[q_next];
+            mbar_expect_tx(&qfull[b], Q_BYTES);
+            uint8_t* q = sQ + b * Q_BYTES;
+            tma_load_3d(q, &mapQ, &qfull[b], 0, x.kvh * G, x.r0);
+            tma_load_3d(q + HALF_Q, &mapQ, &qfull[b], 64, x.kvh * G, x.r0);
+            ++q_next;
+          }
+        };
+        load_q(true);
+        while (qk_ready()) {
+          if (q_next <= qu) load_q(true);
+          issue_qk();
+          load_q(false);
+        }
+      } else if (!IMP_ONLY) {
         while (pu < n_my) {
           while (qk_ready() && qg < pg + NSB) issue_qk();
           issue_pv();
         }
       } else {
         while (qk_ready()) issue_qk();
+      }
+    }
+  } else if (warp == 3 && a.split_issue) {
+    // ================================================================ PV^T issuer (split issue)
+    if (lane == 0 && !IMP_ONLY) {
+      Tracer tr(a.trace, 3);
+      uint32_t pg = 0;
+      for (int pu = 0; pu < n_my; ++pu) {
+        const Unit& x = utab[pu];
+        const uint32_t ob = pu & 1;
+        const int NQ = (x.nq + 15) & ~15;
+        const uint32_t idesc_pv = idesc_bf16(DH, NQ, true, true);
+        const uint32_t idesc_l = idesc_bf16(128, NQ, false, true);
+        const uint32_t dO = tmem + O_COL + ob * NQM;
+        const uint32_t dl = tmem + L_COL + ob * NQM;
+        const uint64_t ones_desc = desc_kmajor_noswz(smem_u32(ones), 0, 0);
+        for (int pt = x.t_lo; pt < x.t_hi; ++pt, ++pg) {
+          const uint32_t pb = pg % NPB, vs = pg % SV;
+          const bool first = pt == x.t_lo;
+          mbar_wait(&pfull[pb], (pg / NPB) & 1);
+          tr.ev(5);
+          if (first) mbar_wait(&ofree[ob], ((pu >> 1) & 1) ^ 1);
+          mbar_wait(&vfull[vs], (pg / SV) & 1);
+          tr.ev(6);
+          tc_fence_after();
+          const uint32_t vb = smem_u32(sV + vs * KV_BYTES);
+          const uint32_t pa = smem_u32(sP + pb * P_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < KT / 16; ++kk) {
+            const uint64_t pdesc = desc_mnmajor_noswz(pa + kk * 256, 128, P_CHUNK);
+            const uint32_t acc = (first && kk == 0) ? 0u : 1u;
+            mma_bf16(dO, desc_mnmajor_sw128(vb + kk * 16 * 128, HALF_KV), pdesc, idesc_pv, acc);
+            mma_bf16(dl, ones_desc, pdesc, idesc_l, acc);
+          }
+          mma_commit(&vempty[vs]);
+          mma_commit(&pvdone[pb]);
+          if (pt + 1 == x.t_hi) mma_commit(&ofull[ob]);
+        }
       }
     }
   } else if (warp == 3) {

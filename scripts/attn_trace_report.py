@@ -5,7 +5,7 @@ import sys
 import numpy as np
 
 d = np.load(sys.argv[1] if len(sys.argv) > 1 else "gpurun_out/attn_trace.npz")["trace"]
-ROLES = ["Kprod", "Vprod", "MMA", "Qload", "softmax", "epilogue"]
+ROLES = ["Kprod", "Vprod", "MMA", "PV", "softmax", "epilogue"]
 MASK = (1 << 56) - 1
 
 
