@@ -200,7 +200,6 @@ struct AttnArgs {
   int* plan_n;                  // [grid] units per CTA (nullptr: the kernel builds its table itself)
   int pre_pf_tiles;             // key tiles of the first unit prefetched into L2 before the PDL wait
   int max_slots;                // request slots (rows of the page table)
-  int split_issue;              // 1: QK^T and PV^T MMAs issued by two threads (warp 1 / warp 3), 0: one thread
   int debug_check;              // 1: unit-table sanity checks (trap with a message; FOCUS_ATTN_CHECK=1)
 };
 void launch_attention(const AttnArgs& a, cudaStream_t s);

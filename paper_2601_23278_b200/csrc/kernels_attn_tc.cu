@@ -22,14 +22,13 @@
 // (deterministic).
 //
 // Persistent CTA (one per SM), 384 threads, warp-specialised:
-//   warp 0 / 2  TMA producers: K tiles / V tiles (128 keys x 128, 128-B swizzle), 2-slot rings each
-//               (K is freed when QK^T completes, V when PV completes)
-//   warp 1      QK^T issuer (one thread) + Q loader (one 3-D TMA box per 64-column half: rows n = r*G + g):
-//               S^T into one of three TMEM tiles
+//   warp 0 / 2  TMA producers: K tiles / V tiles (128 keys x 128, 128-B swizzle); 3-slot K ring (freed when
+//               QK^T completes: the K stream is bound by the TMA latency, ~3 us under full load), 2-slot V
+//               ring (freed when PV completes)
+//   warp 1      QK^T issuer (one thread) + Q loader: S^T into one of three TMEM tiles; one Q buffer
 //   warp 3      TMEM allocator + PV^T issuer (one thread): O^T += V^T P^T into a double-buffered TMEM
-//               accumulator (one per unit in flight) and the row sums L^T += ONES P^T.  Two issuing threads,
-//               so a QK^T never waits behind a PV^T's dependencies (FOCUS_ATTN_SPLIT_ISSUE=0: one thread,
-//               warp 3 then loads Q)
+//               accumulator (one per unit in flight) and the row sums L^T += ONES P^T.  Two issuing
+//               threads, so a QK^T never waits behind a PV^T's dependencies
 //   warps 4-7   softmax, thread = key: online softmax in the log2 domain with a lazy running max
 //               (the max only moves when a score exceeds it by > 2^8; then a cross-warp max, O^T
 //               column rescale and sum rescale), P^T -> double-buffered smem as bf16; block-column
@@ -48,15 +47,15 @@ using namespace tc;
 constexpr int DH = 128;           // head_dim of the tensor-core path
 constexpr int KT = 128;           // keys per tile (MMA M)
 constexpr int NQM = 64;           // max query rows per unit (MMA N)
-constexpr int SK = 2;             // K ring slots
+constexpr int SK = 3;             // K ring slots (the K stream is latency-bound: slot cycle = TMA latency)
 constexpr int SV = 2;             // V ring slots
-constexpr int UCAP = 40;          // unit descriptors per CTA kept in smem
+constexpr int UCAP = 24;          // unit descriptors per CTA kept in smem
 constexpr int NTHREADS = 384;
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kRescaleThresh = 8.0f;   // log2 units
 
 constexpr int HALF_Q = NQM * 128;               // 8 KB: one 64-column half of the Q tile
-constexpr int Q_BYTES = 2 * HALF_Q;             // 16 KB
+constexpr int Q_BYTES = 2 * HALF_Q;             // 16 KB (one buffer: unit u+1's Q loads once unit u's QK^T are done)
 constexpr int HALF_KV = KT * 128;               // 16 KB: one 64-column half of a K / V tile
 constexpr int KV_BYTES = 2 * HALF_KV;           // 32 KB
 constexpr int P_CHUNK = (KT / 8) * 128;         // 2 KB: 8 query rows x 128 keys of P^T
@@ -69,11 +68,11 @@ constexpr int S_COL = 2 * NQM;                  // S^T buffers [128, 192), [192,
 constexpr int L_COL = (2 + NSB) * NQM;          // row-sum buffers [320, 384), [384, 448): ONES . P^T
 constexpr int MAXS = 16;                        // split partials merged through smem
 constexpr int OFF_Q = 0;
-constexpr int OFF_K = OFF_Q + 2 * Q_BYTES;
+constexpr int OFF_K = OFF_Q + Q_BYTES;
 constexpr int OFF_V = OFF_K + SK * KV_BYTES;
 constexpr int OFF_P = OFF_V + SV * KV_BYTES;
 constexpr int OFF_BAR = OFF_P + NPB * P_BYTES;
-constexpr int N_BARS = 2 * SK + 2 * SV + 4 + 2 * NSB + 2 * NPB + 6;
+constexpr int N_BARS = 2 * SK + 2 * SV + 2 + 2 * NSB + 2 * NPB + 6;
 constexpr int OFF_MISC = OFF_BAR + 8 * N_BARS + 16;
 constexpr int OFF_M = OFF_MISC;                 // float [NQM] running max (log2 units)
 constexpr int OFF_ALPHA = OFF_M + NQM * 4;      // float [NQM]
@@ -84,9 +83,10 @@ constexpr int OFF_RED = OFF_STAT + 2 * NQM * 4; // float [4][64]
 constexpr int OFF_FLAG = OFF_RED + 4 * 64 * 4;  // int [2][4]
 constexpr int OFF_ONES = OFF_FLAG + 64;         // 128 B of bf16 ones (A operand of the row-sum MMA)
 constexpr int OFF_MERGE = OFF_ONES + 128;       // float [MAXS + 1][NQM] split-merge scales + 1/l
-constexpr int OFF_OST = OFF_MERGE + (MAXS + 1) * NQM * 4;   // bf16 [NQM][DH] output staging (rows r, heads g)
-constexpr int OFF_UTAB = OFF_OST + NQM * DH * 2;
+constexpr int OFF_OST = OFF_MERGE + (MAXS + 1) * NQM * 4;   // bf16 [2][16][DH] output staging, 16 query rows per buffer
+constexpr int OFF_UTAB = OFF_OST + 2 * 16 * DH * 2;
 constexpr int SMEM_BYTES = OFF_UTAB + UCAP * 80 + 1024;
+static_assert(SMEM_BYTES <= 227 * 1024 - 64, "attention shared memory");
 
 using Unit = AttnUnit;
 static_assert(sizeof(Unit) == 80, "unit descriptor size");
@@ -634,9 +634,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   uint64_t* kempty = kfull + SK;           // [SK]
   uint64_t* vfull = kempty + SK;           // [SV]
   uint64_t* vempty = vfull + SV;           // [SV]
-  uint64_t* qfull = vempty + SV;           // [2]
-  uint64_t* qempty = qfull + 2;            // [2]
-  uint64_t* sfull = qempty + 2;            // [NSB]
+  uint64_t* qfull = vempty + SV;           // [1]
+  uint64_t* qempty = qfull + 1;            // [1]
+  uint64_t* sfull = qempty + 1;            // [NSB]
   uint64_t* sfree = sfull + NSB;           // [NSB]  (4 softmax warps)
   uint64_t* pfull = sfree + NSB;           // [NPB]  (4 softmax warps)
   uint64_t* pvdone = pfull + NPB;          // [NPB]
@@ -656,7 +656,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   ss.sfull = sfull; ss.sfree = sfree; ss.pfull = pfull; ss.pvdone = pvdone; ss.ofree = ofree; ss.statfull = statfull;
   uint16_t* ones = (uint16_t*)(smem + OFF_ONES);
   Unit* utab = (Unit*)(smem + OFF_UTAB);
-  int* pre = (int*)sQ;                     // setup only (aliases the Q buffers: 17 KB of scan scratch)
+  int* pre = (int*)sP;                     // setup only (aliases the P^T buffers: 17 KB of scan scratch)
   int* nsp = pre + 1028;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -681,8 +681,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     for (int i = 0; i < SV; ++i) { mbar_init(&vfull[i], 1); mbar_init(&vempty[i], 1); }
     for (int i = 0; i < NSB; ++i) { mbar_init(&sfull[i], 1); mbar_init(&sfree[i], 4); }
     for (int i = 0; i < NPB; ++i) { mbar_init(&pfull[i], 4); mbar_init(&pvdone[i], 1); }
+    mbar_init(&qfull[0], 1);
+    mbar_init(&qempty[0], 1);
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&qfull[i], 1); mbar_init(&qempty[i], 1);
       mbar_init(&ofull[i], 1); mbar_init(&ofree[i], 4);
       mbar_init(&statfull[i], 4);
     }
@@ -820,124 +821,56 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
     }
   } else if (warp == 1) {
-    // ================================================================ MMA issuer
-    // Two cursors over the CTA's flattened tile sequence: QK^T runs up to two tiles ahead of PV (the
-    // S^T tile is double-buffered and freed as soon as the softmax has read it), so the K ring is
-    // released early and the TMA keeps streaming while the softmax works.
+    // ================================================================ QK^T issuer + Q loader
+    // S^T(t) = K_t . Q^T into one of NSB TMEM tiles, up to NSB tiles ahead of the softmax; the K ring
+    // slot is released as soon as its QK^T completes.  This thread issues no PV^T (warp 3 does), so a
+    // QK^T never waits behind the softmax.  Q: one buffer; unit u's Q tile (one 3-D TMA box per 64-column
+    // half: row n = r*G + g holds head kvh*G + g of block row r0 + r; rows past the unit belong to other
+    // requests or are zero-filled out of bounds and their results are discarded) is loaded once the
+    // QK^T MMAs of unit u-1 have completed -- the softmax still has up to NSB S^T tiles queued then.
     if (lane == 0) {
       Tracer tr(a.trace, 2);
-      int qu = 0, qt = n_my > 0 ? utab[0].t_lo : 0;   // QK cursor (unit, tile)
-      int pu = 0, pt = qt;                            // PV cursor
-      uint32_t qg = 0, pg = 0;
-      auto qk_ready = [&]() { return qu < n_my; };
-      auto issue_qk = [&]() {
+      uint32_t qg = 0;
+      for (int qu = 0; qu < n_my; ++qu) {
         const Unit& x = utab[qu];
-        const uint32_t ob = qu & 1;
-        if (qt == x.t_lo) {
-          mbar_wait(&qfull[ob], (qu >> 1) & 1);
-          tr.ev(2);
-        }
-        const uint32_t ks = qg % SK, sb = qg % NSB;
-        mbar_wait(&kfull[ks], (qg / SK) & 1);
-        tr.ev(3);
-        mbar_wait(&sfree[sb], ((qg / NSB) & 1) ^ 1);
-        tr.ev(4);
-        tc_fence_after();
+        if (qu > 0) mbar_wait(&qempty[0], (qu - 1) & 1);
+        mbar_expect_tx(&qfull[0], Q_BYTES);
+        tma_load_3d(sQ, &mapQ, &qfull[0], 0, x.kvh * G, x.r0);
+        tma_load_3d(sQ + HALF_Q, &mapQ, &qfull[0], 64, x.kvh * G, x.r0);
+        mbar_wait(&qfull[0], qu & 1);
+        tr.ev(2);
         const int NQ = (x.nq + 15) & ~15;
         const uint32_t idesc_qk = idesc_bf16(KT, NQ, false, false);
-        const uint32_t qa = smem_u32(sQ + ob * Q_BYTES);
-        const uint32_t kb = smem_u32(sK + ks * KV_BYTES);
-        const uint32_t d = tmem + S_COL + sb * NQM;
+        const uint32_t qa = smem_u32(sQ);
+        for (int qt = x.t_lo; qt < x.t_hi; ++qt, ++qg) {
+          const uint32_t ks = qg % SK, sb = qg % NSB;
+          mbar_wait(&kfull[ks], (qg / SK) & 1);
+          tr.ev(3);
+          mbar_wait(&sfree[sb], ((qg / NSB) & 1) ^ 1);
+          tr.ev(4);
+          tc_fence_after();
+          const uint32_t kb = smem_u32(sK + ks * KV_BYTES);
+          const uint32_t d = tmem + S_COL + sb * NQM;
 #pragma unroll
-        for (int kk = 0; kk < DH / 16; ++kk) {
-          const int h = kk >> 2, w = (kk & 3) * 32;
-          mma_bf16(d, desc_kmajor_sw128(kb + h * HALF_KV + w), desc_kmajor_sw128(qa + h * HALF_Q + w), idesc_qk,
-                   kk > 0 ? 1u : 0u);
-        }
-        mma_commit(&sfull[sb]);
-        mma_commit(&kempty[ks]);
-        ++qg;
-        if (++qt == x.t_hi) {
-          mma_commit(&qempty[ob]);
-          if (++qu < n_my) qt = utab[qu].t_lo;
-        }
-      };
-      auto issue_pv = [&]() {
-        const Unit& x = utab[pu];
-        const uint32_t ob = pu & 1, pb = pg % NPB;
-        const bool first = pt == x.t_lo, last = pt + 1 == x.t_hi;
-        const int NQ = (x.nq + 15) & ~15;
-        const uint32_t idesc_pv = idesc_bf16(DH, NQ, true, true);
-        const uint32_t idesc_l = idesc_bf16(128, NQ, false, true);
-        mbar_wait(&pfull[pb], (pg / NPB) & 1);
-        tr.ev(5);
-        if (first) mbar_wait(&ofree[ob], ((pu >> 1) & 1) ^ 1);
-        const uint32_t vs = pg % SV;
-        mbar_wait(&vfull[vs], (pg / SV) & 1);
-        tr.ev(6);
-        tc_fence_after();
-        const uint32_t dO = tmem + O_COL + ob * NQM;
-        const uint32_t dl = tmem + L_COL + ob * NQM;
-        const uint32_t vb = smem_u32(sV + vs * KV_BYTES);
-        const uint32_t pa = smem_u32(sP + pb * P_BYTES);
-        const uint64_t ones_desc = desc_kmajor_noswz(smem_u32(ones), 0, 0);
-#pragma unroll
-        for (int kk = 0; kk < KT / 16; ++kk) {
-          const uint64_t pdesc = desc_mnmajor_noswz(pa + kk * 256, 128, P_CHUNK);
-          const uint32_t acc = (first && kk == 0) ? 0u : 1u;
-          mma_bf16(dO, desc_mnmajor_sw128(vb + kk * 16 * 128, HALF_KV), pdesc, idesc_pv, acc);
-          // row sums on the tensor core: L^T[lane][n] += sum_k 1 * P^T[k][n] (every lane holds l_n)
-          mma_bf16(dl, ones_desc, pdesc, idesc_l, acc);
-        }
-        mma_commit(&vempty[vs]);
-        mma_commit(&pvdone[pb]);
-        if (last) mma_commit(&ofull[ob]);
-        ++pg;
-        if (++pt == x.t_hi && ++pu < n_my) pt = utab[pu].t_lo;
-      };
-      tr.ev(0);
-      if (a.split_issue) {
-        // QK^T issuer only (PV^T is issued by warp 3), and the Q loader: the Q tile of unit u goes into
-        // buffer u & 1 once the QK^T MMAs of unit u - 2 have completed (probed after every issue, waited
-        // for only when unit u is about to start), so a QK^T never waits behind a PV^T's dependencies
-        // and the K ring slot is released as soon as its tile has landed and an S^T buffer is free.
-        int q_next = 0;
-        auto load_q = [&](bool block) {
-          while (q_next < n_my && q_next <= qu + 1) {
-            const uint32_t b = q_next & 1;
-            if (q_next >= 2) {
-              const uint32_t par = ((q_next >> 1) & 1) ^ 1;
-              if (block) mbar_wait(&qempty[b], par);
-              else if (!mbar_test(&qempty[b], par)) return;
-            }
-            const Unit& x = utab[q_next];
-            mbar_expect_tx(&qfull[b], Q_BYTES);
-            uint8_t* q = sQ + b * Q_BYTES;
-            tma_load_3d(q, &mapQ, &qfull[b], 0, x.kvh * G, x.r0);
-            tma_load_3d(q + HALF_Q, &mapQ, &qfull[b], 64, x.kvh * G, x.r0);
-            ++q_next;
+          for (int kk = 0; kk < DH / 16; ++kk) {
+            const int h = kk >> 2, w = (kk & 3) * 32;
+            mma_bf16(d, desc_kmajor_sw128(kb + h * HALF_KV + w), desc_kmajor_sw128(qa + h * HALF_Q + w), idesc_qk,
+                     kk > 0 ? 1u : 0u);
           }
-        };
-        load_q(true);
-        while (qk_ready()) {
-          if (q_next <= qu) load_q(true);
-          issue_qk();
-          load_q(false);
+          mma_commit(&sfull[sb]);
+          mma_commit(&kempty[ks]);
         }
-      } else if (!IMP_ONLY) {
-        while (pu < n_my) {
-          while (qk_ready() && qg < pg + NSB) issue_qk();
-          issue_pv();
-        }
-      } else {
-        while (qk_ready()) issue_qk();
+        mma_commit(&qempty[0]);
       }
     }
-  } else if (warp == 3 && a.split_issue) {
-    // ================================================================ PV^T issuer (split issue)
+  } else if (warp == 3) {
+    // ================================================================ PV^T issuer
+    // O^T += V_t^T . P_t^T and the row sums L^T += ONES . P_t^T (every lane holds l_n) into the unit's
+    // double-buffered TMEM accumulator
     if (lane == 0 && !IMP_ONLY) {
       Tracer tr(a.trace, 3);
       uint32_t pg = 0;
+      const uint64_t ones_desc = desc_kmajor_noswz(smem_u32(ones), 0, 0);
       for (int pu = 0; pu < n_my; ++pu) {
         const Unit& x = utab[pu];
         const uint32_t ob = pu & 1;
@@ -946,7 +879,6 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const uint32_t idesc_l = idesc_bf16(128, NQ, false, true);
         const uint32_t dO = tmem + O_COL + ob * NQM;
         const uint32_t dl = tmem + L_COL + ob * NQM;
-        const uint64_t ones_desc = desc_kmajor_noswz(smem_u32(ones), 0, 0);
         for (int pt = x.t_lo; pt < x.t_hi; ++pt, ++pg) {
           const uint32_t pb = pg % NPB, vs = pg % SV;
           const bool first = pt == x.t_lo;
@@ -969,25 +901,6 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           mma_commit(&pvdone[pb]);
           if (pt + 1 == x.t_hi) mma_commit(&ofull[ob]);
         }
-      }
-    }
-  } else if (warp == 3) {
-    // ================================================================ Q loader (TMA, 3-D boxes)
-    // Q tile row n = r * G + g holds head kvh*G + g of block row r0 + r: per 64-column half one box
-    // {64 columns, G heads, rpc rows} (rows past the unit belong to other requests or are zero-filled
-    // out of bounds; their results are discarded).
-    if (lane == 0) {
-      Tracer tr(a.trace, 3);
-      for (int it = 0; it < n_my; ++it) {
-        const Unit& x = utab[it];
-        const uint32_t ob = it & 1;
-        tr.ev(0);
-        mbar_wait(&qempty[ob], ((it >> 1) & 1) ^ 1);
-        tr.ev(1);
-        mbar_expect_tx(&qfull[ob], Q_BYTES);
-        uint8_t* q = sQ + ob * Q_BYTES;
-        tma_load_3d(q, &mapQ, &qfull[ob], 0, x.kvh * G, x.r0);
-        tma_load_3d(q + HALF_Q, &mapQ, &qfull[ob], 64, x.kvh * G, x.r0);
       }
     }
   } else if (warp >= 4 && warp < 8) {
@@ -1030,25 +943,30 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const int d = threadIdx.x - 256;
     const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
     Tracer tr(d == 0 ? a.trace : nullptr, 5);
-    // Output rows leave through shared memory: element (query row n = r*G + g, lane d) goes to
-    // ost[n * DH + d], i.e. block row r's G heads are one contiguous G*DH*2-byte run, matching the
-    // output row [r0 + r][kvh*G*DH, (kvh+1)*G*DH); one bulk async copy per block row then writes it
-    // (instead of 2-byte scattered stores from every thread).
-    __nv_bfloat16* ost = reinterpret_cast<__nv_bfloat16*>(smem + OFF_OST);
-    auto stage_begin = [&]() {                     // the previous unit's bulk stores have read ost
-      if (d == 0) bulk_wait_read0();
+    // Output rows leave through shared memory, 16 query rows at a time: element (query row n = r*G + g,
+    // lane d) of chunk c goes to ost[c & 1][(n - 16c) * DH + d], i.e. block row r's G heads are one
+    // contiguous G*DH*2-byte run matching the output row [r0 + r][kvh*G*DH, (kvh+1)*G*DH); one bulk async
+    // copy per block row then writes it (instead of 2-byte scattered stores from every thread).  Two
+    // chunk buffers: chunk c is staged while chunk c-1's bulk stores drain.
+    __nv_bfloat16* ost0 = reinterpret_cast<__nv_bfloat16*>(smem + OFF_OST);
+    uint32_t cc = 0;                               // chunks staged so far (buffer = cc & 1)
+    auto chunk_buf = [&]() -> __nv_bfloat16* {     // all 128 threads: a free buffer for the next chunk
+      if (d == 0) bulk_wait_read1();               // chunk cc-2's stores have read buffer cc & 1
       named_bar(2, 128);
+      return ost0 + (cc & 1) * 16 * DH;
     };
-    auto stage_flush = [&](const Unit& xr) {       // all 128 threads
+    auto chunk_flush = [&](const Unit& xr, int c) {   // all 128 threads
       fence_proxy_async();
       named_bar(2, 128);
       if (d == 0) {
-        const int nr = (xr.nq + G - 1) / G;
-        for (int r = 0; r < nr; ++r)
+        const __nv_bfloat16* buf = ost0 + (cc & 1) * 16 * DH;
+        const int r1 = min((16 * c + 16) / G, xr.nq / G);
+        for (int r = 16 * c / G; r < r1; ++r)
           bulk_store_s2g(a.out + (size_t)(xr.r0 + r) * a.ldo + (size_t)xr.kvh * G * DH,
-                         smem_u32(ost + (size_t)r * G * DH), (uint32_t)(G * DH * 2));
+                         smem_u32(buf + (size_t)(r * G - 16 * c) * DH), (uint32_t)(G * DH * 2));
         bulk_commit();
       }
+      ++cc;
     };
     for (int it = 0; it < n_my; ++it) {
       const Unit& xr = utab[it];
@@ -1060,23 +978,24 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       tr.ev(1);
       tc_fence_after();
       if (xr.nsplit == 1) {
-        // O / l -> bf16 staging, 16 query rows at a time, then one bulk store per block row
-        stage_begin();
+        // O / l -> bf16 staging, 16 query rows at a time, one bulk store per block row
 #pragma unroll 1
         for (int c = 0; c < nch; ++c) {
           uint32_t r[16], rl[16];
           tmem_ld32x16(tmem + lane_base + O_COL + ob * NQM + 16 * c, r);
           tmem_ld32x16(tmem + lane_base + L_COL + ob * NQM + 16 * c, rl);
           tmem_wait_ld();
+          if (c == nch - 1) {                      // the accumulator is in registers: free it early
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&ofree[ob]);
+          }
+          __nv_bfloat16* ost = chunk_buf();
 #pragma unroll
           for (int e = 0; e < 16; ++e)
-            if (16 * c + e < nq)
-              ost[(16 * c + e) * DH + d] = __float2bfloat16_rn(__uint_as_float(r[e]) / __uint_as_float(rl[e]));
+            if (16 * c + e < nq) ost[e * DH + d] = __float2bfloat16_rn(__uint_as_float(r[e]) / __uint_as_float(rl[e]));
+          chunk_flush(xr, c);
         }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&ofree[ob]);
-        stage_flush(xr);
         tr.ev(2);
       } else {
         // split piece: partial (unnormalised O^T rows, running max, row sum) -> workspace; the
@@ -1110,7 +1029,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         named_bar(2, 128);
         if (merge_flag == xr.nsplit - 1) {               // last piece: merge
           __threadfence();
-          stage_begin();
+          named_bar(2, 128);                             // the previous merge's readers of fsc are done
           const int ns = xr.nsplit;
           float* fsc = reinterpret_cast<float*>(smem + OFF_MERGE);   // [MAXS][NQM] scales, [MAXS][..] 1/l
           if (d < nq) {
@@ -1147,12 +1066,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll
               for (int e = 0; e < 16; ++e) acc[e] += v[e] * fsc[s2 * NQM + n0 + e];
             }
+            __nv_bfloat16* ost = chunk_buf();
 #pragma unroll
             for (int e = 0; e < 16; ++e)
-              if (n0 + e < nq) ost[(n0 + e) * DH + d] = __float2bfloat16_rn(acc[e] * fsc[MAXS * NQM + n0 + e]);
+              if (n0 + e < nq) ost[e * DH + d] = __float2bfloat16_rn(acc[e] * fsc[MAXS * NQM + n0 + e]);
+            chunk_flush(xr, n0 / 16);
           }
           if (d == 0) a.sem[xr.pair] = 0;                 // re-arm for the next launch
-          stage_flush(xr);                               // (its barrier also orders fsc reuse by the next merge)
         }
         tr.ev(2);
       }
