@@ -83,7 +83,7 @@ constexpr int OFF_RED = OFF_STAT + 2 * NQM * 4; // float [4][64]
 constexpr int OFF_FLAG = OFF_RED + 4 * 64 * 4;  // int [2][4]
 constexpr int OFF_ONES = OFF_FLAG + 64;         // 128 B of bf16 ones (A operand of the row-sum MMA)
 constexpr int OFF_MERGE = OFF_ONES + 128;       // float [MAXS + 1][NQM] split-merge scales + 1/l
-constexpr int OFF_OST = OFF_MERGE + (MAXS + 1) * NQM * 4;   // bf16 [2][16][DH] output staging, 16 query rows per buffer
+constexpr int OFF_OST = OFF_MERGE + (MAXS + 1) * NQM * 4;   // bf16 [32][DH] output staging: 32 query rows per pass
 constexpr int OFF_UTAB = OFF_OST + 2 * 16 * DH * 2;
 constexpr int SMEM_BYTES = OFF_UTAB + UCAP * 80 + 1024;
 static_assert(SMEM_BYTES <= 227 * 1024 - 64, "attention shared memory");
@@ -943,30 +943,25 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const int d = threadIdx.x - 256;
     const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
     Tracer tr(d == 0 ? a.trace : nullptr, 5);
-    // Output rows leave through shared memory, 16 query rows at a time: element (query row n = r*G + g,
-    // lane d) of chunk c goes to ost[c & 1][(n - 16c) * DH + d], i.e. block row r's G heads are one
-    // contiguous G*DH*2-byte run matching the output row [r0 + r][kvh*G*DH, (kvh+1)*G*DH); one bulk async
-    // copy per block row then writes it (instead of 2-byte scattered stores from every thread).  Two
-    // chunk buffers: chunk c is staged while chunk c-1's bulk stores drain.
-    __nv_bfloat16* ost0 = reinterpret_cast<__nv_bfloat16*>(smem + OFF_OST);
-    uint32_t cc = 0;                               // chunks staged so far (buffer = cc & 1)
-    auto chunk_buf = [&]() -> __nv_bfloat16* {     // all 128 threads: a free buffer for the next chunk
-      if (d == 0) bulk_wait_read1();               // chunk cc-2's stores have read buffer cc & 1
+    // Output rows leave through shared memory, 32 query rows (two 16-row chunks) at a time: element
+    // (query row n = r*G + g, lane d) of pass p goes to ost[(n - 32p) * DH + d], i.e. block row r's G heads
+    // are one contiguous G*DH*2-byte run matching the output row [r0 + r][kvh*G*DH, (kvh+1)*G*DH); one
+    // bulk async copy per block row then writes it (instead of 2-byte scattered stores from every thread).
+    __nv_bfloat16* ost = reinterpret_cast<__nv_bfloat16*>(smem + OFF_OST);
+    auto pass_begin = [&]() {                      // all 128 threads: the previous pass's stores have read ost
+      if (d == 0) bulk_wait_read0();
       named_bar(2, 128);
-      return ost0 + (cc & 1) * 16 * DH;
     };
-    auto chunk_flush = [&](const Unit& xr, int c) {   // all 128 threads
+    auto pass_flush = [&](const Unit& xr, int p) {   // all 128 threads: rows [32p, 32p + 32) of the unit
       fence_proxy_async();
       named_bar(2, 128);
       if (d == 0) {
-        const __nv_bfloat16* buf = ost0 + (cc & 1) * 16 * DH;
-        const int r1 = min((16 * c + 16) / G, xr.nq / G);
-        for (int r = 16 * c / G; r < r1; ++r)
+        const int r1 = min((32 * p + 32) / G, xr.nq / G);
+        for (int r = 32 * p / G; r < r1; ++r)
           bulk_store_s2g(a.out + (size_t)(xr.r0 + r) * a.ldo + (size_t)xr.kvh * G * DH,
-                         smem_u32(buf + (size_t)(r * G - 16 * c) * DH), (uint32_t)(G * DH * 2));
+                         smem_u32(ost + (size_t)(r * G - 32 * p) * DH), (uint32_t)(G * DH * 2));
         bulk_commit();
       }
-      ++cc;
     };
     for (int it = 0; it < n_my; ++it) {
       const Unit& xr = utab[it];
@@ -978,23 +973,34 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       tr.ev(1);
       tc_fence_after();
       if (xr.nsplit == 1) {
-        // O / l -> bf16 staging, 16 query rows at a time, one bulk store per block row
+        // O * (1/l) -> bf16 staging (MUFU reciprocal: ~1 ulp of fp32 before the bf16 rounding), 32 query rows
+        // per pass, one bulk store per block row
 #pragma unroll 1
-        for (int c = 0; c < nch; ++c) {
-          uint32_t r[16], rl[16];
-          tmem_ld32x16(tmem + lane_base + O_COL + ob * NQM + 16 * c, r);
-          tmem_ld32x16(tmem + lane_base + L_COL + ob * NQM + 16 * c, rl);
+        for (int p = 0; 2 * p < nch; ++p) {
+          const bool two = 2 * p + 1 < nch;
+          uint32_t r[32], rl[32];
+          tmem_ld32x16(tmem + lane_base + O_COL + ob * NQM + 32 * p, r);
+          tmem_ld32x16(tmem + lane_base + L_COL + ob * NQM + 32 * p, rl);
+          if (two) {
+            tmem_ld32x16(tmem + lane_base + O_COL + ob * NQM + 32 * p + 16, r + 16);
+            tmem_ld32x16(tmem + lane_base + L_COL + ob * NQM + 32 * p + 16, rl + 16);
+          }
           tmem_wait_ld();
-          if (c == nch - 1) {                      // the accumulator is in registers: free it early
+          tr.ev(3);
+          if (2 * p + 2 >= nch) {                  // the accumulator is in registers: free it early
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&ofree[ob]);
           }
-          __nv_bfloat16* ost = chunk_buf();
+          pass_begin();
+          tr.ev(4);
 #pragma unroll
-          for (int e = 0; e < 16; ++e)
-            if (16 * c + e < nq) ost[e * DH + d] = __float2bfloat16_rn(__uint_as_float(r[e]) / __uint_as_float(rl[e]));
-          chunk_flush(xr, c);
+          for (int e = 0; e < 32; ++e)
+            if ((e < 16 || two) && 32 * p + e < nq)
+              ost[e * DH + d] = __float2bfloat16_rn(__uint_as_float(r[e]) * rcp_approx(__uint_as_float(rl[e])));
+          tr.ev(5);
+          pass_flush(xr, p);
+          tr.ev(6);
         }
         tr.ev(2);
       } else {
@@ -1029,7 +1035,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         named_bar(2, 128);
         if (merge_flag == xr.nsplit - 1) {               // last piece: merge
           __threadfence();
-          named_bar(2, 128);                             // the previous merge's readers of fsc are done
+          pass_begin();                                  // (also: the previous merge's readers of fsc are done)
           const int ns = xr.nsplit;
           float* fsc = reinterpret_cast<float*>(smem + OFF_MERGE);   // [MAXS][NQM] scales, [MAXS][..] 1/l
           if (d < nq) {
@@ -1066,12 +1072,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll
               for (int e = 0; e < 16; ++e) acc[e] += v[e] * fsc[s2 * NQM + n0 + e];
             }
-            __nv_bfloat16* ost = chunk_buf();
+            if (n0 % 32 == 0 && n0 > 0) {              // rows [n0 - 32, n0) staged: write them, reuse ost
+              pass_flush(xr, n0 / 32 - 1);
+              pass_begin();
+            }
 #pragma unroll
             for (int e = 0; e < 16; ++e)
-              if (n0 + e < nq) ost[e * DH + d] = __float2bfloat16_rn(acc[e] * fsc[MAXS * NQM + n0 + e]);
-            chunk_flush(xr, n0 / 16);
+              if (n0 + e < nq) ost[(n0 % 32 + e) * DH + d] = __float2bfloat16_rn(acc[e] * fsc[MAXS * NQM + n0 + e]);
           }
+          pass_flush(xr, (nq - 1) / 32);
           if (d == 0) a.sem[xr.pair] = 0;                 // re-arm for the next launch
         }
         tr.ev(2);

@@ -349,6 +349,11 @@ __device__ __forceinline__ uint4 lds128(uint32_t saddr) {
                : "memory");
   return v;
 }
+__device__ __forceinline__ float rcp_approx(float x) {   // MUFU.RCP (~1 ulp)
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
