@@ -80,7 +80,7 @@ constexpr int OFF_THR = OFF_ALPHA + NQM * 4;    // float [NQM] raw-score rescale
 constexpr int OFF_NM = OFF_THR + NQM * 4;       // float [NQM] -m (0 while m = -inf)
 constexpr int OFF_STAT = OFF_NM + NQM * 4;      // float [2][NQM] m for the epilogue (split merge)
 constexpr int OFF_RED = OFF_STAT + 2 * NQM * 4; // float [4][64]
-constexpr int OFF_FLAG = OFF_RED + 4 * 64 * 4;  // int [2][4]
+constexpr int OFF_FLAG = OFF_RED + 4 * 64 * 4;  // float [4] chunk threshold minima (64 B reserved)
 constexpr int OFF_ONES = OFF_FLAG + 64;         // 128 B of bf16 ones (A operand of the row-sum MMA)
 constexpr int OFF_MERGE = OFF_ONES + 128;       // float [MAXS + 1][NQM] split-merge scales + 1/l
 constexpr int OFF_OST = OFF_MERGE + (MAXS + 1) * NQM * 4;   // bf16 [32][DH] output staging: 32 query rows per pass
@@ -199,7 +199,7 @@ struct SoftSmem {
   float* nm;         // [NQM] -m (0 while m = -inf)
   float* stat;       // [2][NQM] m of the finished unit (split merge)
   float* red;        // [4][64]
-  int* flags;        // [2][4]
+  float* tmin;       // [4] per 16-row chunk: the smallest row threshold (the per-tile check compares with it)
   uint8_t* sP;
   uint64_t *sfull, *sfree, *pfull, *pvdone, *ofree, *statfull;
 };
@@ -225,6 +225,7 @@ __device__ __forceinline__ void softmax_unit(const AttnArgs& a, const Unit& xr, 
     ss.thr[L] = L < nq ? -CUDART_INF_F : CUDART_INF_F;
     ss.nm[L] = 0.f;
   }
+  if (L < NQM / 16) ss.tmin[L] = 16 * L < nq ? -CUDART_INF_F : CUDART_INF_F;
   named_bar(1, 128);
   for (int t = xr.t_lo; t < xr.t_hi; ++t, ++g) {
     const uint32_t sb = g % NSB, pb = g % NPB;
@@ -242,9 +243,17 @@ __device__ __forceinline__ void softmax_unit(const AttnArgs& a, const Unit& xr, 
     tc_fence_before();                             // S^T is in registers: the tile may be overwritten
     __syncwarp();
     if (lane == 0) mbar_arrive(&ss.sfree[sb]);
-    // ---- (1) threshold check
+    // ---- (1) threshold check: against the chunk's smallest row threshold (conservative: a hit only sends
+    // the tile through the exact per-row test below)
     bool need = false;
-    if (kvalid) {
+    if (kvalid && !CAUSAL) {
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) {
+        const float tc = ss.tmin[c];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) need |= __uint_as_float(r[c][e]) > tc;
+      }
+    } else if (kvalid) {
 #pragma unroll
       for (int c = 0; c < NCH; ++c) {
 #pragma unroll
@@ -268,12 +277,9 @@ __device__ __forceinline__ void softmax_unit(const AttnArgs& a, const Unit& xr, 
     }
     if (IMP_ONLY) continue;
     tr.ev(7);
-    const int anyw = __any_sync(0xffffffffu, need);
-    if (lane == 0) ss.flags[(g & 1) * 4 + th.q4] = anyw;
-    named_bar(1, 128);
+    const bool any_need = named_bar_or(1, 128, need);   // one barrier: does any key of the tile need it?
     tr.ev(8);
-    const int* fl = ss.flags + (g & 1) * 4;
-    if (fl[0] | fl[1] | fl[2] | fl[3]) {
+    if (any_need) {
       tr.ev(9);
       // ---- slow path: exact tile max per row (transposed butterfly + 4-warp combine)
 #pragma unroll
@@ -292,6 +298,7 @@ __device__ __forceinline__ void softmax_unit(const AttnArgs& a, const Unit& xr, 
         ss.red[th.q4 * 64 + rd * 32 + lane] = warp_transpose_reduce<true>(v, lane);
       }
       named_bar(1, 128);
+      bool moved = false;
       if (L < NQM) {
         float al = 1.f;
         if (L < nq && L < NCH * 16) {
@@ -303,12 +310,20 @@ __device__ __forceinline__ void softmax_unit(const AttnArgs& a, const Unit& xr, 
             ss.m[L] = mn;
             ss.nm[L] = -mn;
             ss.thr[L] = (mn + kRescaleThresh) / th.sl2;
+            moved = true;
           }
         }
         ss.alpha[L] = al;
       }
+      moved = named_bar_or(1, 128, moved);         // did any row's running max move?
+      if (L < NQM / 16) {                          // chunk minima of the (possibly) moved thresholds
+        float tm = CUDART_INF_F;
+#pragma unroll
+        for (int e = 0; e < 16; ++e) tm = fminf(tm, ss.thr[16 * L + e]);
+        ss.tmin[L] = tm;
+      }
       named_bar(1, 128);
-      if (t > xr.t_lo) {                           // O^T and L^T columns *= alpha (PV of tile g-1 done)
+      if (t > xr.t_lo && moved) {                  // O^T and L^T columns *= alpha (PV of tile g-1 done)
         mbar_wait(&ss.pvdone[(g - 1) % NPB], ((g - 1) / NPB) & 1);
         tr.ev(10);
         tc_fence_after();
@@ -651,7 +666,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   ss.nm = (float*)(smem + OFF_NM);
   ss.stat = (float*)(smem + OFF_STAT);
   ss.red = (float*)(smem + OFF_RED);
-  ss.flags = (int*)(smem + OFF_FLAG);
+  ss.tmin = (float*)(smem + OFF_FLAG);
   ss.sP = sP;
   ss.sfull = sfull; ss.sfree = sfree; ss.pfull = pfull; ss.pvdone = pvdone; ss.ofree = ofree; ss.statfull = statfull;
   uint16_t* ones = (uint16_t*)(smem + OFF_ONES);
