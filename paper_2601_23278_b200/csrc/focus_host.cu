@@ -347,7 +347,10 @@ void derive(focus_ctx* x) {
   const int64_t pages = c.kv_pages > 0 ? c.kv_pages : (int64_t)c.max_requests * x->max_pages_per_req;
   x->kv_pages = pages;
   x->kv_layer_elems = (size_t)pages * c.n_kv_heads * c.page_size * c.head_dim;
-  x->attn_tc = attn_tc_supported(c.head_dim, c.page_size, x->G) && getenv("FOCUS_ATTN_SIMT") == nullptr;
+  // (the tensor-core kernel's importance epilogue unrolls MaxPool windows up to k = 5; wider windows take
+  // the SIMT kernel)
+  x->attn_tc = attn_tc_supported(c.head_dim, c.page_size, x->G) && c.maxpool_kernel <= 5 &&
+               getenv("FOCUS_ATTN_SIMT") == nullptr;
   x->attn_rpc = x->attn_tc ? attn_tc_rows_per_chunk(x->G) : kAttnQRows / x->G;
   x->n_chunks = (x->B + x->attn_rpc - 1) / x->attn_rpc;
   x->split_tiles = 16;                         // 128-key tiles per split (the kernel may enlarge it)
@@ -617,7 +620,11 @@ bool plan_attention(focus_ctx* x, AttnArgs& a, int k) {
   return true;
 }
 
-void run_attention(focus_ctx* x, const AttnArgs& a) {
+void run_attention(focus_ctx* x, const AttnArgs& a0) {
+  AttnArgs a = a0;
+  // debug: FOCUS_ATTN_TRACE_IMP=1 traces the layer's importance-only launch instead of its attention
+  static const int trace_imp = getenv("FOCUS_ATTN_TRACE_IMP") ? 1 : 0;
+  if (a.trace && trace_imp != a.imp_only) a.trace = nullptr;
   if (a.trace) cudaMemsetAsync(a.trace, 0, (size_t)num_sms() * 8 * kTraceEv * 8, x->stream);
   if (x->attn_tc) launch_attention_tc(x->mapK, x->mapV, a.q == x->qS ? x->mapQ_qs : x->mapQ_qkv, a, x->stream);
   else launch_attention(a, x->stream);

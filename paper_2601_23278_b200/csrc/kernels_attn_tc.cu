@@ -53,6 +53,7 @@ constexpr int UCAP = 24;          // unit descriptors per CTA kept in smem
 constexpr int NTHREADS = 384;
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kRescaleThresh = 8.0f;   // log2 units
+constexpr int kMaxPoolRad = 2;           // MaxPool1D kernel <= 5 (the host rejects larger)
 
 constexpr int HALF_Q = NQM * 128;               // 8 KB: one 64-column half of the Q tile
 constexpr int Q_BYTES = 2 * HALF_Q;             // 16 KB (one buffer: unit u+1's Q loads once unit u's QK^T are done)
@@ -72,7 +73,7 @@ constexpr int OFF_K = OFF_Q + Q_BYTES;
 constexpr int OFF_V = OFF_K + SK * KV_BYTES;
 constexpr int OFF_P = OFF_V + SV * KV_BYTES;
 constexpr int OFF_BAR = OFF_P + NPB * P_BYTES;
-constexpr int N_BARS = 2 * SK + 2 * SV + 2 + 2 * NSB + 2 * NPB + 6;
+constexpr int N_BARS = 2 * SK + 2 * SV + 4 + 2 * NSB + 2 * NPB + 6;
 constexpr int OFF_MISC = OFF_BAR + 8 * N_BARS + 16;
 constexpr int OFF_M = OFF_MISC;                 // float [NQM] running max (log2 units)
 constexpr int OFF_ALPHA = OFF_M + NQM * 4;      // float [NQM]
@@ -395,44 +396,74 @@ __device__ __forceinline__ void softmax_unit(const AttnArgs& a, const Unit& xr, 
 // Eq.2 on the block scores of the unit (scratch rows = query rows n = r*G + g): per row MaxPool1D
 // (k = mp_kernel, -inf outside P; A-I3, A-I5), softmax over P, then the sum over rows and heads in a
 // fixed order (lanes, then warps) -> one partial per (request, chunk, kv head).
-__device__ __noinline__ void importance_epilogue(const AttnArgs& a, const Unit& xr, const SoftThread& th,
-                                                 const SoftSmem& ss) {
+template <int KB>
+__device__ __noinline__ void importance_epilogue_t(const AttnArgs& a, const Unit& xr, const SoftThread& th,
+                                                   const SoftSmem& ss) {
   named_bar(1, 128);                               // all block scores of the unit are in scratch
   const int B = a.B, rad = a.mp_kernel / 2, L = th.L, lane = th.lane;
   const uint64_t P = xr.P;
   const bool rr = L < xr.nq;
-  const float* sc = th.scr + L * kMaxB;
-  float w[kMaxB];
-  float mx = -CUDART_INF_F;
+  // the row's B scores in registers (one batch of vector loads: a per-element load chain through the
+  // L2 made this epilogue ~22 k cycles per unit), then MaxPool / softmax in registers
+  float w[KB];
   if (rr) {
-    for (int j = 0; j < B; ++j) {
+    const float* sc = th.scr + L * kMaxB;
+    float sv[KB];
+#pragma unroll
+    for (int j4 = 0; j4 < KB; j4 += 4) {
+      const float4 v4 = j4 < B ? *reinterpret_cast<const float4*>(sc + j4) : make_float4(0.f, 0.f, 0.f, 0.f);
+      sv[j4] = v4.x; sv[j4 + 1] = v4.y; sv[j4 + 2] = v4.z; sv[j4 + 3] = v4.w;
+    }
+    float mx = -CUDART_INF_F;
+#pragma unroll
+    for (int j = 0; j < KB; ++j) {
       float v = -CUDART_INF_F;
-      if ((P >> j) & 1ull) {
-        const int lo = max(0, j - rad), hi = min(B - 1, j + rad);
-        for (int jj = lo; jj <= hi; ++jj)
-          if ((P >> jj) & 1ull) v = fmaxf(v, sc[jj]);
+      if (j < B && ((P >> j) & 1ull)) {
+#pragma unroll
+        for (int d = -kMaxPoolRad; d <= kMaxPoolRad; ++d) {
+          const int jj = j + d;
+          if (jj >= 0 && jj < KB && d >= -rad && d <= rad && jj < B && ((P >> jj) & 1ull)) v = fmaxf(v, sv[jj]);
+        }
       }
       w[j] = v;
       mx = fmaxf(mx, v);
     }
     float z = 0.f;
-    for (int j = 0; j < B; ++j) {
-      const float e = w[j] == -CUDART_INF_F ? 0.f : expf(w[j] - mx);
+#pragma unroll
+    for (int j = 0; j < KB; ++j) {
+      const float e = w[j] == -CUDART_INF_F ? 0.f : __expf(w[j] - mx);
       w[j] = e;
       z += e;
     }
-    for (int j = 0; j < B; ++j) w[j] = w[j] / z;
+    const float iz = 1.0f / z;
+#pragma unroll
+    for (int j = 0; j < KB; ++j) w[j] *= iz;
+  } else {
+#pragma unroll
+    for (int j = 0; j < KB; ++j) w[j] = 0.f;
   }
-  for (int j = 0; j < B; ++j) {
-    float v = rr ? w[j] : 0.f;
-    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (lane == 0) ss.red[th.q4 * 64 + j] = v;
+  // column sums over the warp's 32 rows: transposed butterfly (31 shuffles per 32 columns), lane j
+  // then holds column 32q + j of this warp, in a fixed order
+#pragma unroll
+  for (int q = 0; q < KB / 32 + (KB % 32 ? 1 : 0); ++q) {
+    float v[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = (32 * q + i < KB) ? w[32 * q + i] : 0.f;
+    const float cs = warp_transpose_reduce<false>(v, lane);
+    if (32 * q + lane < B) ss.red[th.q4 * 64 + 32 * q + lane] = cs;
   }
   named_bar(1, 128);
   if (th.q4 == 0)
     for (int j = lane; j < B; j += 32)
       a.imp[(size_t)xr.pair * B + j] = ((ss.red[j] + ss.red[64 + j]) + ss.red[128 + j]) + ss.red[192 + j];
   named_bar(1, 128);                               // red[] reuse
+}
+
+__device__ __forceinline__ void importance_epilogue(const AttnArgs& a, const Unit& xr, const SoftThread& th,
+                                                    const SoftSmem& ss) {
+  if (a.B <= 16) importance_epilogue_t<16>(a, xr, th, ss);
+  else if (a.B <= 32) importance_epilogue_t<32>(a, xr, th, ss);
+  else importance_epilogue_t<64>(a, xr, th, ss);
 }
 
 // Unit table of CTA `cta` of `ncta` (the attention grid): per-request unit counts, exclusive prefix,
@@ -649,9 +680,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   uint64_t* kempty = kfull + SK;           // [SK]
   uint64_t* vfull = kempty + SK;           // [SV]
   uint64_t* vempty = vfull + SV;           // [SV]
-  uint64_t* qfull = vempty + SV;           // [1]
-  uint64_t* qempty = qfull + 1;            // [1]
-  uint64_t* sfull = qempty + 1;            // [NSB]
+  uint64_t* qfull = vempty + SV;           // [2]  (the second buffer: importance-only mode)
+  uint64_t* qempty = qfull + 2;            // [2]
+  uint64_t* sfull = qempty + 2;            // [NSB]
   uint64_t* sfree = sfull + NSB;           // [NSB]  (4 softmax warps)
   uint64_t* pfull = sfree + NSB;           // [NPB]  (4 softmax warps)
   uint64_t* pvdone = pfull + NPB;          // [NPB]
@@ -696,8 +727,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     for (int i = 0; i < SV; ++i) { mbar_init(&vfull[i], 1); mbar_init(&vempty[i], 1); }
     for (int i = 0; i < NSB; ++i) { mbar_init(&sfull[i], 1); mbar_init(&sfree[i], 4); }
     for (int i = 0; i < NPB; ++i) { mbar_init(&pfull[i], 4); mbar_init(&pvdone[i], 1); }
-    mbar_init(&qfull[0], 1);
-    mbar_init(&qempty[0], 1);
+    for (int i = 0; i < 2; ++i) { mbar_init(&qfull[i], 1); mbar_init(&qempty[i], 1); }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&ofull[i], 1); mbar_init(&ofree[i], 4);
       mbar_init(&statfull[i], 4);
@@ -839,24 +869,33 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     // ================================================================ QK^T issuer + Q loader
     // S^T(t) = K_t . Q^T into one of NSB TMEM tiles, up to NSB tiles ahead of the softmax; the K ring
     // slot is released as soon as its QK^T completes.  This thread issues no PV^T (warp 3 does), so a
-    // QK^T never waits behind the softmax.  Q: one buffer; unit u's Q tile (one 3-D TMA box per 64-column
-    // half: row n = r*G + g holds head kvh*G + g of block row r0 + r; rows past the unit belong to other
-    // requests or are zero-filled out of bounds and their results are discarded) is loaded once the
-    // QK^T MMAs of unit u-1 have completed -- the softmax still has up to NSB S^T tiles queued then.
+    // QK^T never waits behind the softmax.  Q: unit u's Q tile (one 3-D TMA box per 64-column half: row
+    // n = r*G + g holds head kvh*G + g of block row r0 + r; rows past the unit belong to other requests or
+    // are zero-filled out of bounds and their results are discarded) goes into buffer u % NQB once the
+    // QK^T MMAs of unit u - NQB have completed.  One buffer for attention (the softmax still has up to NSB
+    // S^T tiles of the previous unit queued then); two in the importance-only mode, whose units are one
+    // tile each (the idle V ring holds the second).
     if (lane == 0) {
       Tracer tr(a.trace, 2);
+      constexpr int NQB = IMP_ONLY ? 2 : 1;
+      auto qbuf = [&](int b) { return b == 0 ? sQ : sV; };
+      auto load_q = [&](int u) {
+        const Unit& x = utab[u];
+        const int b = u % NQB;
+        mbar_expect_tx(&qfull[b], Q_BYTES);
+        tma_load_3d(qbuf(b), &mapQ, &qfull[b], 0, x.kvh * G, x.r0);
+        tma_load_3d(qbuf(b) + HALF_Q, &mapQ, &qfull[b], 64, x.kvh * G, x.r0);
+      };
+      for (int u = 0; u < NQB && u < n_my; ++u) load_q(u);
       uint32_t qg = 0;
       for (int qu = 0; qu < n_my; ++qu) {
         const Unit& x = utab[qu];
-        if (qu > 0) mbar_wait(&qempty[0], (qu - 1) & 1);
-        mbar_expect_tx(&qfull[0], Q_BYTES);
-        tma_load_3d(sQ, &mapQ, &qfull[0], 0, x.kvh * G, x.r0);
-        tma_load_3d(sQ + HALF_Q, &mapQ, &qfull[0], 64, x.kvh * G, x.r0);
-        mbar_wait(&qfull[0], qu & 1);
+        const int qb = qu % NQB;
+        mbar_wait(&qfull[qb], (qu / NQB) & 1);
         tr.ev(2);
         const int NQ = (x.nq + 15) & ~15;
         const uint32_t idesc_qk = idesc_bf16(KT, NQ, false, false);
-        const uint32_t qa = smem_u32(sQ);
+        const uint32_t qa = smem_u32(qbuf(qb));
         for (int qt = x.t_lo; qt < x.t_hi; ++qt, ++qg) {
           const uint32_t ks = qg % SK, sb = qg % NSB;
           mbar_wait(&kfull[ks], (qg / SK) & 1);
@@ -875,7 +914,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           mma_commit(&sfull[sb]);
           mma_commit(&kempty[ks]);
         }
-        mma_commit(&qempty[0]);
+        mma_commit(&qempty[qb]);
+        if (qu + NQB < n_my) {                     // this buffer's next unit
+          mbar_wait(&qempty[qb], (qu / NQB) & 1);
+          load_q(qu + NQB);
+        }
       }
     }
   } else if (warp == 3) {
@@ -928,7 +971,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     th.lane_base = (uint32_t)(th.q4 * 32) << 16;
     th.sl2 = a.scale * kLog2e;
     th.G = G;
-    th.scr = a.imp_scratch + (size_t)blockIdx.x * NQM * kMaxB;
+    // block-score scratch [64 rows][64 columns]: the idle V ring (past the second Q buffer) in the
+    // importance-only mode, a per-CTA global slice otherwise (layer 0, where the V ring is busy)
+    th.scr = IMP_ONLY ? reinterpret_cast<float*>(sV + Q_BYTES) : a.imp_scratch + (size_t)blockIdx.x * NQM * kMaxB;
     Tracer tr(th.L == 0 ? a.trace : nullptr, 4);
     uint32_t g = 0;
     const bool causal = a.ext_mode == 2;
