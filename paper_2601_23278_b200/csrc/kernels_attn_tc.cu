@@ -270,11 +270,15 @@ __device__ __forceinline__ void softmax_unit(const AttnArgs& a, const Unit& xr, 
       }
     }
     if (xr.want_imp && kvalid && k >= xr.s0 && k < xr.s0 + a.B) {   // block-column scores (Eq.2 epilogue)
+      // scratch [block column j][query row n]: this thread's column is one contiguous run (vector stores)
+      float* col = th.scr + (size_t)(k - xr.s0) * NQM;
 #pragma unroll
       for (int c = 0; c < NCH; ++c)
 #pragma unroll
-        for (int e = 0; e < 16; ++e)
-          if (16 * c + e < nq) th.scr[(16 * c + e) * kMaxB + (k - xr.s0)] = __uint_as_float(r[c][e]) * a.scale;
+        for (int e4 = 0; e4 < 16; e4 += 4)
+          *reinterpret_cast<float4*>(col + 16 * c + e4) =
+              make_float4(__uint_as_float(r[c][e4]) * a.scale, __uint_as_float(r[c][e4 + 1]) * a.scale,
+                          __uint_as_float(r[c][e4 + 2]) * a.scale, __uint_as_float(r[c][e4 + 3]) * a.scale);
     }
     if (IMP_ONLY) continue;
     tr.ev(7);
@@ -407,13 +411,9 @@ __device__ __noinline__ void importance_epilogue_t(const AttnArgs& a, const Unit
   // L2 made this epilogue ~22 k cycles per unit), then MaxPool / softmax in registers
   float w[KB];
   if (rr) {
-    const float* sc = th.scr + L * kMaxB;
-    float sv[KB];
+    float sv[KB];                                  // scratch [column j][row]: consecutive rows coalesce
 #pragma unroll
-    for (int j4 = 0; j4 < KB; j4 += 4) {
-      const float4 v4 = j4 < B ? *reinterpret_cast<const float4*>(sc + j4) : make_float4(0.f, 0.f, 0.f, 0.f);
-      sv[j4] = v4.x; sv[j4 + 1] = v4.y; sv[j4 + 2] = v4.z; sv[j4 + 3] = v4.w;
-    }
+    for (int j = 0; j < KB; ++j) sv[j] = j < B ? th.scr[(size_t)j * NQM + L] : 0.f;
     float mx = -CUDART_INF_F;
 #pragma unroll
     for (int j = 0; j < KB; ++j) {
