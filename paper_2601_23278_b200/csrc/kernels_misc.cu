@@ -54,6 +54,8 @@ __global__ void __launch_bounds__(1024) k_step_setup(const int* __restrict__ req
   pdl_wait();
   __shared__ int scan[1024];
   __shared__ int carry;
+  __shared__ uint64_t sP[1024];
+  __shared__ int sslot[1024], soff[1024];
   if (threadIdx.x == 0) carry = 0;
   __syncthreads();
   const uint64_t full = full_mask(B);
@@ -87,15 +89,21 @@ __global__ void __launch_bounds__(1024) k_step_setup(const int* __restrict__ req
       __syncthreads();
     }
     const int excl = carry + scan[threadIdx.x] - np;
-    if (i < n_req) {
-      offP[i] = excl;
-      const focus_req_state& s = st[slot];
-      int r = excl;
-      for (uint64_t m = P; m; m &= m - 1) {
-        const int j = __ffsll((long long)m) - 1;
-        rowP[r] = RowInfo{slot, j, s.s + j, i};
-        tokP[r] = s.tok[j];
-        ++r;
+    if (i < n_req) offP[i] = excl;
+    sP[threadIdx.x] = P;
+    sslot[threadIdx.x] = slot;
+    soff[threadIdx.x] = excl;
+    __syncthreads();
+    // row maps: one thread per (request, block position), so the token loads are all in flight at once
+    const int nb = min((int)blockDim.x, n_req - base);
+    for (int e = threadIdx.x; e < nb * B; e += blockDim.x) {
+      const int li = e / B, j = e - li * B;
+      const uint64_t Pm = sP[li];
+      if ((Pm >> j) & 1ull) {
+        const int sl = sslot[li];
+        const int r = soff[li] + __popcll(Pm & ((1ull << j) - 1ull));
+        rowP[r] = RowInfo{sl, j, st[sl].s + j, base + li};
+        tokP[r] = st[sl].tok[j];
       }
     }
     __syncthreads();
