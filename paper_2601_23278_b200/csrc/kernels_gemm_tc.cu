@@ -175,6 +175,28 @@ __device__ __forceinline__ uint32_t pack_bf2(float a, float b) {
 // part / nparts: the tile's columns are split into nparts equal groups (of 32-column chunks, SwiGLU
 // 64-column pairs, RoPE half-head pairs) and this warp emits group `part` (two warps per TMEM lane
 // quarter share a tile when nparts = 2).
+// 192-wide QKV tiles (see k_gemm_pair): weight rows (relative to head 3j) of the 32-row boxes of
+// [tile parity][pair rank][box]
+__device__ __constant__ int kQkv192Rows[12] = {0, 32, 64, 96, 128, 192, 160, 224, 256, 288, 320, 352};
+// RoPE step st of QKV tile nt: accumulator columns lo (dims d0..d0+31) and hi (d0+64..d0+95) of `head`
+template <int BN>
+__device__ __forceinline__ void qkv_step(int nt, int st, int& lo, int& hi, int& head, int& d0) {
+  if constexpr (BN == 192) {
+    const int j3 = 3 * (nt >> 1);
+    if ((nt & 1) == 0) {
+      lo = st == 2 ? 128 : 32 * st;  hi = st == 2 ? 160 : 32 * st + 64;  head = j3 + (st == 2);  d0 = st == 1 ? 32 : 0;
+    } else {
+      lo = st == 0 ? 0 : 32 + 32 * st;  hi = st == 0 ? 32 : 96 + 32 * st;  head = j3 + 1 + (st > 0);  d0 = st == 2 ? 32 : (st == 0 ? 32 : 0);
+    }
+  } else {
+    const int hh = st >> 1;
+    d0 = (st & 1) * 32;
+    lo = hh * 128 + d0;
+    hi = lo + 64;
+    head = nt * (BN / 128) + hh;
+  }
+}
+
 template <int MODE, int BN, typename Chunk>
 __device__ __forceinline__ void epilogue_tile(Chunk&& chunk, int row0, int M, int nt, int N, float* __restrict__ C,
                                               int ldc, const GemmEpi& epi, uint32_t buf, int part = 0,
@@ -301,18 +323,18 @@ __device__ __forceinline__ void epilogue_tile(Chunk&& chunk, int row0, int M, in
     const unsigned long long kv_row = row < M ? (unsigned long long)kv_offset(epi.kv, ri.slot, ri.pos, 0) : 0ull;
     const size_t kv_head_stride = (size_t)epi.kv.page_size * epi.kv.head_dim;
     // (head, 32-column half-pair) steps of the tile, split evenly between the parts
-    constexpr int kSteps = (BN / 128) * 2;
+    constexpr int kSteps = BN == 192 ? 3 : (BN / 128) * 2;
 #pragma unroll 1
-    for (int st = part * (kSteps / nparts); st < (part + 1) * (kSteps / nparts); ++st) {
-      const int hh = st >> 1, c0 = (st & 1) * 32;
-      const int head = nt * (BN / 128) + hh;              // 0..Hq-1 q, then k, then v
+    for (int st = part * kSteps / nparts; st < (part + 1) * kSteps / nparts; ++st) {
+      int lo_col, hi_col, head, c0;                      // head: 0..Hq-1 q, then k, then v
+      qkv_step<BN>(nt, st, lo_col, hi_col, head, c0);
       const bool is_v = head >= epi.n_q_heads + hkv;
       const bool is_k = !is_v && head >= epi.n_q_heads;
       const int kvh = head - epi.n_q_heads - (is_v ? hkv : 0);
       {
         float lo[32], hi[32];
-        chunk(hh * 128 + c0, lo);
-        chunk(hh * 128 + c0 + 64, hi);
+        chunk(lo_col, lo);
+        chunk(hi_col, hi);
         if (!is_v && row < M) {
           const float* cr = epi.ropeT + (size_t)c0 * epi.rope_ld + row;          // [f][row]: coalesced
           const float* sr = cr + (size_t)64 * epi.rope_ld;
@@ -718,7 +740,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           stamp(0);
           if (rank == 0) mbar_expect_tx(&full[stage], 2 * STAGE_BYTES);
           const uint32_t fb = full_l + stage * 8;
-          if (hints) {
+          if (MODE == GEMM_QKV_ROPE && BN == 192) {
+            // 192-wide QKV tile = 1.5 heads, gathered so every RoPE pair (d, d + 64) stays in the tile:
+            // even tiles n = 2j: head 3j + head 3j+1 dims [0,32) and [64,96); odd tiles: head 3j+1 dims
+            // [32,64) and [96,128) + head 3j+2.  Weight rows in 32-row boxes, 3 per CTA of the pair.
+            const int base = 384 * (nt >> 1);
+            const int seg = ((nt & 1) * 2 + (int)rank) * 3;
+#pragma unroll
+            for (int i = 0; i < 3; ++i)
+              tma_load_3d_pair_hint(sB + stage * G::B_STAGE + i * 32 * 128, &mapB, fb, 0, base + kQkv192Rows[seg + i],
+                                    ks * KA, pol_b);
+            tma_load_3d_pair_hint(sA + stage * G::A_STAGE, &mapA, fb, 0, mp * 2 * BM + (int)rank * BM, ks * KA, pol_a);
+          } else if (hints) {
             tma_load_3d_pair_hint(sA + stage * G::A_STAGE, &mapA, fb, 0, mp * 2 * BM + (int)rank * BM, ks * KA, pol_a);
             tma_load_3d_pair_hint(sB + stage * G::B_STAGE, &mapB, fb, 0, nt * BN + (int)rank * (BN / 2), ks * KA, pol_b);
           } else {
@@ -1585,10 +1618,13 @@ static bool launch_pair(const bf16* A, int lda, int a_rows, const bf16* W, int N
   using namespace tc;
   if ((mode == GEMM_SWIGLU || mode == GEMM_QKV_ROPE) && (!epi || N % BN)) return false;
   if (mode == GEMM_SWIGLU && BN != 2 * kGuGroup) return false;
-  if (mode == GEMM_QKV_ROPE && (epi->kv.head_dim != 128 || BN % 128)) return false;
+  if constexpr (BN == 192) {                        // 1.5-head QKV tiles only (RoPE pairs kept in the tile)
+    if (mode != GEMM_QKV_ROPE || KA != 1 || N % 384) return false;
+  }
+  if (mode == GEMM_QKV_ROPE && (epi->kv.head_dim != 128 || (BN % 128 && BN != 192))) return false;
   CUtensorMap ma, mb;
   if (K % (BK * KA)) return false;
-  if (!get_map(A, a_rows, K, lda, BM, &ma, KA) || !get_map(W, N, K, K, BN / 2, &mb, KA)) return false;
+  if (!get_map(A, a_rows, K, lda, BM, &ma, KA) || !get_map(W, N, K, K, BN == 192 ? 32 : BN / 2, &mb, KA)) return false;
   // one pair per unit, at most one CTA per SM (opt-in stream-K: every SM busy, units cut at pair
   // boundaries).  The grid comes from the row-count upper bound M_max (persistent pairs; pairs without a unit at the live
   // count exit): the launch must not depend on the host's row-count estimate, which only picks the
@@ -1624,6 +1660,10 @@ static bool launch_pair(const bf16* A, int lda, int a_rows, const bf16* W, int N
   // launch-specific is baked into a captured graph)
   if (split2_ok) sk |= 4 | ((split - 1) << 3);
 
+  if constexpr (BN == 192) {
+    launch_pair_k<GEMM_QKV_ROPE, BN, KA>(grid, s, ma, mb, C, ldc, N, K, M_dev, M_max, e, pf_hint, ws, sk);
+    return true;
+  }
   switch (mode) {
     case GEMM_ADD: launch_pair_k<GEMM_ADD, BN, KA>(grid, s, ma, mb, C, ldc, N, K, M_dev, M_max, e, pf_hint, ws, sk); break;
     case GEMM_SWIGLU:
@@ -1641,7 +1681,7 @@ static bool launch_pair(const bf16* A, int lda, int a_rows, const bf16* W, int N
 // the ONLY host decision that depends on the row-count estimate (grids come from M_max).  The
 // whole-step graph cache keys on these choices, so a captured graph is replayed exactly when the
 // eager sequence would launch the same kernels.
-enum { GC_SPLIT = 1, GC_128x2, GC_256x2, GC_128x1, GC_256x1, GC_SINGLE_128, GC_SINGLE_256, GC_SWAP };
+enum { GC_SPLIT = 1, GC_128x2, GC_256x2, GC_128x1, GC_256x1, GC_SINGLE_128, GC_SINGLE_256, GC_SWAP, GC_QKV192 };
 
 // swap-AB decode GEMM (see k_gemm_swap): M_max <= 256 (SWIGLU: 64) live rows, 128-aligned feature tiles,
 // and few enough tiles that a cluster of >= 2 K ranges per tile fits one wave (the LM head's ~1 200
@@ -1829,6 +1869,15 @@ int gemm_tc_choice(int N, int K, GemmMode mode, int M_max, int m_est, bool allow
     // the split decision uses the GEMM's shape only (K), never the row count, so results are batch
     // invariant
     if (mode == GEMM_ADD && ka_env == 0 && split_parts(K) >= 2) return GC_SPLIT;
+    // QKV: 192-wide (1.5-head) tiles when 256-wide tiles leave a partial wave that 192-wide ones fill
+    // better (C3 S rows: 48 -> 64 units on 74 pairs); FOCUS_GEMM_QKV192=0: off
+    static int q192 = -1;
+    if (q192 < 0) q192 = (getenv("FOCUS_GEMM_QKV192") && getenv("FOCUS_GEMM_QKV192")[0] == '0') ? 0 : 1;
+    if (q192 && mode == GEMM_QKV_ROPE && ka_env == 0 && !force256 && N % 384 == 0) {
+      const long long mpairs = (m + 2 * BM - 1) / (2 * BM), np = num_sms() / 2;
+      const long long u192 = mpairs * (N / 192);
+      if (units256 < np && u192 <= np && u192 > units256) return GC_QKV192;
+    }
     if (ka == 2 && K % (2 * BK) == 0) return narrow2 ? GC_128x2 : GC_256x2;
     return narrow2 ? GC_128x1 : GC_256x1;
   }
@@ -1854,6 +1903,7 @@ bool launch_gemm_tc(const bf16* A, int lda, int a_rows, const bf16* W, int N, in
     case GC_256x2: return launch_pair<256, 2>(A, lda, a_rows, W, N, K, C, ldc, M_dev, M_max, mode, ws, s, epi, m);
     case GC_128x1: return launch_pair<128, 1>(A, lda, a_rows, W, N, K, C, ldc, M_dev, M_max, mode, ws, s, epi, m);
     case GC_256x1: return launch_pair<256, 1>(A, lda, a_rows, W, N, K, C, ldc, M_dev, M_max, mode, ws, s, epi, m);
+    case GC_QKV192: return launch_pair<192, 1>(A, lda, a_rows, W, N, K, C, ldc, M_dev, M_max, mode, ws, s, epi, m);
     default: break;
   }
   // opt-in (FOCUS_GEMM_PAIR=0): one CTA per tile; (FOCUS_GEMM_MC=1) clusters of 4 CTAs (the 4 m-tiles
