@@ -244,6 +244,34 @@ __device__ __forceinline__ void softmax_unit(const AttnArgs& a, const Unit& xr, 
     tc_fence_before();                             // S^T is in registers: the tile may be overwritten
     __syncwarp();
     if (lane == 0) mbar_arrive(&ss.sfree[sb]);
+    if (!IMP_ONLY && t == xr.t_lo) {
+      // running-max estimate for the unit's first tile: the scores of its first valid key (one thread
+      // holds them for every row; they are handed to the row threads through red[]), instead of an exact
+      // tile max.  Correctness does not depend on it: any score above estimate + 2^8 (log2 units) still
+      // takes the exact path below.
+      const int L0 = max(0, xr.kbeg - t * KT);
+      if (L == L0) {
+#pragma unroll
+        for (int c = 0; c < NCH; ++c)
+#pragma unroll
+          for (int e = 0; e < 16; ++e) ss.red[16 * c + e] = __uint_as_float(r[c][e]);
+      }
+      named_bar(1, 128);
+      if (L < nq && L < NCH * 16) {
+        const float mv = ss.red[L] * th.sl2;
+        ss.m[L] = mv;
+        ss.nm[L] = -mv;
+        ss.thr[L] = (mv + kRescaleThresh) / th.sl2;
+      }
+      named_bar(1, 128);
+      if (L < NCH) {
+        float tm = CUDART_INF_F;
+#pragma unroll
+        for (int e = 0; e < 16; ++e) tm = fminf(tm, ss.thr[16 * L + e]);
+        ss.tmin[L] = tm;
+      }
+      named_bar(1, 128);
+    }
     // ---- (1) threshold check: against the chunk's smallest row threshold (conservative: a hit only sends
     // the tile through the exact per-row test below)
     bool need = false;
