@@ -30,9 +30,11 @@
 //               accumulator (one per unit in flight) and the row sums L^T += ONES P^T.  Two issuing
 //               threads, so a QK^T never waits behind a PV^T's dependencies
 //   warps 4-7   softmax, thread = key: online softmax in the log2 domain with a lazy running max
-//               (the max only moves when a score exceeds it by > 2^8; then a cross-warp max, O^T
-//               column rescale and sum rescale), P^T -> double-buffered smem as bf16; block-column
-//               scores -> per-CTA scratch and the Eq.2 epilogue
+//               (started from the unit's first key's scores; it only moves when a score exceeds it by
+//               > 2^8: a one-barrier vote, then a cross-warp exact max and, if a max moved, the O^T / L^T
+//               column rescale), P^T -> double-buffered smem as bf16; block-column scores -> scratch and
+//               the Eq.2 epilogue (importance-only mode: one tile per unit, scratch and a second Q
+//               buffer in the idle V ring)
 //   warps 8-11  epilogue, thread = d_h lane of O^T: O/l -> bf16 rows (or split partials + merge)
 #include <math_constants.h>
 #include <cstdio>
