@@ -201,6 +201,8 @@ struct AttnArgs {
   int pre_pf_tiles;             // key tiles of the first unit prefetched into L2 before the PDL wait
   int max_slots;                // request slots (rows of the page table)
   int debug_check;              // 1: unit-table sanity checks (trap with a message; FOCUS_ATTN_CHECK=1)
+  float rescale_log2;           // lazy softmax: the running max moves when a score exceeds it by this
+                                // (log2 units; 8 by default, FOCUS_ATTN_RESCALE_LOG2 for tests)
 };
 void launch_attention(const AttnArgs& a, cudaStream_t s);
 bool attn_tc_supported(int head_dim, int page_size, int group);

@@ -593,6 +593,10 @@ AttnArgs attn_args(focus_ctx* x, int l, const bf16* q, int ldq, int n_req, const
   a.l2_prefetch = getenv("FOCUS_ATTN_PF") ? std::max(0, atoi(getenv("FOCUS_ATTN_PF"))) : 0;   // opt-in
   a.nch_fixed = getenv("FOCUS_ATTN_NCH4") ? 1 : 0;
   a.debug_check = getenv("FOCUS_ATTN_CHECK") ? 1 : 0;
+  {
+    const char* e = getenv("FOCUS_ATTN_RESCALE_LOG2");
+    a.rescale_log2 = e ? std::max(0.0f, std::min(64.0f, (float)atof(e))) : 8.0f;
+  }
   a.page_skip = (getenv("FOCUS_ATTN_PAGESKIP") && getenv("FOCUS_ATTN_PAGESKIP")[0] == '0') ? 0 : 1;
   a.kv_hint = (getenv("FOCUS_ATTN_L2HINT") && getenv("FOCUS_ATTN_L2HINT")[0] == '0') ? 0 : 1;
   a.imp_scratch = x->attn_scratch;

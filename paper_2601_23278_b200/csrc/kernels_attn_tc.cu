@@ -54,7 +54,6 @@ constexpr int SV = 2;             // V ring slots
 constexpr int UCAP = 24;          // unit descriptors per CTA kept in smem
 constexpr int NTHREADS = 384;
 constexpr float kLog2e = 1.4426950408889634f;
-constexpr float kRescaleThresh = 8.0f;   // log2 units
 constexpr int kMaxPoolRad = 2;           // MaxPool1D kernel <= 5 (the host rejects larger)
 
 constexpr int HALF_Q = NQM * 128;               // 8 KB: one 64-column half of the Q tile
@@ -263,7 +262,7 @@ __device__ __forceinline__ void softmax_unit(const AttnArgs& a, const Unit& xr, 
         const float mv = ss.red[L] * th.sl2;
         ss.m[L] = mv;
         ss.nm[L] = -mv;
-        ss.thr[L] = (mv + kRescaleThresh) / th.sl2;
+        ss.thr[L] = (mv + a.rescale_log2) / th.sl2;
       }
       named_bar(1, 128);
       if (L < NCH) {
@@ -339,12 +338,12 @@ __device__ __forceinline__ void softmax_unit(const AttnArgs& a, const Unit& xr, 
         if (L < nq && L < NCH * 16) {
           const float mt = fmaxf(fmaxf(ss.red[L], ss.red[64 + L]), fmaxf(ss.red[128 + L], ss.red[192 + L]));
           const float mo = ss.m[L];
-          if (mt > mo + kRescaleThresh || (mo == -CUDART_INF_F && mt > -CUDART_INF_F)) {
+          if (mt > mo + a.rescale_log2 || (mo == -CUDART_INF_F && mt > -CUDART_INF_F)) {
             const float mn = fmaxf(mt, mo);
             al = ex2(mo - mn);                     // 0 when mo = -inf
             ss.m[L] = mn;
             ss.nm[L] = -mn;
-            ss.thr[L] = (mn + kRescaleThresh) / th.sl2;
+            ss.thr[L] = (mn + a.rescale_log2) / th.sl2;
             moved = true;
           }
         }

@@ -235,3 +235,13 @@ def test_layer_stages_pair_gemm_small_m(monkeypatch):
     monkeypatch.setenv("FOCUS_GEMM_SWAP", "0")
     test_layer_stages(M8B4, 16, 3, 100, (0, 1, 3), 64)
     test_layer_stages(M1P7B3, 4, 5, 70, (0, 1, 2), 64)
+
+
+def test_layer_stages_frequent_rescale(monkeypatch):
+    """Stage-wise parity with the lazy-softmax threshold cut from 2^8 to 2^0.25 (FOCUS_ATTN_RESCALE_LOG2),
+    so the running max, which starts from each unit's first key, moves on most tiles: the exact per-row
+    max and the O^T / row-sum rescale of the tensor-core attention run constantly (at the default
+    threshold they never fire on these random-weight logits)."""
+    monkeypatch.setenv("FOCUS_ATTN_RESCALE_LOG2", "0.25")
+    test_layer_stages(MINI128, 16, 3, 1100, (0, 1, 2), 16)
+    test_layer_stages(M8B4, 16, 5, 100, (0, 2), 64)
