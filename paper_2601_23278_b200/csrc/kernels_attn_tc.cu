@@ -747,10 +747,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     a.trace[((size_t)blockIdx.x * 8 + 7) * kTraceEv + 2] = gt;
   }
   if (threadIdx.x < 64) ones[threadIdx.x] = 0x3F80;   // bf16 1.0
-  // K/V rings zeroed once: boxes past a unit's last key are not loaded, so the rows they would have
-  // filled must hold finite values (P = 0 there, and 0 * finite = 0 in the PV MMA)
-  for (int i = threadIdx.x; i < (SK + SV) * KV_BYTES / 16; i += NTHREADS)
-    reinterpret_cast<uint4*>(sK)[i] = make_uint4(0, 0, 0, 0);
+  // V ring zeroed once: boxes past a unit's last key are not loaded, so the V rows they would have filled
+  // must hold finite values (P = 0 there, and 0 * finite = 0 in the PV MMA).  Stale K rows only reach
+  // S^T entries of keys outside the unit, which the softmax never reads (P = 0 is written for them).
+  for (int i = threadIdx.x; i < SV * KV_BYTES / 16; i += NTHREADS)
+    reinterpret_cast<uint4*>(sV)[i] = make_uint4(0, 0, 0, 0);
   if (threadIdx.x == 0) {
     for (int i = 0; i < SK; ++i) { mbar_init(&kfull[i], 1); mbar_init(&kempty[i], 1); }
     for (int i = 0; i < SV; ++i) { mbar_init(&vfull[i], 1); mbar_init(&vempty[i], 1); }
