@@ -158,6 +158,13 @@ __global__ void __launch_bounds__(1024) k_commit(CommitArgs a) {
         cf[t] = 1.0f / p.s;
         tk[t] = p.idx;
         jp[t] = __ldcg(&a.rowL[lo + k].j);
+        if (tk[t] < 0 || tk[t] >= a.mask_id || !(cf[t] >= 0.f)) {
+          // no valid argmax (non-finite logits): flag the step instead of committing an out-of-range id
+          // (which the next step's embedding gather would read past the table with)
+          atomicExch(&a.cnt->invariant, 1);
+          tk[t] = 0;
+          cf[t] = -CUDART_INF_F;
+        }
         a.tokconf[lo + k] = TokConf{p.idx, cf[t]};
       }
     }
@@ -180,7 +187,8 @@ __global__ void __launch_bounds__(1024) k_commit(CommitArgs a) {
         const int oj = __shfl_xor_sync(0xffffffffu, bj, off);
         if (oc > bc || (oc == bc && oj < bj)) { bc = oc; bj = oj; }
       }
-      D = 1ull << bj;
+      if (bj < 64) D = 1ull << bj;
+      else atomicExch(&a.cnt->invariant, 1);      // every confidence invalid (flagged above): decode nothing
     }
     // apply decisions (each lane its own rows)
 #pragma unroll
