@@ -24,25 +24,35 @@ __global__ void __launch_bounds__(256) k_moe_route(const float* __restrict__ z, 
   const int row = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (row >= live(M_dev, M_max)) return;
   const float* zr = z + (size_t)row * ldz;
-  unsigned taken[32] = {};                               // bit b of word w: expert 32 w + b already chosen
+  // the row's logits in registers once (lane holds experts lane + 32 i): one batch of L2 loads instead
+  // of K passes of dependent loads
+  float v[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = lane + 32 * i < E ? __ldcg(zr + lane + 32 * i) : -CUDART_INF_F;
+  unsigned taken = 0u;                                   // bit i: expert lane + 32 i already chosen
   float zk[16];
   int ek[16];
   for (int k = 0; k < K; ++k) {
     float best = -CUDART_INF_F;
-    int bi = 0x7fffffff;
-    for (int e = lane; e < E; e += 32) {
-      if ((taken[e >> 5] >> (e & 31)) & 1u) continue;
-      const float v = __ldcg(zr + e);
-      if (v > best || (v == best && e < bi)) { best = v; bi = e; }
+    int bi = 0x7fffffff, fe = 0x7fffffff;                // fe: lowest expert not yet chosen (fallback)
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      const int e = lane + 32 * i;
+      if (e < E && !((taken >> i) & 1u)) {
+        if (v[i] > best || (v[i] == best && e < bi)) { best = v[i]; bi = e; }
+        fe = min(fe, e);
+      }
     }
     for (int o = 16; o; o >>= 1) {
       const float ob = __shfl_xor_sync(0xffffffffu, best, o);
       const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      fe = min(fe, __shfl_xor_sync(0xffffffffu, fe, o));
       if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
     }
+    if (bi >= E) bi = fe;                                // no comparable logit (NaN row): lowest free expert
     zk[k] = best;
     ek[k] = bi;
-    taken[bi >> 5] |= 1u << (bi & 31);
+    if ((bi & 31) == lane) taken |= 1u << (bi >> 5);
   }
   if (lane == 0) {
     float s = 0.f;
@@ -84,9 +94,14 @@ __global__ void __launch_bounds__(256) k_moe_place(const int* __restrict__ sel, 
   for (int r0 = 0; r0 < M; r0 += 256) {
     const int r = r0 + threadIdx.x;
     int kk = -1;
-    if (r < M)
-      for (int k = 0; k < K; ++k)
-        if (__ldcg(sel + (size_t)r * K + k) == e) kk = k;   // an expert is selected at most once per row
+    if (r < M) {
+      int sk[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) sk[k] = k < K ? __ldcg(sel + (size_t)r * K + k) : -1;   // one batch of loads
+#pragma unroll
+      for (int k = 0; k < 16; ++k)
+        if (sk[k] == e) kk = k;                        // an expert is selected at most once per row
+    }
     const int flag = kk >= 0;
     const unsigned b = __ballot_sync(0xffffffffu, flag);
     if (lane == 0) wsum[warp] = __popc(b);
