@@ -40,11 +40,20 @@ __global__ void __launch_bounds__(1024) k_select_plan(SelectArgs a) {
           // partials of the chunks that hold rows (chunk-major, kv head minor), in that fixed order
           const int n_parts = ((__popcll(P) + a.attn_rpc - 1) / a.attn_rpc) * a.n_kv_heads;
           const size_t base = (size_t)i * a.n_chunks * a.n_kv_heads;
-          for (int p = 0; p < n_parts; ++p) {
-            // L2 loads: I0 was written several kernels back (layer-0 attention); under programmatic
-            // dependent launch only the immediate predecessor's writes are guaranteed through L1
-            i0 = __fadd_rn(i0, __ldcg(a.I0p + (base + p) * B + j));
-            i1 = __fadd_rn(i1, __ldcg(a.I1p + (base + p) * B + j));
+          // L2 loads: I0 was written several kernels back (layer-0 attention); under programmatic
+          // dependent launch only the immediate predecessor's writes are guaranteed through L1.  Loaded
+          // 8 partials at a time (all in flight), added in the fixed order p = 0, 1, ...
+          for (int p0 = 0; p0 < n_parts; p0 += 8) {
+            float v0[8], v1[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const bool ok = p0 + q < n_parts;
+              v0[q] = ok ? __ldcg(a.I0p + (base + p0 + q) * B + j) : 0.f;
+              v1[q] = ok ? __ldcg(a.I1p + (base + p0 + q) * B + j) : 0.f;
+            }
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              if (p0 + q < n_parts) { i0 = __fadd_rn(i0, v0[q]); i1 = __fadd_rn(i1, v1[q]); }
           }
         }
         d[t] = __fsub_rn(i1, i0);
