@@ -697,7 +697,7 @@ __device__ int build_units(const AttnArgs& a, int cta, int ncta, int* scratch, U
 template <bool IMP_ONLY>
 __global__ void __launch_bounds__(NTHREADS, 1)
     k_attn_tc(const __grid_constant__ CUtensorMap mapK, const __grid_constant__ CUtensorMap mapV,
-              const __grid_constant__ CUtensorMap mapQ, AttnArgs a) {
+              const __grid_constant__ CUtensorMap mapQ, const __grid_constant__ AttnArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* sQ = smem + OFF_Q;
@@ -1194,7 +1194,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 // Unit table of one attention launch shape (CTA b of the attention grid = block b here), computed
 // once per step instead of in the prologue of every attention launch (34 launches share the plan of
 // layers >= 2).
-__global__ void __launch_bounds__(NTHREADS) k_attn_plan(AttnArgs a) {
+__global__ void __launch_bounds__(NTHREADS) k_attn_plan(const __grid_constant__ AttnArgs a) {
   pdl_trigger();
   pdl_wait();
   __shared__ __align__(16) int scratch[4400];
