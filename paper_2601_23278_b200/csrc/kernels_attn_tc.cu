@@ -278,10 +278,14 @@ __device__ __forceinline__ void softmax_unit(const AttnArgs& a, const Unit& xr, 
     bool need = false;
     if (kvalid && !CAUSAL) {
 #pragma unroll
-      for (int c = 0; c < NCH; ++c) {
-        const float tc = ss.tmin[c];
+      for (int c = 0; c < NCH; ++c) {             // max tree of the chunk's 16 scores, one compare
+        float m8[8];
 #pragma unroll
-        for (int e = 0; e < 16; ++e) need |= __uint_as_float(r[c][e]) > tc;
+        for (int e = 0; e < 8; ++e) m8[e] = fmaxf(__uint_as_float(r[c][e]), __uint_as_float(r[c][e + 8]));
+#pragma unroll
+        for (int e = 0; e < 4; ++e) m8[e] = fmaxf(m8[e], m8[e + 4]);
+        const float mx = fmaxf(fmaxf(m8[0], m8[2]), fmaxf(m8[1], m8[3]));
+        need |= mx > ss.tmin[c];
       }
     } else if (kvalid) {
 #pragma unroll
