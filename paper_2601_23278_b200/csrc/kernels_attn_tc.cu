@@ -25,7 +25,7 @@
 //   warp 0 / 2  TMA producers: K tiles / V tiles (128 keys x 128, 128-B swizzle); 3-slot K ring (freed when
 //               QK^T completes: the K stream is bound by the TMA latency, ~3 us under full load), 2-slot V
 //               ring (freed when PV completes)
-//   warp 1      QK^T issuer (one thread) + Q loader: S^T into one of three TMEM tiles; one Q buffer
+//   warp 1      QK^T issuer (one thread) + Q loader: S^T into one of four TMEM tiles; one Q buffer
 //   warp 3      TMEM allocator + PV^T issuer (one thread): O^T += V^T P^T into a double-buffered TMEM
 //               accumulator (one per unit in flight) and the row sums L^T += ONES P^T.  Two issuing
 //               threads, so a QK^T never waits behind a PV^T's dependencies
@@ -65,9 +65,10 @@ constexpr int P_BYTES = (NQM / 8) * P_CHUNK;    // 16 KB
 constexpr int NPB = 2;                          // P^T buffers (measured: one buffer stalls the softmax on PV(g-1))
 constexpr int TMEM_COLS = 512;
 constexpr int O_COL = 0;                        // O^T buffers [0, 64), [64, 128)
-constexpr int NSB = 3;                          // S^T buffers: QK^T runs up to NSB tiles ahead of PV
-constexpr int S_COL = 2 * NQM;                  // S^T buffers [128, 192), [192, 256), [256, 320)
-constexpr int L_COL = (2 + NSB) * NQM;          // row-sum buffers [320, 384), [384, 448): ONES . P^T
+constexpr int NSB = 4;                          // S^T buffers: QK^T runs up to NSB tiles ahead of PV
+constexpr int S_COL = 2 * NQM;                  // S^T buffers [128, 192) .. [320, 384)
+constexpr int L_COL = (2 + NSB) * NQM;          // row-sum buffers (two): ONES . P^T
+static_assert(L_COL + 2 * NQM <= TMEM_COLS, "TMEM columns");
 constexpr int MAXS = 16;                        // split partials merged through smem
 constexpr int OFF_Q = 0;
 constexpr int OFF_K = OFF_Q + Q_BYTES;
