@@ -22,9 +22,8 @@
 // (deterministic).
 //
 // Persistent CTA (one per SM), 384 threads, warp-specialised:
-//   warp 0 / 2  TMA producers: K tiles / V tiles (128 keys x 128, 128-B swizzle); 3-slot K ring (freed when
-//               QK^T completes: the K stream is bound by the TMA latency, ~3 us under full load), 2-slot V
-//               ring (freed when PV completes)
+//   warp 0 / 2  TMA producers: K tiles / V tiles (128 keys x 128, 128-B swizzle); 2-slot K ring (freed when
+//               QK^T completes), 3-slot V ring (freed when PV completes)
 //   warp 1      QK^T issuer (one thread) + Q loader: S^T into one of four TMEM tiles; one Q buffer
 //   warp 3      TMEM allocator + PV^T issuer (one thread): O^T += V^T P^T into a double-buffered TMEM
 //               accumulator (one per unit in flight) and the row sums L^T += ONES P^T.  Two issuing
@@ -49,8 +48,9 @@ using namespace tc;
 constexpr int DH = 128;           // head_dim of the tensor-core path
 constexpr int KT = 128;           // keys per tile (MMA M)
 constexpr int NQM = 64;           // max query rows per unit (MMA N)
-constexpr int SK = 3;             // K ring slots (the K stream is latency-bound: slot cycle = TMA latency)
-constexpr int SV = 2;             // V ring slots
+constexpr int SK = 2;             // K ring slots (freed as soon as QK^T completes)
+constexpr int SV = 3;             // V ring slots (held from landing until PV completes; measured 2 K + 3 V > 3 K + 2 V
+                                  // once QK^T had its own issuer and four S^T buffers)
 constexpr int UCAP = 24;          // unit descriptors per CTA kept in smem
 constexpr int NTHREADS = 384;
 constexpr float kLog2e = 1.4426950408889634f;
